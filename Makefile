@@ -1,0 +1,30 @@
+# Top-level build.  Everything lands in-tree so gpurun ships it to the GPU box.
+#   paper_1503_05032_b200/libcsr5g.so   the product (sm_100a, static cudart)
+#   oracle/liboracle.so, oracle/_ref/   test infrastructure (oracle/Makefile)
+NVCC     ?= /usr/local/cuda/bin/nvcc
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+            -Xptxas -v -cudart static --expt-relaxed-constexpr
+PKG      := paper_1503_05032_b200
+SRCS     := $(wildcard $(PKG)/csrc/*.cu)
+OBJS     := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
+HDRS     := $(wildcard $(PKG)/csrc/*.cuh) include/csr5g.h
+
+.PHONY: all lib oracle clean
+all: lib oracle
+
+lib: $(PKG)/libcsr5g.so
+
+build/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -DCSR5G_BUILD -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; false)
+
+$(PKG)/libcsr5g.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC $(OBJS) -o $@
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(PKG)/libcsr5g.so
+	$(MAKE) -C oracle clean

@@ -1,0 +1,161 @@
+/*
+ * csr5g.h -- C ABI of the B200-native CSR5 SpMV library (libcsr5g.so).
+ *
+ * Drop-in boundary for the reference's hot path (namespace csr5 in
+ * /root/reference/proj/core).  Every entry point below replaces one reference
+ * interface; the citation names it.  Plain pointers and sizes only: device
+ * pointers are prefixed d_, host pointers h_; `stream` is a cudaStream_t
+ * passed as void* (NULL = the legacy default stream).
+ *
+ * Errors: every function returns a CSR5G_* status.  csr5g_last_error()
+ * returns the message of the last failure on the calling thread; for the
+ * argument errors the text is the reference's own std::invalid_argument text.
+ *
+ * There is no CPU fallback: on a host without a usable sm_100 device every
+ * compute entry point fails with CSR5G_ECUDA.
+ */
+#ifndef CSR5G_H
+#define CSR5G_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(CSR5G_BUILD)
+#define CSR5G_API __attribute__((visibility("default")))
+#else
+#define CSR5G_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSR5G_OK 0
+#define CSR5G_EINVAL 1   /* reference: std::invalid_argument */
+#define CSR5G_ERUNTIME 2 /* reference: std::runtime_error */
+#define CSR5G_ERANGE 3   /* reference: std::out_of_range / unsupported size */
+#define CSR5G_ECUDA 4    /* CUDA runtime failure (no device, launch error, ...) */
+#define CSR5G_ENOMEM 5   /* device allocation failed */
+
+#define CSR5G_MODE_DETERMINISTIC 0 /* reference SpmvMode::deterministic (spmv.hpp:16) */
+#define CSR5G_MODE_ATOMIC 1        /* reference SpmvMode::atomic */
+
+typedef struct csr5g_matrix_s *csr5g_matrix;
+
+/* Reference TuningParams (tuning.hpp:13-24).  omega must be 32 (one warp
+ * lane per tile column).  sigma = 0 selects sigma with the reference rule
+ * select_sigma(nnz/m, <r,s,t,u>) (tuning.cpp:25-34). */
+typedef struct {
+  int64_t omega, sigma, r, s, t, u;
+} csr5g_params;
+
+/* Sizes of a built handle (Csr5Matrix fields, format.hpp:130-176). */
+typedef struct {
+  int64_t m, n, nnz;            /* global matrix */
+  int64_t omega, sigma;
+  int64_t p, p_complete, tail_len; /* global tile counts */
+  int64_t tile_begin, tile_end; /* complete tiles held: [tile_begin, tile_end) */
+  int32_t has_tail;             /* this handle owns the CSR tail */
+  int32_t tile_ptr_bits, word_bits, y_offset_bits, seg_offset_bits;
+  int32_t num_sms, spmv_warps;  /* persistent SpMV grid */
+  int64_t tile_ptr_len;         /* tile_ptr words held (tiles + closing entry) */
+  int64_t empty_offset_len;     /* empty_offset entries held */
+  int64_t nnz_held;             /* col_idx/val entries held */
+  int64_t metadata_bytes;       /* tile_ptr + tile_desc at stored widths (format.hpp:171) */
+  int64_t device_bytes;         /* all device memory owned by the handle */
+  int64_t spmv_bytes;           /* algorithmic HBM bytes of one SpMV */
+  int64_t first_row, last_row;  /* rows of the first / last head held */
+  int64_t own_row_begin, own_row_end; /* rows this handle writes in y (shards) */
+  double build_ms, alloc_ms;    /* last build: total and allocation share */
+} csr5g_info;
+
+/* One boundary partial of a shard: row = -1 when there is none. */
+typedef struct {
+  int64_t row;
+  double value;
+} csr5g_partial;
+
+CSR5G_API const char *csr5g_last_error(void);
+CSR5G_API const char *csr5g_version(void);
+
+/* tuning.cpp:25-34 select_sigma (no fixed sigma). */
+CSR5G_API int csr5g_select_sigma(double nnz_per_row, int64_t r, int64_t s, int64_t t, int64_t u,
+                       int64_t *out);
+/* descriptor.cpp:22-36 make_descriptor_layout. */
+CSR5G_API int csr5g_layout(int64_t omega, int64_t sigma, int32_t *y_offset_bits, int32_t *seg_offset_bits,
+                 int32_t *word_bits);
+
+/* format.cpp:165-252 csr_to_csr5 (format.hpp:182).  Inputs are the caller's
+ * device CSR (row_ptr int64[m+1], col_idx int32[nnz], val f64[nnz]); they are
+ * only read.  The handle owns every CSR5 array.  Synchronises `stream`. */
+CSR5G_API int csr5g_build(int device, int64_t m, int64_t n, int64_t nnz, const int64_t *d_row_ptr,
+                const int32_t *d_col_idx, const double *d_val, const csr5g_params *params,
+                void *stream, csr5g_matrix *out);
+
+/* Shard build for the multi-GPU driver: holds global complete tiles
+ * [tile_begin, tile_end) (and the tail when with_tail).  d_row_ptr is the
+ * FULL global row_ptr; d_col_idx / d_val point at global position
+ * tile_begin * omega * sigma.  sigma must be explicit (global).  The held
+ * arrays equal the slices of the single-device arrays bit for bit. */
+CSR5G_API int csr5g_build_shard(int device, int64_t m, int64_t n, int64_t nnz, const int64_t *d_row_ptr,
+                      const int32_t *d_col_idx, const double *d_val, const csr5g_params *params,
+                      int64_t tile_begin, int64_t tile_end, int32_t with_tail, void *stream,
+                      csr5g_matrix *out);
+
+CSR5G_API int csr5g_info_get(csr5g_matrix h, csr5g_info *out);
+
+/* Copies the held arrays to host buffers, widened to the reference's 64-bit
+ * types (PackedWords, format.hpp:106-124; index_t vectors).  Any pointer may
+ * be NULL to skip that array.  Sizes: tile_ptr tile_ptr_len, tile_desc
+ * (tile_end-tile_begin)*omega, eo_ptr (tile_end-tile_begin)+1, eo
+ * empty_offset_len, col_idx/val nnz_held. */
+CSR5G_API int csr5g_export(csr5g_matrix h, uint64_t *h_tile_ptr, uint64_t *h_tile_desc, int64_t *h_eo_ptr,
+                 int64_t *h_eo, int64_t *h_col_idx, double *h_val);
+
+/* spmv.cpp:224-298 spmv_csr5 (spmv.hpp:58): y = A x, y fully overwritten
+ * (rows own_row_begin..own_row_end for a shard).  Stream-ordered, no sync.
+ * Not re-entrant on one handle across concurrent streams (one scratch). */
+CSR5G_API int csr5g_spmv(csr5g_matrix h, const double *d_x, double *d_y, int32_t mode, void *stream);
+
+/* Same, recording ev_tiles_begin / ev_tiles_end (from csr5g_event_create)
+ * around the dominant tile kernel, for roofline timing. */
+CSR5G_API int csr5g_spmv_evt(csr5g_matrix h, const double *d_x, double *d_y, int32_t mode, void *stream,
+                   void *ev_tiles_begin, void *ev_tiles_end);
+
+/* Shard boundary exchange.  After csr5g_spmv on a shard, d_send (device,
+ * one csr5g_partial) holds the partial of a first row this shard does not
+ * own (row = -1 if none).  The driver all-gathers every shard's record into
+ * d_all[world] and calls csr5g_fixup, which adds, in shard order, the
+ * partials of later shards whose row this shard owns. */
+CSR5G_API int csr5g_shard_send_record(csr5g_matrix h, csr5g_partial **d_send);
+/* Redirect the send record to caller device memory (e.g. this rank's slot of
+ * an all-gather buffer); NULL restores the handle's own record. */
+CSR5G_API int csr5g_set_send_buffer(csr5g_matrix h, csr5g_partial *d_send);
+CSR5G_API int csr5g_fixup(csr5g_matrix h, const csr5g_partial *d_all, int32_t world, int32_t rank,
+                double *d_y, void *stream);
+
+/* format.cpp:254-265 csr5_to_csr: undo the tile transposition into the
+ * caller's device buffers (col_idx int32[nnz_held], val f64[nnz_held]). */
+CSR5G_API int csr5g_to_csr(csr5g_matrix h, int32_t *d_col_idx, double *d_val, void *stream);
+
+/* Implicit destruction of Csr5Matrix (value type) -> explicit release. */
+CSR5G_API int csr5g_release(csr5g_matrix h);
+
+/* Timing helpers (cudaEvent with timing) for callers without a CUDA runtime. */
+CSR5G_API int csr5g_event_create(void **ev);
+CSR5G_API int csr5g_event_record(void *ev, void *stream);
+CSR5G_API int csr5g_event_elapsed_ms(void *ev_begin, void *ev_end, float *ms);
+CSR5G_API int csr5g_event_destroy(void *ev);
+
+/* Synthetic inputs on the device (bench / tests): counter-based, so the
+ * same call gives the same matrix on any GPU.  kind: 0 = 2D 5-point Laplacian
+ * (a x a grid), 1 = 3D 27-point stencil (a^3 grid).  Fills caller buffers
+ * sized by csr5g_stencil_size. */
+CSR5G_API int csr5g_stencil_size(int32_t kind, int64_t a, int64_t *m, int64_t *nnz);
+CSR5G_API int csr5g_stencil_fill(int32_t kind, int64_t a, int64_t *d_row_ptr, int32_t *d_col_idx,
+                       double *d_val, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSR5G_H */

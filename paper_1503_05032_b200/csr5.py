@@ -1,0 +1,298 @@
+"""Host-side mirror of the reference API (namespace csr5, proj/core) over the
+CUDA C ABI.  Same names, argument meaning and error behaviour:
+
+=========================  =====================================================
+reference (proj/core)      here
+=========================  =====================================================
+TuningParams               TuningParams (omega must be 32; sigma=0 -> auto rule)
+CsrMatrix                  CsrMatrix (device tensors: int64 row_ptr, int32 col_idx,
+                           float64 val)
+csr_to_csr5(a, params)     csr_to_csr5(a, params) -> Csr5Matrix (device handle)
+spmv_csr5(a5, x, y, mode)  spmv_csr5(a5, x, y=None, mode="deterministic")
+csr5_to_csr(a5)            csr5_to_csr(a5) -> CsrMatrix
+dump_format(a5, out)       dump_format(a5) -> str
+Csr5Matrix dtor            Csr5Matrix.release() (also on garbage collection)
+std::invalid_argument      ValueError (same message text)
+=========================  =====================================================
+
+torch is used only as device-memory and stream plumbing; all compute is in
+libcsr5g.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ._lib import (MODE_ATOMIC, MODE_DETERMINISTIC, Info, Params, Partial, check, lib)
+
+_MODES = {"deterministic": MODE_DETERMINISTIC, "atomic": MODE_ATOMIC,
+          MODE_DETERMINISTIC: MODE_DETERMINISTIC, MODE_ATOMIC: MODE_ATOMIC}
+
+
+@dataclass
+class TuningParams:
+    """tuning.hpp:13-24.  GPU tiles are one warp wide, so omega = 32."""
+
+    omega: int = 32
+    sigma: int = 0  # 0: select_sigma(nnz/m, <r,s,t,u>) like `spmv-bench --sigma auto`
+    r: int = 4
+    s: int = 32
+    t: int = 256
+    u: int = 4
+
+    def _c(self) -> Params:
+        return Params(self.omega, self.sigma, self.r, self.s, self.t, self.u)
+
+
+@dataclass
+class CsrMatrix:
+    """Canonical CSR on the device (csr.hpp:25-35)."""
+
+    m: int
+    n: int
+    row_ptr: torch.Tensor  # int64 [m+1]
+    col_idx: torch.Tensor  # int32 [nnz]
+    val: torch.Tensor  # float64 [nnz]
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+    @staticmethod
+    def from_host(m, n, row_ptr, col_idx, val, device="cuda") -> "CsrMatrix":
+        return CsrMatrix(
+            int(m), int(n),
+            torch.as_tensor(np.ascontiguousarray(row_ptr, dtype=np.int64)).to(device),
+            torch.as_tensor(np.ascontiguousarray(col_idx, dtype=np.int32)).to(device),
+            torch.as_tensor(np.ascontiguousarray(val, dtype=np.float64)).to(device),
+        )
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def select_sigma(nnz_per_row: float, r=4, s=32, t=256, u=4) -> int:
+    """tuning.cpp:25-34."""
+    out = C.c_int64()
+    check(lib().csr5g_select_sigma(float(nnz_per_row), r, s, t, u, C.byref(out)))
+    return out.value
+
+
+def layout(omega: int, sigma: int):
+    """descriptor.cpp:22-36 -> (y_offset_bits, seg_offset_bits, word_bits)."""
+    yb, sb, wb = C.c_int32(), C.c_int32(), C.c_int32()
+    check(lib().csr5g_layout(omega, sigma, C.byref(yb), C.byref(sb), C.byref(wb)))
+    return yb.value, sb.value, wb.value
+
+
+class Csr5Matrix:
+    """Owning handle to the device CSR5 arrays (format.hpp:130-176)."""
+
+    def __init__(self, handle: C.c_void_p, device: int):
+        self._h = handle
+        self.device = device
+        info = Info()
+        check(lib().csr5g_info_get(self._h, C.byref(info)))
+        self.info = info
+
+    # reference field names
+    def __getattr__(self, name):
+        info = self.__dict__.get("info")
+        if info is not None and name in dict(Info._fields_):
+            return getattr(info, name)
+        raise AttributeError(name)
+
+    @property
+    def handle(self) -> C.c_void_p:
+        if self._h is None:
+            raise ValueError("csr5g: matrix was released")
+        return self._h
+
+    def release(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            lib().csr5g_release(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+    def export(self) -> dict:
+        """All held arrays on the host, widened like the reference (uint64 words,
+        int64 indices)."""
+        i = self.info
+        pcs = i.tile_end - i.tile_begin
+        out = dict(
+            tile_ptr=np.zeros(i.tile_ptr_len, np.uint64),
+            tile_desc=np.zeros(pcs * i.omega, np.uint64),
+            eo_ptr=np.zeros(pcs + 1, np.int64),
+            eo=np.zeros(i.empty_offset_len, np.int64),
+            col_idx=np.zeros(i.nnz_held, np.int64),
+            val=np.zeros(i.nnz_held, np.float64),
+        )
+        check(lib().csr5g_export(self.handle, *(C.c_void_p(a.ctypes.data) for a in out.values())))
+        return out
+
+    def send_record_ptr(self) -> int:
+        p = C.c_void_p()
+        check(lib().csr5g_shard_send_record(self.handle, C.byref(p)))
+        return p.value
+
+
+def _check_csr(a: CsrMatrix):
+    for name, t, dt in (("row_ptr", a.row_ptr, torch.int64), ("col_idx", a.col_idx, torch.int32),
+                        ("val", a.val, torch.float64)):
+        if not t.is_cuda or t.dtype != dt or not t.is_contiguous():
+            raise ValueError(f"csr5g: {name} must be a contiguous CUDA {dt} tensor")
+    if a.row_ptr.numel() != a.m + 1:
+        raise ValueError(f"csr: row_ptr has size {a.row_ptr.numel()}, expected {a.m + 1}")
+
+
+def csr_to_csr5(a: CsrMatrix, params: TuningParams | None = None, stream=None) -> Csr5Matrix:
+    """format.cpp:165-252: build the tiled format on the device (input untouched)."""
+    params = params or TuningParams()
+    _check_csr(a)
+    dev = a.row_ptr.device.index or 0
+    h = C.c_void_p()
+    with torch.cuda.device(dev):
+        check(lib().csr5g_build(dev, a.m, a.n, a.nnz, a.row_ptr.data_ptr(), a.col_idx.data_ptr(),
+                                a.val.data_ptr(), C.byref(params._c()), _stream_ptr(stream),
+                                C.byref(h)))
+    return Csr5Matrix(h, dev)
+
+
+def csr_to_csr5_shard(a_row_ptr: torch.Tensor, col_slice: torch.Tensor, val_slice: torch.Tensor,
+                      m: int, n: int, nnz: int, params: TuningParams, tile_begin: int,
+                      tile_end: int, with_tail: bool, stream=None) -> Csr5Matrix:
+    """Shard of the global tile range [tile_begin, tile_end) (multi-GPU driver)."""
+    dev = a_row_ptr.device.index or 0
+    h = C.c_void_p()
+    with torch.cuda.device(dev):
+        check(lib().csr5g_build_shard(dev, m, n, nnz, a_row_ptr.data_ptr(), col_slice.data_ptr(),
+                                      val_slice.data_ptr(), C.byref(params._c()), tile_begin,
+                                      tile_end, int(with_tail), _stream_ptr(stream), C.byref(h)))
+    return Csr5Matrix(h, dev)
+
+
+def spmv_csr5(a5: Csr5Matrix, x: torch.Tensor, y: torch.Tensor | None = None,
+              mode="deterministic", stream=None) -> torch.Tensor:
+    """spmv.cpp:224-298: y = A x on the device; y is fully overwritten."""
+    if x.dim() != 1 or x.numel() != a5.n:
+        raise ValueError(f"spmv: x has length {x.numel()}, expected {a5.n}")
+    if y is None:
+        y = torch.empty(a5.m, dtype=torch.float64, device=x.device)
+    elif y.numel() != a5.m:
+        raise ValueError(f"spmv: y has length {y.numel()}, expected {a5.m}")
+    if x.dtype != torch.float64 or y.dtype != torch.float64 or not x.is_cuda or not y.is_cuda:
+        raise ValueError("spmv: x and y must be CUDA float64 tensors")
+    if mode not in _MODES:
+        raise ValueError(f"spmv: unknown mode {mode!r}")
+    with torch.cuda.device(a5.device):
+        check(lib().csr5g_spmv(a5.handle, x.data_ptr(), y.data_ptr(), _MODES[mode],
+                               _stream_ptr(stream)))
+    return y
+
+
+def spmv_host(a5: Csr5Matrix, x: np.ndarray, mode="deterministic") -> np.ndarray:
+    """Host-vector overload (spmv.hpp:60): stages x to the device and y back."""
+    xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64)).to(f"cuda:{a5.device}")
+    return spmv_csr5(a5, xd, mode=mode).cpu().numpy()
+
+
+def csr5_to_csr(a5: Csr5Matrix, row_ptr: torch.Tensor, stream=None) -> CsrMatrix:
+    """format.cpp:254-265: undo the tile transposition (row_ptr is unchanged by
+    the format, so the caller's copy is reused)."""
+    i = a5.info
+    dev = f"cuda:{a5.device}"
+    col = torch.empty(i.nnz_held, dtype=torch.int32, device=dev)
+    val = torch.empty(i.nnz_held, dtype=torch.float64, device=dev)
+    with torch.cuda.device(a5.device):
+        check(lib().csr5g_to_csr(a5.handle, col.data_ptr(), val.data_ptr(), _stream_ptr(stream)))
+    return CsrMatrix(i.m, i.n, row_ptr, col, val)
+
+
+def dump_format(a5: Csr5Matrix) -> str:
+    """format.cpp:267-305 text dump, produced from the device arrays."""
+    i = a5.info
+    ex = a5.export()
+    om, sg = i.omega, i.sigma
+    yb, sb = i.y_offset_bits, i.seg_offset_bits
+    lines = [f"csr5 m={i.m} n={i.n} nnz={i.nnz} omega={om} sigma={sg} tiles={i.p} "
+             f"complete={i.p_complete} tail={i.tail_len} tile_ptr_bits={i.tile_ptr_bits} "
+             f"desc_word_bits={i.word_bits} metadata_bytes={i.metadata_bytes} "
+             f"empty_offset_entries={i.empty_offset_len}"]
+    ntiles = i.tile_ptr_len - 1
+    for k in range(ntiles):
+        tid = i.tile_begin + k
+        raw = int(ex["tile_ptr"][k])
+        row, emp = raw & 0x7FFFFFFF, raw >> 31
+        s = f"tile {tid}: row={row} empty={emp}"
+        if tid >= i.p_complete:
+            lines.append(s + f" tail nnz={i.tail_len}")
+            continue
+        words = [int(w) for w in ex["tile_desc"][k * om:(k + 1) * om]]
+        ys = [(w >> (sb + sg)) & ((1 << yb) - 1) for w in words]
+        ss = [(w >> sg) & ((1 << sb) - 1) for w in words]
+        bfs = ["".join("1" if (w >> (sg - 1 - j)) & 1 else "0" for j in range(sg)) for w in words]
+        s += " y_offset=[" + ",".join(map(str, ys)) + "] seg_offset=[" + ",".join(map(str, ss))
+        s += "] bit_flag=[" + ",".join(bfs) + "]"
+        if emp:
+            lo, hi = int(ex["eo_ptr"][k]), int(ex["eo_ptr"][k + 1])
+            s += " empty_offset=[" + ",".join(str(int(v)) for v in ex["eo"][lo:hi]) + "]"
+        lines.append(s)
+    return "\n".join(lines) + "\n"
+
+
+def stencil(kind: int, a: int, device="cuda", stream=None) -> CsrMatrix:
+    """Synthetic 2D 5-point (kind 0) / 3D 27-point (kind 1) matrix on the device."""
+    m, nnz = C.c_int64(), C.c_int64()
+    check(lib().csr5g_stencil_size(kind, a, C.byref(m), C.byref(nnz)))
+    rp = torch.empty(m.value + 1, dtype=torch.int64, device=device)
+    ci = torch.empty(nnz.value, dtype=torch.int32, device=device)
+    va = torch.empty(nnz.value, dtype=torch.float64, device=device)
+    check(lib().csr5g_stencil_fill(kind, a, rp.data_ptr(), ci.data_ptr(), va.data_ptr(),
+                                   _stream_ptr(stream)))
+    return CsrMatrix(m.value, m.value, rp, ci, va)
+
+
+class Event:
+    """cudaEvent from libcsr5g (timing on the launching stream)."""
+
+    def __init__(self):
+        self.p = C.c_void_p()
+        check(lib().csr5g_event_create(C.byref(self.p)))
+
+    def record(self, stream=None):
+        check(lib().csr5g_event_record(self.p, _stream_ptr(stream)))
+
+    def elapsed_ms(self, end: "Event") -> float:
+        ms = C.c_float()
+        check(lib().csr5g_event_elapsed_ms(self.p, end.p, C.byref(ms)))
+        return ms.value
+
+    def __del__(self):
+        try:
+            lib().csr5g_event_destroy(self.p)
+        except Exception:
+            pass
+
+
+def spmv_csr5_evt(a5: Csr5Matrix, x: torch.Tensor, y: torch.Tensor, ev0: Event, ev1: Event,
+                  mode="deterministic", stream=None) -> torch.Tensor:
+    """spmv_csr5 recording ev0/ev1 around the tile kernel (roofline timing)."""
+    check(lib().csr5g_spmv_evt(a5.handle, x.data_ptr(), y.data_ptr(), _MODES[mode],
+                               _stream_ptr(stream), ev0.p, ev1.p))
+    return y
+
+
+__all__ = ["TuningParams", "CsrMatrix", "Csr5Matrix", "csr_to_csr5", "csr_to_csr5_shard",
+           "spmv_csr5", "spmv_host", "csr5_to_csr", "dump_format", "select_sigma", "layout",
+           "stencil", "Event", "spmv_csr5_evt", "Partial"]

@@ -1,0 +1,223 @@
+// abi.cu -- the extern "C" boundary (include/csr5g.h).  Argument checking and
+// error text follow the reference (tuning.cpp, descriptor.cpp, spmv.cpp:17-27);
+// everything else forwards to convert.cu / spmv.cu.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+namespace csr5g {
+
+namespace {
+thread_local std::string g_error;
+}
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_error = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+            ") in " + what;
+  return e == cudaErrorMemoryAllocation ? CSR5G_ENOMEM : CSR5G_ECUDA;
+}
+
+}  // namespace csr5g
+
+using namespace csr5g;
+
+struct csr5g_matrix_s {
+  Handle* h;
+};
+
+extern "C" {
+
+const char* csr5g_last_error(void) { return g_error.c_str(); }
+
+const char* csr5g_version(void) { return "csr5g 0.1 sm_100a"; }
+
+int csr5g_select_sigma(double nnz_per_row, int64_t r, int64_t s, int64_t t, int64_t u,
+                       int64_t* out) {
+  if (!out) return fail(CSR5G_EINVAL, "csr5g: out is NULL");
+  if (!(r <= s && s <= t)) return fail(CSR5G_EINVAL, "select_sigma: bounds must satisfy r <= s <= t");
+  if (nnz_per_row <= (double)r)
+    *out = r;
+  else if (nnz_per_row <= (double)s)
+    *out = (int64_t)std::llround(nnz_per_row);
+  else if (nnz_per_row <= (double)t)
+    *out = s;
+  else
+    *out = u;
+  return CSR5G_OK;
+}
+
+int csr5g_layout(int64_t omega, int64_t sigma, int32_t* yb, int32_t* sb, int32_t* wb) {
+  if (omega < 1 || sigma < 1)
+    return fail(CSR5G_EINVAL, "descriptor layout: omega and sigma must be >= 1");
+  auto ceil_log2 = [](int64_t v) {
+    const uint64_t x = (uint64_t)v - 1;
+    return x ? 64 - __builtin_clzll(x) : 0;
+  };
+  const int y = ceil_log2(omega * sigma), s = ceil_log2(omega);
+  const int64_t total = y + s + sigma;
+  if (total > 64)
+    return fail(CSR5G_EINVAL, "descriptor layout: " + std::to_string(total) +
+                                  " bits per column exceed a 64-bit word; choose a smaller sigma");
+  if (yb) *yb = y;
+  if (sb) *sb = s;
+  if (wb) *wb = total <= 32 ? 32 : 64;
+  return CSR5G_OK;
+}
+
+static int wrap_build(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* rp,
+                      const int32_t* ci, const double* va, const csr5g_params* params, int64_t tb,
+                      int64_t te, bool shard, int with_tail, void* stream, csr5g_matrix* out) {
+  if (!out) return fail(CSR5G_EINVAL, "csr5g: out is NULL");
+  *out = nullptr;
+  Handle* h = nullptr;
+  const int rc = build_handle(device, m, n, nnz, rp, ci, va, params, tb, te, shard, with_tail,
+                              static_cast<cudaStream_t>(stream), &h);
+  if (rc) return rc;
+  *out = new csr5g_matrix_s{h};
+  return CSR5G_OK;
+}
+
+int csr5g_build(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d_row_ptr,
+                const int32_t* d_col_idx, const double* d_val, const csr5g_params* params,
+                void* stream, csr5g_matrix* out) {
+  return wrap_build(device, m, n, nnz, d_row_ptr, d_col_idx, d_val, params, 0, 0, false, 0, stream,
+                    out);
+}
+
+int csr5g_build_shard(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d_row_ptr,
+                      const int32_t* d_col_idx, const double* d_val, const csr5g_params* params,
+                      int64_t tile_begin, int64_t tile_end, int32_t with_tail, void* stream,
+                      csr5g_matrix* out) {
+  return wrap_build(device, m, n, nnz, d_row_ptr, d_col_idx, d_val, params, tile_begin, tile_end,
+                    true, with_tail, stream, out);
+}
+
+int csr5g_info_get(csr5g_matrix h, csr5g_info* out) {
+  if (!h || !out) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
+  *out = h->h->info;
+  return CSR5G_OK;
+}
+
+int csr5g_export(csr5g_matrix hm, uint64_t* h_tile_ptr, uint64_t* h_tile_desc, int64_t* h_eo_ptr,
+                 int64_t* h_eo, int64_t* h_col_idx, double* h_val) {
+  if (!hm) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
+  Handle* h = hm->h;
+  CSR5G_CUDA(cudaSetDevice(h->device));
+  CSR5G_CUDA(cudaDeviceSynchronize());
+  const csr5g_info& in = h->info;
+  const int64_t pcs = h->pcs;
+  if (h_tile_ptr) {
+    CSR5G_CUDA(cudaMemcpy(h_tile_ptr, h->tile_ptr, sizeof(uint32_t) * in.tile_ptr_len,
+                          cudaMemcpyDeviceToHost));
+    auto* w32 = reinterpret_cast<uint32_t*>(h_tile_ptr);
+    for (int64_t i = in.tile_ptr_len - 1; i >= 0; --i) h_tile_ptr[i] = w32[i];
+  }
+  if (h_tile_desc) {
+    const int64_t cnt = pcs * kOmega;
+    if (h->wide) {
+      CSR5G_CUDA(cudaMemcpy(h_tile_desc, h->desc, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost));
+    } else {
+      CSR5G_CUDA(cudaMemcpy(h_tile_desc, h->desc, sizeof(uint32_t) * cnt, cudaMemcpyDeviceToHost));
+      auto* w32 = reinterpret_cast<uint32_t*>(h_tile_desc);
+      for (int64_t i = cnt - 1; i >= 0; --i) h_tile_desc[i] = w32[i];
+    }
+  }
+  if (h_eo_ptr)
+    CSR5G_CUDA(cudaMemcpy(h_eo_ptr, h->eo_ptr, sizeof(int64_t) * (pcs + 1), cudaMemcpyDeviceToHost));
+  if (h_eo) {
+    CSR5G_CUDA(cudaMemcpy(h_eo, h->eo, sizeof(int32_t) * in.empty_offset_len, cudaMemcpyDeviceToHost));
+    auto* w32 = reinterpret_cast<int32_t*>(h_eo);
+    for (int64_t i = in.empty_offset_len - 1; i >= 0; --i) h_eo[i] = w32[i];
+  }
+  if (h_col_idx) {
+    CSR5G_CUDA(cudaMemcpy(h_col_idx, h->col, sizeof(int32_t) * in.nnz_held, cudaMemcpyDeviceToHost));
+    auto* w32 = reinterpret_cast<int32_t*>(h_col_idx);
+    for (int64_t i = in.nnz_held - 1; i >= 0; --i) h_col_idx[i] = w32[i];
+  }
+  if (h_val)
+    CSR5G_CUDA(cudaMemcpy(h_val, h->val, sizeof(double) * in.nnz_held, cudaMemcpyDeviceToHost));
+  return CSR5G_OK;
+}
+
+int csr5g_spmv(csr5g_matrix h, const double* d_x, double* d_y, int32_t mode, void* stream) {
+  return csr5g_spmv_evt(h, d_x, d_y, mode, stream, nullptr, nullptr);
+}
+
+int csr5g_spmv_evt(csr5g_matrix h, const double* d_x, double* d_y, int32_t mode, void* stream,
+                   void* ev0, void* ev1) {
+  if (!h) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
+  if (mode != CSR5G_MODE_DETERMINISTIC && mode != CSR5G_MODE_ATOMIC)
+    return fail(CSR5G_EINVAL, "csr5g: unknown spmv mode " + std::to_string(mode));
+  if (h->h->info.m > 0 && !d_y) return fail(CSR5G_EINVAL, "spmv: y is NULL");
+  if (h->h->info.n > 0 && !d_x) return fail(CSR5G_EINVAL, "spmv: x is NULL");
+  return launch_spmv(h->h, d_x, d_y, mode, static_cast<cudaStream_t>(stream),
+                     static_cast<cudaEvent_t>(ev0), static_cast<cudaEvent_t>(ev1));
+}
+
+int csr5g_shard_send_record(csr5g_matrix h, csr5g_partial** d_send) {
+  if (!h || !d_send) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  *d_send = h->h->send;
+  return CSR5G_OK;
+}
+
+int csr5g_set_send_buffer(csr5g_matrix h, csr5g_partial* d_send) {
+  if (!h) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
+  h->h->send_ext = d_send;
+  return CSR5G_OK;
+}
+
+int csr5g_fixup(csr5g_matrix h, const csr5g_partial* d_all, int32_t world, int32_t rank,
+                double* d_y, void* stream) {
+  if (!h || !d_all || !d_y) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  if (rank < 0 || rank >= world) return fail(CSR5G_EINVAL, "csr5g: rank outside [0, world)");
+  return launch_fixup(h->h, d_all, world, rank, d_y, static_cast<cudaStream_t>(stream));
+}
+
+int csr5g_to_csr(csr5g_matrix h, int32_t* d_col_idx, double* d_val, void* stream) {
+  if (!h) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
+  if (h->h->info.nnz_held > 0 && (!d_col_idx || !d_val))
+    return fail(CSR5G_EINVAL, "csr5g: NULL output");
+  return launch_to_csr(h->h, d_col_idx, d_val, static_cast<cudaStream_t>(stream));
+}
+
+int csr5g_release(csr5g_matrix h) {
+  if (!h) return CSR5G_OK;
+  free_handle(h->h);
+  delete h;
+  return CSR5G_OK;
+}
+
+int csr5g_event_create(void** ev) {
+  if (!ev) return fail(CSR5G_EINVAL, "csr5g: NULL event");
+  cudaEvent_t e;
+  CSR5G_CUDA(cudaEventCreate(&e));
+  *ev = e;
+  return CSR5G_OK;
+}
+
+int csr5g_event_record(void* ev, void* stream) {
+  CSR5G_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream)));
+  return CSR5G_OK;
+}
+
+int csr5g_event_elapsed_ms(void* a, void* b, float* ms) {
+  CSR5G_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(b)));
+  CSR5G_CUDA(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(a), static_cast<cudaEvent_t>(b)));
+  return CSR5G_OK;
+}
+
+int csr5g_event_destroy(void* ev) {
+  CSR5G_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(ev)));
+  return CSR5G_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,535 @@
+// convert.cu -- CSR -> CSR5 on the device (reference: format.cpp:165-252).
+//
+// Five kernels, all bit-exact with the reference arrays:
+//   k_rowscan        one pass over row_ptr: empty-row bitmap + head bitmap over
+//                    nonzero positions (the row_ptr walk of format.cpp:93-97)
+//   k_tile_ptr       thread per tile boundary: upper_bound + bounded empty-row
+//                    check over the bitmap (format.cpp:52-82)
+//   k_desc_transpose warp per tile, lane = column: popc / warp scan -> y_offset,
+//                    ballot / ffs -> seg_offset, pack (format.cpp:84-121,
+//                    descriptor.cpp:38-62); then the tile transpose of col/val
+//                    through padded shared memory (format.cpp:226-249)
+//   (CUB exclusive scan of per-tile head counts -> empty_offset_ptr)
+//   k_eo             warp per flagged tile: row offsets of its heads
+//                    (format.cpp:123-136, 213-224)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <new>
+
+#include "internal.cuh"
+
+namespace csr5g {
+namespace {
+
+__global__ void k_rowscan(const int64_t* __restrict__ rp, int64_t m, int64_t pos_begin,
+                          int64_t pos_end, uint32_t* __restrict__ empty_bits,
+                          uint32_t* __restrict__ head_bits) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool inr = r < m;
+  int64_t lo = 0, hi = 0;
+  if (inr) {
+    lo = rp[r];
+    hi = rp[r + 1];
+  }
+  const uint32_t em = __ballot_sync(kFull, inr && lo == hi);
+  if (lane == 0 && r < m) empty_bits[r >> 5] = em;
+  // Head bit at row_ptr[r]; rows are sorted, so lanes sharing a bitmap word
+  // are contiguous: OR them together and issue one atomic per word group.
+  const bool valid = inr && lo >= pos_begin && lo < pos_end;
+  const int64_t local = lo - pos_begin;
+  const int64_t word = valid ? (local >> 5) : (-1 - (int64_t)lane);
+  uint32_t bits = valid ? (1u << (local & 31)) : 0u;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t ob = __shfl_down_sync(kFull, bits, d);
+    const int64_t ow = __shfl_down_sync(kFull, word, d);
+    if (lane + d < 32 && ow == word) bits |= ob;
+  }
+  const int64_t pw = __shfl_up_sync(kFull, word, 1);
+  if (valid && (lane == 0 || pw != word)) atomicOr(&head_bits[word], bits);
+}
+
+// tile_ptr entries for global tiles [t_first, t_first + count).
+__global__ void k_tile_ptr(const int64_t* __restrict__ rp, int64_t m, int64_t B, int64_t p,
+                           int64_t t_first, int64_t count,
+                           const uint32_t* __restrict__ empty_bits, uint32_t* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= count) return;
+  const int64_t t = t_first + idx;
+  const int64_t row = row_of_nonzero_dev(rp, m, t * B);
+  bool flag = false;
+  if (t < p) {
+    const int64_t next = row_of_nonzero_dev(rp, m, (t + 1) * B);
+    // Rows strictly inside (row, next) that are non-empty each own one of the
+    // tile's B nonzeros, so a longer range must contain an empty row.
+    if (next - row - 1 >= B) {
+      flag = true;
+    } else {
+      // inclusive right endpoint, rid < m (format.cpp:65-78)
+      const int64_t hi = next < m - 1 ? next : m - 1;
+      for (int64_t wd = row >> 5; wd <= (hi >> 5) && !flag; ++wd) {
+        uint32_t bits = empty_bits[wd];
+        const int64_t lo_bit = wd * 32, hi_bit = lo_bit + 31;
+        if (row > lo_bit) bits &= ~0u << (row - lo_bit);
+        if (hi < hi_bit) bits &= ~0u >> (hi_bit - hi);
+        flag = bits != 0;
+      }
+    }
+  }
+  out[idx] = (uint32_t)row | (flag ? 0x80000000u : 0u);
+}
+
+// sigma head bits of column `lane` of local tile k, bit j = depth j.
+__device__ __forceinline__ uint64_t column_bits(const uint32_t* __restrict__ head_bits, int64_t k,
+                                                int B, int sigma, int lane) {
+  const int64_t pos = k * B + (int64_t)lane * sigma;
+  const int64_t w0 = pos >> 5;
+  const int o = (int)(pos & 31);
+  uint64_t bits = ((uint64_t)head_bits[w0] | ((uint64_t)head_bits[w0 + 1] << 32)) >> o;
+  if (o) bits |= (uint64_t)head_bits[w0 + 2] << (64 - o);
+  bits &= (1ull << sigma) - 1;  // sigma <= 48
+  if (lane == 0) bits |= 1ull;  // bf[0] = 1, format.cpp:98
+  return bits;
+}
+
+template <typename W>
+__global__ void __launch_bounds__(128) k_desc_transpose(
+    const uint32_t* __restrict__ head_bits, const uint32_t* __restrict__ tile_ptr,
+    const int32_t* __restrict__ col_in, const double* __restrict__ val_in,
+    int32_t* __restrict__ col_out, double* __restrict__ val_out, W* __restrict__ desc,
+    int64_t* __restrict__ eo_cnt, int64_t pcs, int sigma) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t k = (int64_t)blockIdx.x * 4 + wib;
+  if (k >= pcs) return;
+  const int B = 32 * sigma;
+
+  // ---- descriptor (format.cpp:102-121 + descriptor.cpp:38-62) ----
+  const uint64_t bits = column_bits(head_bits, k, B, sigma, lane);
+  const int cnt = __popcll(bits);
+  int incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int t = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += t;
+  }
+  const int yoff = incl - cnt;
+  const int H = __shfl_sync(kFull, incl, 31);
+  const uint32_t hb = __ballot_sync(kFull, cnt > 0);
+  const uint64_t above = (uint64_t)hb >> (lane + 1);
+  const int seg = cnt ? (above ? __ffsll((long long)above) - 1 : 31 - lane) : 0;
+  const uint64_t flags = __brevll(bits) >> (64 - sigma);  // depth j at bit sigma-1-j
+  desc[k * 32 + lane] =
+      (W)(((uint64_t)yoff << (kSegBits + sigma)) | ((uint64_t)seg << sigma) | flags);
+  if (lane == 0) eo_cnt[k] = (tile_ptr[k] >> 31) ? H : 0;
+
+  // ---- transpose: logical i*sigma+j -> physical j*32+i (format.hpp:76-88) ----
+  const uint64_t pol = policy_evict_first();
+  double* buf = smem + (size_t)wib * sigma * 33;
+  const float inv = 1.0f / (float)sigma;
+  const int64_t tb = k * B;
+  for (int e = lane; e < B; e += 32) {
+    const double v = ld_stream(val_in + tb + e, pol);
+    const int i = __float2int_rz(((float)e + 0.5f) * inv);
+    buf[(e - i * sigma) * 33 + i] = v;
+  }
+  __syncwarp();
+  for (int j = 0; j < sigma; ++j) val_out[tb + j * 32 + lane] = buf[j * 33 + lane];
+  __syncwarp();
+  int32_t* ib = reinterpret_cast<int32_t*>(buf);
+  for (int e = lane; e < B; e += 32) {
+    const int32_t c = ld_stream(col_in + tb + e, pol);
+    const int i = __float2int_rz(((float)e + 0.5f) * inv);
+    ib[(e - i * sigma) * 33 + i] = c;
+  }
+  __syncwarp();
+  for (int j = 0; j < sigma; ++j) col_out[tb + j * 32 + lane] = ib[j * 33 + lane];
+}
+
+// empty_offset entries of flagged tiles (format.cpp:123-136): for every head
+// in column-major order, row_of_nonzero(g) - tile_row.
+__global__ void k_eo(const uint32_t* __restrict__ head_bits, const uint32_t* __restrict__ tile_ptr,
+                     const int64_t* __restrict__ rp, int64_t m, int64_t pcs, int sigma,
+                     int64_t pos0, const int64_t* __restrict__ eo_ptr, int32_t* __restrict__ eo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (k >= pcs) return;
+  const uint32_t tp = tile_ptr[k];
+  if (!(tp >> 31)) return;
+  const int B = 32 * sigma;
+  const int64_t tile_row = tp & 0x7fffffffu;
+  const int64_t next_row = tile_ptr[k + 1] & 0x7fffffffu;
+  uint64_t bits = column_bits(head_bits, k, B, sigma, lane);
+  const int cnt = __popcll(bits);
+  int incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int t = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += t;
+  }
+  int64_t out = eo_ptr[k] + (incl - cnt);
+  const int64_t hi = (next_row + 2 < m + 1) ? next_row + 2 : m + 1;
+  while (bits) {
+    const int j = __ffsll((long long)bits) - 1;
+    bits &= bits - 1;
+    const int64_t g = pos0 + k * B + (int64_t)lane * sigma + j;
+    const int64_t row = upper_bound_dev(rp, tile_row + 1, hi, g) - 1;
+    eo[out++] = (int32_t)(row - tile_row);
+  }
+}
+
+// A few scalars of the held range, one thread: row_of_nonzero at two positions
+// and row_ptr at two rows (negative query = skip).
+__global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0, int64_t g1,
+                          int64_t r0, int64_t r1, int64_t* __restrict__ out) {
+  out[0] = g0 >= 0 ? row_of_nonzero_dev(rp, m, g0) : -1;
+  out[1] = g1 >= 0 ? row_of_nonzero_dev(rp, m, g1) : -1;
+  out[2] = (r0 >= 0 && r0 <= m) ? rp[r0] : -1;
+  out[3] = (r1 >= 0 && r1 <= m) ? rp[r1] : -1;
+}
+
+__global__ void k_untranspose(const int32_t* __restrict__ col_in, const double* __restrict__ val_in,
+                              int32_t* __restrict__ col_out, double* __restrict__ val_out,
+                              int64_t n_tiled, int sigma) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_tiled) return;
+  const int B = 32 * sigma;
+  const int64_t k = idx / B;
+  const int rem = (int)(idx - k * B);
+  const int i = rem / sigma, j = rem - (rem / sigma) * sigma;
+  const int64_t src = k * B + (int64_t)j * 32 + i;
+  col_out[idx] = col_in[src];
+  val_out[idx] = val_in[src];
+}
+
+template <typename T>
+int dev_alloc(T** p, size_t count, double* alloc_ms, int64_t* bytes) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const size_t nb = std::max<size_t>(count * sizeof(T), 16);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), nb);
+  *alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CSR5G_ENOMEM, "csr5g: device allocation of " + std::to_string(nb) +
+                                  " bytes failed: " + cudaGetErrorString(e));
+  }
+  *bytes += (int64_t)nb;
+  return CSR5G_OK;
+}
+
+int check_params(const csr5g_params* pr, int64_t m, int64_t nnz, bool shard, int64_t* sigma_out,
+                 int32_t* yb, int32_t* sb, int32_t* wb) {
+  if (!pr) return fail(CSR5G_EINVAL, "csr5g: params is NULL");
+  int64_t sigma = pr->sigma;
+  if (sigma == 0) {
+    if (shard) return fail(CSR5G_EINVAL, "csr5g: a shard build needs the global sigma");
+    const int rc = csr5g_select_sigma(m > 0 ? (double)nnz / (double)m : 0.0, pr->r, pr->s, pr->t,
+                                      pr->u, &sigma);
+    if (rc) return rc;
+  }
+  // tuning.cpp:8-15
+  if (pr->omega < 1 || sigma < 1) return fail(CSR5G_EINVAL, "tuning: omega and sigma must be >= 1");
+  if (pr->omega * sigma < 2)
+    return fail(CSR5G_EINVAL,
+                "tuning: omega * sigma must be >= 2; a tile needs at least two entries for "
+                "segmentation");
+  if (!(pr->r <= pr->s && pr->s <= pr->t))
+    return fail(CSR5G_EINVAL, "tuning: bounds must satisfy r <= s <= t");
+  if (pr->u < 1) return fail(CSR5G_EINVAL, "tuning: u must be >= 1");
+  if (pr->omega != kOmega)
+    return fail(CSR5G_EINVAL,
+                "csr5g: omega must be 32 on the GPU path (one warp lane per tile column), got " +
+                    std::to_string(pr->omega));
+  const int rc = csr5g_layout(pr->omega, sigma, yb, sb, wb);
+  if (rc) return rc;
+  *sigma_out = sigma;
+  return CSR5G_OK;
+}
+
+}  // namespace
+
+void free_handle(Handle* h) {
+  if (!h) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  cudaFree(h->row_ptr);
+  cudaFree(h->tile_ptr);
+  cudaFree(h->desc);
+  cudaFree(h->eo_ptr);
+  cudaFree(h->eo);
+  cudaFree(h->col);
+  cudaFree(h->val);
+  cudaFree(h->item_row);
+  cudaFree(h->item_val);
+  cudaFree(h->send);
+  cudaSetDevice(prev);
+  delete h;
+}
+
+int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d_row_ptr,
+                 const int32_t* d_col_idx, const double* d_val, const csr5g_params* params,
+                 int64_t tile_begin, int64_t tile_end, bool shard, int with_tail,
+                 cudaStream_t stream, Handle** out) {
+  const auto wall0 = std::chrono::steady_clock::now();
+  if (!out) return fail(CSR5G_EINVAL, "csr5g: out is NULL");
+  *out = nullptr;
+  if (m < 0 || n < 0 || nnz < 0) return fail(CSR5G_EINVAL, "csr: negative dimension");
+  if (m >= (int64_t(1) << 31))
+    return fail(CSR5G_ERANGE, "csr5g: m >= 2^31 rows needs 64-bit tile pointers (unsupported)");
+  if (n >= (int64_t(1) << 31))
+    return fail(CSR5G_ERANGE, "csr5g: n >= 2^31 columns does not fit the int32 col_idx");
+  if (m > 0 && !d_row_ptr) return fail(CSR5G_EINVAL, "csr5g: row_ptr is NULL");
+  int64_t sigma = 0;
+  int32_t yb = 0, sb = 0, wb = 0;
+  int rc = check_params(params, m, nnz, shard, &sigma, &yb, &sb, &wb);
+  if (rc) return rc;
+  int ndev = 0;
+  CSR5G_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(CSR5G_ECUDA, "csr5g: no such CUDA device");
+  CSR5G_CUDA(cudaSetDevice(device));
+  int major = 0;
+  CSR5G_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major < 10) return fail(CSR5G_ECUDA, "csr5g: built for sm_100a; device is older");
+
+  const int64_t B = kOmega * sigma;
+  const int64_t p = (nnz + B - 1) / B, pc = nnz / B, tail = nnz % B;
+  if (!shard) {
+    tile_begin = 0;
+    tile_end = pc;
+    with_tail = tail > 0;
+  }
+  if (tile_begin < 0 || tile_end < tile_begin || tile_end > pc)
+    return fail(CSR5G_EINVAL, "csr5g: shard tile range outside [0, p_complete]");
+  const bool is_last = tile_end == pc;
+  if ((with_tail != 0) != (is_last && tail > 0))
+    return fail(CSR5G_EINVAL, "csr5g: the shard ending at p_complete must hold the tail");
+  const int64_t pcs = tile_end - tile_begin;
+  const int64_t nnz_held = pcs * B + (is_last ? tail : 0);
+  if (nnz_held > 0 && (!d_col_idx || !d_val)) return fail(CSR5G_EINVAL, "csr5g: col_idx/val is NULL");
+  const int64_t last_ptr = is_last ? p : tile_end;
+  const int64_t tile_ptr_len = m > 0 ? last_ptr - tile_begin + 1 : 1;
+
+  auto* h = new (std::nothrow) Handle();
+  if (!h) return fail(CSR5G_ENOMEM, "csr5g: host allocation failed");
+  h->device = device;
+  h->wide = wb == 64;
+  h->pcs = pcs;
+  h->t0 = tile_begin;
+  h->B = B;
+  h->is_last = is_last;
+  double alloc_ms = 0.0;
+  int64_t bytes = 0;
+  uint32_t *head_bits = nullptr, *empty_bits = nullptr;
+  int64_t* eo_cnt = nullptr;
+  int64_t* scal = nullptr;
+  void* cub_tmp = nullptr;
+  auto cleanup = [&](int code) {
+    cudaFree(head_bits);
+    cudaFree(empty_bits);
+    cudaFree(eo_cnt);
+    cudaFree(scal);
+    cudaFree(cub_tmp);
+    if (code) free_handle(h);
+    return code;
+  };
+#define TRY(x)                  \
+  do {                          \
+    int rc_ = (x);              \
+    if (rc_) return cleanup(rc_); \
+  } while (0)
+#define TRYC(x)                                            \
+  do {                                                     \
+    cudaError_t e_ = (x);                                  \
+    if (e_ != cudaSuccess) return cleanup(cuda_fail(e_, #x)); \
+  } while (0)
+
+  const size_t wbytes = h->wide ? 8 : 4;
+  TRY(dev_alloc(&h->row_ptr, (size_t)m + 1, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->tile_ptr, (size_t)tile_ptr_len, &alloc_ms, &bytes));
+  TRY(dev_alloc(reinterpret_cast<char**>(&h->desc), (size_t)pcs * kOmega * wbytes, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->eo_ptr, (size_t)pcs + 1, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->col, (size_t)nnz_held, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->val, (size_t)nnz_held, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->send, 1, &alloc_ms, &bytes));
+  int64_t tmp_bytes = 0;
+  const int64_t head_words = (pcs * B + 31) / 32 + 3;
+  const int64_t empty_words = (m + 31) / 32 + 1;
+  TRY(dev_alloc(&head_bits, (size_t)head_words, &alloc_ms, &tmp_bytes));
+  TRY(dev_alloc(&empty_bits, (size_t)empty_words, &alloc_ms, &tmp_bytes));
+  TRY(dev_alloc(&eo_cnt, (size_t)pcs + 1, &alloc_ms, &tmp_bytes));
+  TRY(dev_alloc(&scal, 8, &alloc_ms, &tmp_bytes));
+
+  if (m > 0) TRYC(cudaMemcpyAsync(h->row_ptr, d_row_ptr, sizeof(int64_t) * (m + 1),
+                                  cudaMemcpyDeviceToDevice, stream));
+  TRYC(cudaMemsetAsync(head_bits, 0, sizeof(uint32_t) * head_words, stream));
+  TRYC(cudaMemsetAsync(empty_bits, 0, sizeof(uint32_t) * empty_words, stream));
+  TRYC(cudaMemsetAsync(eo_cnt, 0, sizeof(int64_t) * (pcs + 1), stream));
+  const csr5g_partial none{-1, 0.0};
+  TRYC(cudaMemcpyAsync(h->send, &none, sizeof none, cudaMemcpyHostToDevice, stream));
+
+  const int64_t pos0 = tile_begin * B;
+  if (m > 0) {
+    k_rowscan<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(h->row_ptr, m, pos0, pos0 + pcs * B,
+                                                               empty_bits, head_bits);
+    TRYC(cudaGetLastError());
+    k_tile_ptr<<<(unsigned)((tile_ptr_len + 255) / 256), 256, 0, stream>>>(
+        h->row_ptr, m, B, p, tile_begin, tile_ptr_len, empty_bits, h->tile_ptr);
+    TRYC(cudaGetLastError());
+  } else {
+    TRYC(cudaMemsetAsync(h->tile_ptr, 0, sizeof(uint32_t), stream));  // encode_tile_ptr(0)
+  }
+  if (pcs > 0) {
+    const size_t smem = (size_t)4 * sigma * 33 * sizeof(double);
+    const unsigned grid = (unsigned)((pcs + 3) / 4);
+    if (h->wide) {
+      TRYC(cudaFuncSetAttribute(k_desc_transpose<uint64_t>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_desc_transpose<uint64_t><<<grid, 128, smem, stream>>>(
+          head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint64_t*)h->desc, eo_cnt,
+          pcs, (int)sigma);
+    } else {
+      TRYC(cudaFuncSetAttribute(k_desc_transpose<uint32_t>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_desc_transpose<uint32_t><<<grid, 128, smem, stream>>>(
+          head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint32_t*)h->desc, eo_cnt,
+          pcs, (int)sigma);
+    }
+    TRYC(cudaGetLastError());
+  }
+  if (is_last && tail > 0) {
+    TRYC(cudaMemcpyAsync(h->col + pcs * B, d_col_idx + pcs * B, sizeof(int32_t) * tail,
+                         cudaMemcpyDeviceToDevice, stream));
+    TRYC(cudaMemcpyAsync(h->val + pcs * B, d_val + pcs * B, sizeof(double) * tail,
+                         cudaMemcpyDeviceToDevice, stream));
+  }
+  // empty_offset_ptr: exclusive scan of per-tile head counts (format.cpp:213-217)
+  size_t cub_bytes = 0;
+  TRYC(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, eo_cnt, h->eo_ptr, (int)(pcs + 1), stream));
+  TRY(dev_alloc(reinterpret_cast<char**>(&cub_tmp), cub_bytes, &alloc_ms, &tmp_bytes));
+  TRYC(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, eo_cnt, h->eo_ptr, (int)(pcs + 1), stream));
+
+  // Scalars of the held range.
+  int64_t ptr_first = 0, ptr_close = 0, eo_total = 0;
+  TRYC(cudaMemcpyAsync(&eo_total, h->eo_ptr + pcs, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  uint32_t tp0 = 0, tpc = 0;
+  TRYC(cudaMemcpyAsync(&tp0, h->tile_ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+  TRYC(cudaMemcpyAsync(&tpc, h->tile_ptr + (pcs < tile_ptr_len ? pcs : tile_ptr_len - 1),
+                       sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+  TRYC(cudaStreamSynchronize(stream));
+  ptr_first = tp0 & 0x7fffffffu;
+  ptr_close = tpc & 0x7fffffffu;
+  // queries: g0 = last position of the held complete tiles, g1 = nnz - 1;
+  // r0 = row_ptr[first row], r1 = row_ptr[closing row]
+  const int64_t g0 = pcs > 0 ? tile_end * B - 1 : -1;
+  const int64_t g1 = nnz > 0 ? nnz - 1 : -1;
+  if (m > 0) {
+    k_scalars<<<1, 1, 0, stream>>>(h->row_ptr, m, g0, g1, ptr_first, ptr_close, scal);
+    TRYC(cudaGetLastError());
+  }
+  int64_t sv[4] = {-1, -1, -1, -1};
+  if (m > 0) TRYC(cudaMemcpyAsync(sv, scal, sizeof sv, cudaMemcpyDeviceToHost, stream));
+  TRY(dev_alloc(&h->eo, (size_t)eo_total, &alloc_ms, &bytes));
+  if (pcs > 0 && eo_total > 0) {
+    const int64_t threads = pcs * 32;
+    k_eo<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(
+        head_bits, h->tile_ptr, h->row_ptr, m, pcs, (int)sigma, pos0, h->eo_ptr, h->eo);
+    TRYC(cudaGetLastError());
+  }
+  TRYC(cudaStreamSynchronize(stream));
+
+  // ---- SpMV plan ----
+  const bool is_first = tile_begin == 0;
+  h->first_row = ptr_first;
+  h->first_owned = is_first || sv[2] >= pos0;
+  h->last_row = pcs > 0 ? sv[0] : ptr_first;
+  if (is_last) {
+    h->tail_row_begin = tail > 0 ? ptr_close : (nnz > 0 ? sv[1] + 1 : 0);
+    h->next_row_after = h->tail_row_begin;
+  } else {
+    h->tail_row_begin = m;
+    h->next_row_after = ptr_close;
+  }
+  h->lead_rows = (is_first && nnz > 0) ? ptr_first : 0;
+  h->tail_pos = pc * B;
+  h->has_tail_item = is_last && tail > 0;
+  int sms = 0, bps = 0;
+  TRYC(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  TRY(spmv_occupancy(h->wide, &bps));
+  const int64_t max_warps = (int64_t)sms * bps * kSpmvWarpsPerBlock;
+  h->nwarps = (int)std::min<int64_t>(max_warps, pcs);
+  h->tile_blocks = (h->nwarps + kSpmvWarpsPerBlock - 1) / kSpmvWarpsPerBlock;
+  const int64_t rows_total = h->lead_rows + (m - h->tail_row_begin);
+  h->rows_blocks = rows_total > 0 ? (int)std::min<int64_t>((rows_total + 255) / 256, 2 * sms) : 0;
+  const int64_t items = 2 * (int64_t)h->nwarps + 1;
+  TRY(dev_alloc(&h->item_row, (size_t)items, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->item_val, (size_t)items, &alloc_ms, &bytes));
+
+  // ---- info ----
+  csr5g_info& in = h->info;
+  in.m = m;
+  in.n = n;
+  in.nnz = nnz;
+  in.omega = kOmega;
+  in.sigma = sigma;
+  in.p = p;
+  in.p_complete = pc;
+  in.tail_len = tail;
+  in.tile_begin = tile_begin;
+  in.tile_end = tile_end;
+  in.has_tail = is_last && tail > 0;
+  in.tile_ptr_bits = 32;
+  in.word_bits = wb;
+  in.y_offset_bits = yb;
+  in.seg_offset_bits = sb;
+  in.num_sms = sms;
+  in.spmv_warps = h->nwarps;
+  in.tile_ptr_len = tile_ptr_len;
+  in.empty_offset_len = eo_total;
+  in.nnz_held = nnz_held;
+  in.metadata_bytes = tile_ptr_len * 4 + pcs * kOmega * (int64_t)wbytes;
+  in.device_bytes = bytes;
+  // nnz*(8+4) + 4(p+1) + W*32*pc + 4|eo| + 8n + 8m (per held range)
+  in.spmv_bytes = nnz_held * 12 + tile_ptr_len * 4 + pcs * kOmega * (int64_t)wbytes +
+                  eo_total * 4 + 8 * n + 8 * m;
+  in.first_row = h->first_row;
+  in.last_row = h->last_row;
+  in.own_row_begin = is_first ? 0 : (h->first_owned ? h->first_row : h->first_row + 1);
+  if (is_last) {
+    in.own_row_end = m;
+  } else {
+    const bool close_starts_here = sv[3] >= tile_end * B;  // next shard owns its first row
+    in.own_row_end = close_starts_here ? ptr_close : ptr_close + 1;
+  }
+  in.alloc_ms = alloc_ms;
+  in.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+  *out = h;
+  return cleanup(CSR5G_OK);
+#undef TRY
+#undef TRYC
+}
+
+int launch_to_csr(Handle* h, int32_t* d_col, double* d_val, cudaStream_t stream) {
+  CSR5G_CUDA(cudaSetDevice(h->device));
+  const int64_t tiled = h->pcs * h->B;
+  if (tiled > 0) {
+    k_untranspose<<<(unsigned)((tiled + 255) / 256), 256, 0, stream>>>(h->col, h->val, d_col, d_val,
+                                                                        tiled, (int)h->info.sigma);
+    CSR5G_CUDA(cudaGetLastError());
+  }
+  const int64_t rest = h->info.nnz_held - tiled;
+  if (rest > 0) {
+    CSR5G_CUDA(cudaMemcpyAsync(d_col + tiled, h->col + tiled, sizeof(int32_t) * rest,
+                               cudaMemcpyDeviceToDevice, stream));
+    CSR5G_CUDA(cudaMemcpyAsync(d_val + tiled, h->val + tiled, sizeof(double) * rest,
+                               cudaMemcpyDeviceToDevice, stream));
+  }
+  return CSR5G_OK;
+}
+
+}  // namespace csr5g

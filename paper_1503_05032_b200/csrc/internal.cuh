@@ -1,0 +1,168 @@
+// internal.cuh -- shared types and device helpers of libcsr5g.so.
+//
+// Layout in HBM (one handle; sizes for the held complete tiles k in [0, pcs)):
+//   row_ptr   int64 [m+1]          copy of the global CSR row pointer
+//   tile_ptr  u32   [tile_ptr_len] bit 31 = empty-row flag, low 31 = first row
+//   tile_desc W     [pcs*32]       W = u32 (sigma <= 17) or u64; lane-major per tile
+//   eo_ptr    int64 [pcs+1]        empty_offset list bounds (flagged tiles only)
+//   eo        int32 [E]            row offsets per segment head of flagged tiles
+//   col_idx   int32 [nnz_held]     tile-transposed: (col i, depth j) at k*B + j*32 + i
+//   val       f64   [nnz_held]     same order; tail (last shard) stays in CSR order
+// The transposed order makes every depth step of a tile one fully coalesced
+// 128 B (col) + 256 B (val) warp access.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/csr5g.h"
+
+namespace csr5g {
+
+constexpr int kOmega = 32;
+constexpr int kSegBits = 5;  // ceil_log2(32), descriptor.cpp:22-36
+constexpr int kSpmvThreads = 256;
+constexpr int kSpmvWarpsPerBlock = kSpmvThreads / 32;
+constexpr uint32_t kFull = 0xffffffffu;
+
+// Everything the SpMV kernels read, passed by value.
+struct SpmvArgs {
+  const int64_t* row_ptr;
+  const uint32_t* tile_ptr;
+  const void* desc;
+  const int64_t* eo_ptr;
+  const int32_t* eo;
+  const int32_t* col;
+  const double* val;
+  const double* x;
+  double* y;
+  int64_t* item_row;
+  double* item_val;
+  csr5g_partial* send;
+  int64_t pcs;             // complete tiles held
+  int64_t pos0;            // global nonzero position of local index 0
+  int64_t next_row_after;  // first row after the last held complete tile's range
+  int64_t lead_rows;       // rows [0, lead_rows) are empty and zeroed here
+  int64_t tail_row_begin;  // rows [tail_row_begin, m) computed from the tail here
+  int64_t tail_pos;        // global position where the tail starts (pc*B)
+  int64_t m;
+  int64_t first_row;       // row of head 0 of the first held tile
+  int32_t first_owned;     // that row starts inside this handle
+  int32_t has_tail_item;   // tail exists: its first row is item 2*nwarps
+  int32_t sigma;
+  int32_t B;
+  int32_t nwarps;          // tile warps (each a contiguous tile range)
+  int32_t rows_blocks;     // leading blocks that run the rows part
+  int32_t atomic;          // SpmvMode::atomic
+};
+
+struct Handle {
+  int device = 0;
+  csr5g_info info{};
+  bool wide = false;  // 64-bit descriptor words
+  int64_t pcs = 0, t0 = 0, B = 0;
+  int64_t* row_ptr = nullptr;
+  uint32_t* tile_ptr = nullptr;
+  void* desc = nullptr;
+  int64_t* eo_ptr = nullptr;
+  int32_t* eo = nullptr;
+  int32_t* col = nullptr;
+  double* val = nullptr;
+  int64_t* item_row = nullptr;
+  double* item_val = nullptr;
+  csr5g_partial* send = nullptr;
+  csr5g_partial* send_ext = nullptr;  // caller-provided record slot
+  int64_t next_row_after = 0, lead_rows = 0, tail_row_begin = 0, tail_pos = 0;
+  int64_t first_row = 0, last_row = 0;
+  bool first_owned = true, is_last = true, has_tail_item = false;
+  int nwarps = 0, tile_blocks = 0, rows_blocks = 0;
+};
+
+// ---- errors --------------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define CSR5G_CUDA(call)                                   \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return ::csr5g::cuda_fail(e_, #call); \
+  } while (0)
+
+// ---- launchers implemented in convert.cu / spmv.cu -------------------------
+int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d_row_ptr,
+                 const int32_t* d_col_idx, const double* d_val, const csr5g_params* params,
+                 int64_t tile_begin, int64_t tile_end, bool shard, int with_tail,
+                 cudaStream_t stream, Handle** out);
+void free_handle(Handle* h);
+int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_t stream,
+                cudaEvent_t ev0, cudaEvent_t ev1);
+int launch_fixup(Handle* h, const csr5g_partial* d_all, int world, int rank, double* d_y,
+                 cudaStream_t stream);
+int launch_to_csr(Handle* h, int32_t* d_col, double* d_val, cudaStream_t stream);
+int spmv_occupancy(bool wide, int* blocks_per_sm);
+
+// ---- device helpers ----------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Streaming read-once loads: no L1 allocation, evict-first in L2.
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t* p, uint64_t pol) {
+  uint64_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+// x gathers: L1-cached, evict-last in L2 so the streamed matrix does not push x out.
+__device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// upper_bound over row_ptr[lo, hi): first index with row_ptr[idx] > g (hi if none).
+__device__ __forceinline__ int64_t upper_bound_dev(const int64_t* __restrict__ rp, int64_t lo,
+                                                   int64_t hi, int64_t g) {
+  while (lo < hi) {
+    const int64_t mid = lo + ((hi - lo) >> 1);
+    if (rp[mid] <= g)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// format.cpp:42-50 row_of_nonzero over the full row_ptr (m+1 entries).
+__device__ __forceinline__ int64_t row_of_nonzero_dev(const int64_t* __restrict__ rp, int64_t m,
+                                                      int64_t g) {
+  if (m <= 0) return 0;
+  int64_t r = upper_bound_dev(rp, 0, m + 1, g) - 1;
+  r = r < 0 ? 0 : r;
+  return r > m - 1 ? m - 1 : r;
+}
+
+}  // namespace csr5g

@@ -1,0 +1,57 @@
+"""CPU checks of the drop-in boundary: libcsr5g.so loads and exports every
+symbol include/csr5g.h declares; host-only entry points behave like the
+reference (no compute calls -- there is no GPU here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def declared_symbols():
+    with open(os.path.join(ROOT, "include", "csr5g.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"CSR5G_API\s+[\w\s\*]*?\b(csr5g_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_symbols()
+    for must in ("csr5g_build", "csr5g_spmv", "csr5g_release", "csr5g_export",
+                 "csr5g_build_shard", "csr5g_fixup", "csr5g_to_csr"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1503_05032_b200 import _lib
+    L = _lib.lib()
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+    assert set(_lib.SIGNATURES) == set(declared_symbols())
+
+
+def test_host_entry_points(orc):
+    from paper_1503_05032_b200 import csr5
+    for npr in (0.5, 2.0, 4.0, 4.4, 4.6, 10.0, 31.5, 32.0, 33.0, 100.0, 256.0, 257.0, 1000.0):
+        assert csr5.select_sigma(npr) == orc.select_sigma(npr)
+    for sigma in range(1, 49):
+        assert csr5.layout(32, sigma) == orc.layout(32, sigma)
+    with pytest.raises(ValueError, match="smaller sigma"):
+        csr5.layout(32, 49)
+    with pytest.raises(ValueError, match="r <= s <= t"):
+        csr5.select_sigma(3.0, r=10, s=5)
+
+
+def test_no_cpu_fallback_without_gpu():
+    """Every compute entry point must fail loudly when no device is usable."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_1503_05032_b200 import _lib
+    L = _lib.lib()
+    h = C.c_void_p()
+    p = _lib.Params(32, 4, 4, 32, 256, 4)
+    rc = L.csr5g_build(0, 0, 0, 0, None, None, None, C.byref(p), None, C.byref(h))
+    assert rc == _lib.ECUDA
+    assert "CUDA" in L.csr5g_last_error().decode() or "device" in L.csr5g_last_error().decode()

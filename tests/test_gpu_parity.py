@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA converter and SpMV (through the C ABI) against the
+reference's golden arrays and the pinned CPU oracle on identical inputs.
+
+CSR5 arrays must be bit-exact; y within 1e-12 * max(1, nnz_i) * max_k|a_ik x_k|
+of the reference with empty rows exactly 0 (tests/_util.py).
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import Csr
+from tests._util import assert_y_close
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("tile_ptr", "tile_desc", "eo_ptr", "eo", "col_idx", "val")
+
+
+@pytest.fixture(scope="module")
+def g():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    from paper_1503_05032_b200 import csr5
+    return csr5
+
+
+def to_dev(g, a: Csr):
+    return g.CsrMatrix.from_host(a.m, a.n, a.row_ptr, a.col_idx.astype(np.int32), a.val)
+
+
+def gpu_build(g, a: Csr, sigma: int):
+    return g.csr_to_csr5(to_dev(g, a), g.TuningParams(sigma=sigma))
+
+
+def gpu_y(g, a5, x, mode="deterministic"):
+    xd = torch.as_tensor(x).cuda()
+    y = torch.full((a5.m,), float("nan"), dtype=torch.float64, device="cuda")
+    g.spmv_csr5(a5, xd, y, mode=mode)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def compare_arrays(ex: dict, ref, what):
+    for f in FIELDS:
+        got, exp = ex[f], getattr(ref, f) if not isinstance(ref, dict) else ref[f]
+        assert got.shape == exp.shape, f"{what}: {f} shape {got.shape} != {exp.shape}"
+        assert np.array_equal(got, exp), f"{what}: {f} differs at {np.nonzero(got != exp)[0][:8]}"
+
+
+def test_golden_w32(g, golden, orc):
+    """Every golden case of the reference: arrays bit-exact, y in tolerance."""
+    z, meta = golden
+    for c in meta:
+        k, mk = c["key"], c["mat"]
+        a = Csr(c["m"], c["n"], z[f"{mk}_row_ptr"], z[f"{mk}_col_idx"].astype(np.int64), z[f"{mk}_val"])
+        a5 = gpu_build(g, a, c["sigma"])
+        i = a5.info
+        assert (i.p, i.p_complete, i.tail_len, i.word_bits) == (c["p"], c["pc"], c["tail"], c["word_bits"])
+        ex = a5.export()
+        assert np.array_equal(ex["tile_ptr"], z[f"{k}_tile_ptr"]), (c, ex["tile_ptr"][:8], z[f"{k}_tile_ptr"][:8])
+        assert np.array_equal(ex["tile_desc"], z[f"{k}_tile_desc"]), c
+        assert np.array_equal(ex["eo_ptr"], z[f"{k}_eo_ptr"]), c
+        assert np.array_equal(ex["eo"], z[f"{k}_eo"]), c
+        assert np.array_equal(ex["col_idx"], z[f"{k}_tcol"].astype(np.int64)), c
+        x = z[f"{mk}_x"]
+        for mode in ("deterministic", "atomic"):
+            y = gpu_y(g, a5, x, mode)
+            assert_y_close(y, z[f"{k}_y"], a, x, f"{c['name']} sigma={c['sigma']} {mode}")
+        a5.release()
+
+
+def test_random_corpus_vs_oracle(g, orc):
+    """acceptance.cpp:53-104 shape classes at omega=32 over sigma in [1, 48]."""
+    rng = orc.rng(2024)
+    for case in range(160):
+        m, n = 1 + rng() % 400, 1 + rng() % 300
+        kind = case % 4
+        try:
+            if kind == 3:
+                a = rng.random_csr(m, n, rng() % 8000)
+            else:
+                a = orc.generate_synthetic(kind, m, n, min(m * n, rng() % 8000), rng(), 0.3)
+        except Exception:
+            a = rng.random_csr(m, n, rng() % 3000)
+        sigma = 1 + rng() % 48
+        x = rng.random_x(a.n)
+        ref = orc.build(a, 32, sigma)
+        a5 = gpu_build(g, a, sigma)
+        compare_arrays(a5.export(), ref, f"case {case} m={m} n={n} nnz={a.nnz} sigma={sigma}")
+        assert_y_close(gpu_y(g, a5, x), orc.spmv(a, x, 32, sigma), a, x, f"case {case}")
+        a5.release()
+
+
+def test_auto_sigma_matches_reference_rule(g, orc):
+    rng = orc.rng(11)
+    for npr in (1, 3, 5, 10, 17, 27, 40, 300):
+        m = 200
+        a = orc.generate_synthetic(0, m, 400, m * npr, rng())
+        a5 = g.csr_to_csr5(to_dev(g, a))  # sigma = 0 -> auto
+        assert a5.sigma == orc.select_sigma(npr)
+        a5.release()
+
+
+def hard_shapes(orc):
+    rng = orc.rng(67)
+    yield "m=1 wide row", orc.generate_synthetic(0, 1, 5000, 5000, 1)
+    yield "n=1 tall column", orc.generate_synthetic(0, 3000, 1, 3000, 1)
+    yield "all rows empty", orc.coo_to_csr([], [], [], 77, 7)
+    yield "empty 0x0", Csr(0, 0, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    yield "one long row 30%", orc.generate_synthetic(1, 500, 6000, 18000, 7, 0.3)
+    yield "exact multiple", orc.generate_synthetic(0, 64, 64, 64 * 48, 3)
+    yield "singletons", orc.generate_synthetic(0, 4000, 4000, 4000, 4)
+    # long runs of empty rows (> 32, exercising the cooperative zeroing path)
+    rows = [3] * 50 + [4000] * 20 + [4001] * 700 + [9000] * 5
+    cols = list(range(50)) + list(range(20)) + list(range(700)) + list(range(5))
+    yield "long empty gaps", orc.coo_to_csr(rows, cols, np.linspace(0.5, 1.5, len(rows)), 12000, 800)
+    # every other row empty, plus leading and trailing empties
+    r2 = [5 + 2 * k for k in range(3000) for _ in range(3)]
+    c2 = [j for k in range(3000) for j in range(3)]
+    yield "alternating empties", orc.coo_to_csr(r2, c2, np.linspace(0.5, 1.5, len(r2)), 7000, 5)
+    yield "random skew", orc.generate_synthetic(2, 5000, 3000, 40000, rng())
+
+
+@pytest.mark.parametrize("sigma", [1, 4, 5, 16, 17, 18, 27, 48])
+def test_hard_shapes(g, orc, sigma):
+    for name, a in hard_shapes(orc):
+        x = orc.rng(9).random_x(a.n)
+        ref = orc.build(a, 32, sigma)
+        a5 = gpu_build(g, a, sigma)
+        compare_arrays(a5.export(), ref, f"{name} sigma={sigma}")
+        if a.m:
+            assert_y_close(gpu_y(g, a5, x), orc.spmv(a, x, 32, sigma), a, x, f"{name} sigma={sigma}")
+            assert_y_close(gpu_y(g, a5, x, "atomic"), orc.dense_spmv(a, x), a, x, f"{name} atomic")
+        a5.release()
+
+
+def test_deterministic_is_bitwise_stable(g, orc):
+    a = orc.generate_synthetic(2, 20000, 5000, 400000, 77)
+    a5 = gpu_build(g, a, 16)
+    x = orc.rng(78).random_x(a.n)
+    y0 = gpu_y(g, a5, x)
+    for _ in range(5):
+        assert np.array_equal(gpu_y(g, a5, x), y0)
+
+
+def test_power_of_two_scaling_exact(g, orc):  # test_spmv.cpp:232-242
+    rng = orc.rng(61)
+    a = rng.random_csr(400, 400, 9000)
+    x = rng.random_x(400)
+    a5 = gpu_build(g, a, 8)
+    assert np.array_equal(gpu_y(g, a5, 8.0 * x), 8.0 * gpu_y(g, a5, x))
+
+
+def test_roundtrip(g, orc):  # format.cpp:254-265, acceptance criterion 2
+    rng = orc.rng(23)
+    for sigma in (1, 2, 4, 12, 16, 33):
+        a = rng.random_csr(300, 200, 9000)
+        d = to_dev(g, a)
+        a5 = g.csr_to_csr5(d, g.TuningParams(sigma=sigma))
+        back = g.csr5_to_csr(a5, d.row_ptr)
+        assert np.array_equal(back.col_idx.cpu().numpy(), a.col_idx.astype(np.int32))
+        assert np.array_equal(back.val.cpu().numpy(), a.val)
+
+
+def test_errors_mirror_reference(g, orc):
+    a = orc.coo_to_csr([0], [0], [1.0], 2, 3)
+    d = to_dev(g, a)
+    with pytest.raises(ValueError, match="omega must be 32"):
+        g.csr_to_csr5(d, g.TuningParams(omega=4, sigma=16))
+    with pytest.raises(ValueError, match="omega \\* sigma must be >= 2"):
+        g.csr_to_csr5(d, g.TuningParams(omega=1, sigma=1))
+    with pytest.raises(ValueError, match="smaller sigma"):
+        g.csr_to_csr5(d, g.TuningParams(sigma=49))
+    with pytest.raises(ValueError, match="r <= s <= t"):
+        g.csr_to_csr5(d, g.TuningParams(sigma=4, r=10, s=5))
+    a5 = g.csr_to_csr5(d, g.TuningParams(sigma=4))
+    with pytest.raises(ValueError, match="spmv: x has length 2, expected 3"):
+        g.spmv_csr5(a5, torch.ones(2, dtype=torch.float64, device="cuda"))
+
+
+def test_stencil_generator(g, orc):
+    for kind, a_, nnz_fn in ((0, 13, lambda s: 5 * s * s - 4 * s), (1, 7, lambda s: (3 * s - 2) ** 3)):
+        d = g.stencil(kind, a_)
+        rp = d.row_ptr.cpu().numpy()
+        ci = d.col_idx.cpu().numpy().astype(np.int64)
+        va = d.val.cpu().numpy()
+        assert rp[-1] == nnz_fn(a_)
+        # canonical and symmetric, diagonal dominant values
+        for r in range(d.m):
+            cols = ci[rp[r]:rp[r + 1]]
+            assert np.all(np.diff(cols) > 0)
+            assert r in cols
+        A = np.zeros((d.m, d.m))
+        for r in range(d.m):
+            A[r, ci[rp[r]:rp[r + 1]]] = va[rp[r]:rp[r + 1]]
+        assert np.array_equal(A, A.T)
+
+
+def test_shards_concatenate_and_fix_up(g, orc):
+    """Multi-GPU partition on one device, run shard by shard: the shard arrays
+    are slices of the single-device arrays and boundary fix-ups reproduce y."""
+    from paper_1503_05032_b200 import mg
+    rng = orc.rng(5)
+    cases = [orc.generate_synthetic(1, 300, 30000, 60000, 3, 0.5),  # one row spans shards
+             orc.generate_synthetic(2, 5000, 4000, 120000, 4),
+             orc.generate_synthetic(0, 2000, 2000, 54000, 5)]
+    for a in cases:
+        x = rng.random_x(a.n)
+        sigma = orc.select_sigma(a.nnz / a.m)
+        full = orc.build(a, 32, sigma)
+        y_ref = orc.spmv(a, x, 32, sigma)
+        for world in (2, 3, 5, 8):
+            y = mg.emulate_shards_on_one_device(a, x, sigma, world)
+            assert_y_close(y, y_ref, a, x, f"world={world}")
+            ex = mg.emulate_shard_exports(a, sigma, world)
+            for f in ("tile_desc", "eo", "col_idx", "val"):
+                assert np.array_equal(np.concatenate([e[f] for e in ex]), getattr(full, f)), f
+            tp = np.concatenate([e["tile_ptr"][:-1] for e in ex[:-1]] + [ex[-1]["tile_ptr"]])
+            assert np.array_equal(tp, full.tile_ptr)
