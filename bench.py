@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""CSR5 fp64 SpMV benchmark on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload st27_200]
+    python bench.py --impl reference ...        # the reference's CPU path
+
+One step = one CSR5 SpMV y = A x over the whole matrix (one pass of the hot
+path).  At N=1 the workload is BASELINE config 2, the 3D 27-point stencil
+200^3 (213.8M nnz, sigma = 27 by the reference rule, 64-bit descriptors).
+Under torchrun (N>1) the same matrix is tile-range sharded over the ranks with
+x replicated (strong scaling); a step includes the boundary-row exchange.
+
+`value` is GFLOP/s = 2*nnz / t with A and x resident in HBM; t is the max over
+ranks of CUDA-event time on the launching stream.  The matrix (2.76 GB) is far
+larger than the 126 MB L2, so no L2 flush is done between steps; x (64 MB) is
+reused across steps as it is within one SpMV.  `e2e` is the same metric through
+the host-buffer call: pinned x H2D + SpMV + y D2H per step.  The roofline
+figure is for the dominant tile kernel alone (events around it), with the
+algorithmic bytes of SURVEY 8(d).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CSR5 fp64 SpMV GFLOP/s + HBM GB/s (% roofline) at 1/2/4/8 B200; conv cost"
+UNIT = "GFLOP/s"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    """dram read+write bytes per launch of the tile kernel from the committed
+    `ncu --set full` summary (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t.get(workload, {}).get("k_spmv_dram_bytes")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# --------------------------------------------------------------------------
+# the reference's CPU path (oracle/_ref = the unmodified reference library)
+# --------------------------------------------------------------------------
+def reference_cpu(workload: dict, x, budget_s: float, omega=4, sigma=16, steps=None, warmup=0):
+    """Time the reference csr5::spmv_csr5 (deterministic) on the host cores.
+
+    steps=None: the bench.cpp:147-160 protocol (samples of `inner` back-to-back
+    calls, best sample reported) within ~budget_s.  steps=K: K single calls
+    after `warmup` calls (the --impl reference step loop)."""
+    import ctypes
+
+    import numpy as np
+
+    from oracle.oracle import Oracle, Ref, stencil
+    ref = Ref()
+    t0 = time.time()
+    a = stencil(Oracle(), workload["kind"], workload["a"])
+    gen_s = time.time() - t0
+    h, conv_ms = ref.build_handle(a, omega, sigma)
+    dp = ctypes.POINTER(ctypes.c_double)
+    xv = ref.L.ref_vec_new(np.ascontiguousarray(x).ctypes.data_as(dp), a.n)
+    y = np.zeros(a.m)
+    yp = y.ctypes.data_as(dp)
+    first = ref.L.ref_time_spmv(h, xv, yp, 0, 1)
+    if steps is None:
+        inner = max(1, int(0.5 / max(first / 1e3, 1e-6)))
+        samples = []
+        t_end = time.time() + budget_s
+        while (time.time() < t_end or len(samples) < 2) and len(samples) < 10:
+            samples.append(ref.L.ref_time_spmv(h, xv, yp, 0, inner))
+    else:
+        inner = 1
+        for _ in range(warmup):
+            ref.L.ref_time_spmv(h, xv, yp, 0, 1)
+        samples = [ref.L.ref_time_spmv(h, xv, yp, 0, 1) for _ in range(steps)]
+    scalar = ref.L.ref_time_csr_scalar(h, xv, yp, 3)
+    ref.L.ref_time_spmv(h, xv, yp, 0, 1)  # leave y = the csr5 result
+    threads = ref.max_threads()
+    ref.L.ref_vec_free(xv)
+    ref.L.ref_free(h)
+    return dict(nnz=a.nnz, m=a.m, best_ms=min(samples), mean_ms=sum(samples) / len(samples),
+                samples=samples, inner=inner, conv_ms=conv_ms, gen_s=gen_s, threads=threads,
+                csr_scalar_ms=scalar, omega=omega, sigma=sigma, y=y)
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return model, os.cpu_count()
+
+
+def run_reference(args, workload_name, workload):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    compiled from /root/reference/proj/core/src) on all host threads; rank 0
+    only under torchrun."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1503_05032_b200.synthetic import bench_x
+    n = workload["a"] ** (3 if workload["kind"] == 1 else 2)
+    r = reference_cpu(workload, bench_x(n), 0.0, steps=args.steps, warmup=args.warmup)
+    ms = r["mean_ms"]
+    gf = 2.0 * r["nnz"] / (ms * 1e6)
+    model, ncpu = cpu_info()
+    sample = (f"full {workload_name} matrix, reference csr5::spmv_csr5 omega={r['omega']} "
+              f"sigma={r['sigma']} deterministic, one call per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gf, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name, "desc": workload["desc"], "nnz": r["nnz"],
+                   "m": r["m"], "omega": r["omega"], "sigma": r["sigma"], "mode": "deterministic"},
+        "cpu_baseline": {"value": gf, "unit": UNIT, "cores": r["threads"], "kind": "reference",
+                         "sample": sample, "cpu_model": model, "nproc": ncpu,
+                         "conv_ms": r["conv_ms"], "conv_spmv_equiv": r["conv_ms"] / ms,
+                         "csr_scalar_gflops": 2.0 * r["nnz"] / (r["csr_scalar_ms"] * 1e6)},
+        "e2e": {"value": gf, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def run_ours(args, workload_name, workload):
+    import numpy as np
+    import torch
+
+    from paper_1503_05032_b200 import csr5, mg
+    from paper_1503_05032_b200.synthetic import bench_x
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    a = csr5.stencil(workload["kind"], workload["a"], device=dev)
+    torch.cuda.synchronize()
+    x_host = bench_x(a.n)
+    x = torch.as_tensor(x_host).to(dev)
+    y = torch.empty(a.m, dtype=torch.float64, device=dev)
+    sigma = csr5.select_sigma(a.nnz / a.m)
+
+    # -- conversion (device-resident CSR -> usable CSR5), timed twice --------
+    if world == 1:
+        a5 = csr5.csr_to_csr5(a, csr5.TuningParams(sigma=sigma))
+        a5.release()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a5 = csr5.csr_to_csr5(a, csr5.TuningParams(sigma=sigma))
+        conv_ms = (time.perf_counter() - t0) * 1e3
+        info = a5.info
+        run = lambda: csr5.spmv_csr5(a5, x, y)  # noqa: E731
+    else:
+        lo, hi = mg.Csr5Sharded.slices_for(a.nnz, sigma, rank, world)
+        t0 = time.perf_counter()
+        sh = mg.Csr5Sharded(a.row_ptr, a.col_idx[lo:], a.val[lo:], a.m, a.n, a.nnz, sigma, rank,
+                            world)
+        conv_ms = (time.perf_counter() - t0) * 1e3
+        a5 = sh.a5
+        info = a5.info
+        run = lambda: sh.spmv(x, y)  # noqa: E731
+
+    # -- correctness guard before timing (bench.cpp:130-141 analogue) --------
+    run()
+    torch.cuda.synchronize()
+    A = torch.sparse_csr_tensor(a.row_ptr, a.col_idx.long(), a.val, (a.m, a.n))
+    y_chk = (A @ x.unsqueeze(1)).squeeze(1)
+    own = (info.own_row_begin, info.own_row_end)
+    err = ((y[own[0]:own[1]] - y_chk[own[0]:own[1]]).abs() /
+           y_chk[own[0]:own[1]].abs().clamp(min=1.0)).max().item()
+    if not err <= 1e-12:
+        raise SystemExit(f"correctness guard: max relative error {err} > 1e-12")
+    del A, y_chk
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    for _ in range(args.warmup):
+        run()
+    ev0, ev1 = csr5.Event(), csr5.Event()
+    tk = [(csr5.Event(), csr5.Event()) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    ev0.record()
+    for k in range(args.steps):
+        if world == 1:
+            csr5.spmv_csr5_evt(a5, x, y, tk[k][0], tk[k][1])
+        else:
+            run()
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = max_over_ranks(ev0.elapsed_ms(ev1))
+    ms = total_ms / args.steps
+    tile_ms = (sum(b.elapsed_ms(e) for b, e in tk) / args.steps) if world == 1 else None
+
+    # -- end to end through the host-buffer call ------------------------------
+    xh = torch.as_tensor(x_host).pin_memory()
+    yh = torch.empty(a.m, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        x.copy_(xh, non_blocking=True)
+        run()
+        yh.copy_(y, non_blocking=True)
+    for _ in range(args.warmup):
+        e2e_step()
+    e0, e1 = csr5.Event(), csr5.Event()
+    torch.cuda.synchronize()
+    barrier()
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_ms(e1)) / args.steps
+
+    flops = 2.0 * a.nnz
+    value = flops / (ms * 1e6)
+    peak, peak_src = peaks()
+    line = None
+    if rank == 0:
+        bytes_alg = info.spmv_bytes
+        roof = None
+        if tile_ms:
+            achieved = bytes_alg / (tile_ms * 1e-3) / 1e9
+            traffic = ncu_traffic(workload_name)
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "kernel": "k_spmv (tile kernel)", "kernel_ms": tile_ms,
+                    "algorithmic_bytes": bytes_alg, "peak_source": peak_src,
+                    "frac_of_8TBs_spec": achieved / 8000.0}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                r = reference_cpu(workload, x_host, budget_s=args.cpu_seconds)
+                model, ncpu = cpu_info()
+                yr = r.pop("y")
+                cpu = {"value": 2.0 * r["nnz"] / (r["best_ms"] * 1e6), "unit": UNIT,
+                       "cores": r["threads"], "kind": "reference",
+                       "sample": (f"full {workload_name} matrix, reference csr5::spmv_csr5 "
+                                  f"omega={r['omega']} sigma={r['sigma']} deterministic; best of "
+                                  f"{len(r['samples'])} samples x {r['inner']} calls"),
+                       "cpu_model": model, "nproc": ncpu, "conv_ms": r["conv_ms"],
+                       "conv_spmv_equiv": r["conv_ms"] / r["best_ms"],
+                       "csr_scalar_gflops": 2.0 * r["nnz"] / (r["csr_scalar_ms"] * 1e6),
+                       "y_max_rel_err_vs_gpu": float(np.max(np.abs(yr - y.cpu().numpy()) /
+                                                            np.maximum(1.0, np.abs(yr))))}
+            except Exception as e:  # the CPU number is reported, never gating
+                cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
+                       "sample": f"failed: {e}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name, "desc": workload["desc"], "m": a.m, "n": a.n,
+                       "nnz": a.nnz, "omega": 32, "sigma": sigma, "p": info.p,
+                       "desc_word_bits": info.word_bits, "mode": "deterministic",
+                       "parallelism": f"tile-range shards x{world}, x replicated",
+                       "l2": "inputs larger than L2 (matrix 2.7 GB); no flush",
+                       "x": "mt19937_64(1), 0.5 + (rng()>>11)*2^-53 (bench.cpp:103-105)"},
+            "gbs_effective": info.spmv_bytes * world / (ms * 1e-3) / 1e9 if world == 1 else None,
+            "roofline": roof,
+            "conversion": {"ms": conv_ms, "alloc_ms": info.alloc_ms,
+                           "spmv_equiv": conv_ms / ms,
+                           "spmv_equiv_excl_alloc": (conv_ms - info.alloc_ms) / ms},
+            "cpu_baseline": cpu,
+            "e2e": {"value": flops / (e2e_ms * 1e6), "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * a.n, "d2h_bytes_per_step": 8 * a.m,
+                    "ms_per_step": e2e_ms,
+                    "path": "pinned x H2D + csr5.spmv_csr5 + y D2H, CUDA events"},
+            "gpu_launches": args.steps * (2 if world == 1 else 3),
+            "clocks": clk,
+            "correctness_max_rel_err": err,
+        }
+        print(json.dumps(line), flush=True)
+    a5 = None
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def main():
+    from paper_1503_05032_b200.synthetic import WORKLOADS
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="st27_200")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, args.workload, wl)
+    else:
+        run_ours(args, args.workload, wl)
+
+
+if __name__ == "__main__":
+    main()

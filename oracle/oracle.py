@@ -512,3 +512,17 @@ class Ref:
 
 def have_ref() -> bool:
     return os.path.exists(LIB_REF)
+
+
+def stencil(orc: "Oracle", kind: int, a: int) -> Csr:
+    """Host twin of csr5g_stencil_fill (testgen.c orc_stencil)."""
+    import ctypes as C
+    m = a * a if kind == 0 else a * a * a
+    nnz = (1 if a == 1 else 5 * a * a - 4 * a) if kind == 0 else (1 if a == 1 else (3 * a - 2) ** 3)
+    rp = np.empty(m + 1, np.int64)
+    ci = np.empty(nnz, np.int64)
+    va = np.empty(nnz, np.float64)
+    fn = orc.L.orc_stencil
+    fn.argtypes = [C.c_int, C.c_int64, _i64p, _i64p, _f64p]
+    fn(kind, a, _p(rp, _i64p), _p(ci, _i64p), _p(va, _f64p))
+    return Csr(m, m, rp, ci, va)

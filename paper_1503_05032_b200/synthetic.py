@@ -1,0 +1,69 @@
+"""Synthetic inputs for the benchmark (BASELINE.json configs).
+
+x follows the reference harness convention (bench.cpp:103-105):
+std::mt19937_64 seeded with x_seed = 1, x_i = 0.5 + (rng() >> 11) * 2^-53.
+The engine is restated here in vectorised numpy (MT19937-64, Matsumoto &
+Nishimura); tests check it against the oracle's scalar engine.
+
+Matrices are generated on the device by libcsr5g (csr5g_stencil_fill).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+_N, _M = 312, 156
+_UPPER = np.uint64(0xFFFFFFFF80000000)
+_LOWER = np.uint64(0x7FFFFFFF)
+_A = np.uint64(0xB5026F5AA96619E9)
+
+
+def _seed(seed: int) -> np.ndarray:
+    mt = np.zeros(_N, dtype=np.uint64)
+    mt[0] = seed
+    f = 6364136223846793005
+    for i in range(1, _N):
+        prev = int(mt[i - 1])
+        mt[i] = (f * (prev ^ (prev >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+    return mt
+
+
+def _twist(mt: np.ndarray) -> None:
+    def step(i0, i1, nxt, far):
+        y = (mt[i0:i1] & _UPPER) | (nxt & _LOWER)
+        v = far ^ (y >> np.uint64(1))
+        v ^= np.where((y & np.uint64(1)) != 0, _A, np.uint64(0))
+        mt[i0:i1] = v
+    step(0, _M, mt[1:_M + 1].copy(), mt[_M:_N].copy())           # far = old values
+    step(_M, _N - 1, mt[_M + 1:_N].copy(), mt[0:_N - 1 - _M].copy())  # far = new values
+    step(_N - 1, _N, mt[0:1].copy(), mt[_M - 1:_M].copy())
+
+
+def _temper(x: np.ndarray) -> np.ndarray:
+    x = x ^ ((x >> np.uint64(29)) & np.uint64(0x5555555555555555))
+    x = x ^ ((x << np.uint64(17)) & np.uint64(0x71D67FFFEDA60000))
+    x = x ^ ((x << np.uint64(37)) & np.uint64(0xFFF7EEE000000000))
+    return x ^ (x >> np.uint64(43))
+
+
+def mt19937_64(seed: int, count: int) -> np.ndarray:
+    """First `count` outputs of std::mt19937_64(seed)."""
+    mt = _seed(seed)
+    out = np.empty(((count + _N - 1) // _N) * _N, dtype=np.uint64)
+    for b in range(0, len(out), _N):
+        _twist(mt)
+        out[b:b + _N] = _temper(mt)
+    return out[:count]
+
+
+def bench_x(n: int, seed: int = 1) -> np.ndarray:
+    """x as run_benchmark generates it (bench.cpp:103-105)."""
+    r = mt19937_64(seed, n)
+    return 0.5 + (r >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+WORKLOADS = {
+    "st27_200": dict(kind=1, a=200, desc="3D 27-point stencil 200^3 (8M rows, 213.8M nnz), "
+                                          "values 26/-1"),
+    "lap5_1000": dict(kind=0, a=1000, desc="2D 5-point Laplacian 1000^2 (1M rows, 4.996M nnz), "
+                                            "values 4/-1"),
+}
