@@ -23,6 +23,7 @@ int fail(int code, const std::string& msg) {
 int cuda_fail(cudaError_t e, const char* what) {
   g_error = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
             ") in " + what;
+  cudaGetLastError();  // do not leak a non-sticky error into the next call
   return e == cudaErrorMemoryAllocation ? CSR5G_ENOMEM : CSR5G_ECUDA;
 }
 

@@ -458,12 +458,10 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   h->lead_rows = (is_first && nnz > 0) ? ptr_first : 0;
   h->tail_pos = pc * B;
   h->has_tail_item = is_last && tail > 0;
-  int sms = 0, bps = 0;
+  int sms = 0;
   TRYC(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  TRY(spmv_occupancy(h->wide, &bps));
-  const int64_t max_warps = (int64_t)sms * bps * kSpmvWarpsPerBlock;
-  h->nwarps = (int)std::min<int64_t>(max_warps, pcs);
-  h->tile_blocks = (h->nwarps + kSpmvWarpsPerBlock - 1) / kSpmvWarpsPerBlock;
+  h->info.sigma = sigma;  // spmv_plan picks the sigma-specialised kernel
+  TRY(spmv_plan(h, sms));
   const int64_t rows_total = h->lead_rows + (m - h->tail_row_begin);
   h->rows_blocks = rows_total > 0 ? (int)std::min<int64_t>((rows_total + 255) / 256, 2 * sms) : 0;
   const int64_t items = 2 * (int64_t)h->nwarps + 1;

@@ -48,13 +48,16 @@ struct SpmvArgs {
   int64_t tail_row_begin;  // rows [tail_row_begin, m) computed from the tail here
   int64_t tail_pos;        // global position where the tail starts (pc*B)
   int64_t m;
+  int64_t tile_ptr_len;
   int64_t first_row;       // row of head 0 of the first held tile
   int32_t first_owned;     // that row starts inside this handle
   int32_t has_tail_item;   // tail exists: its first row is item 2*nwarps
   int32_t sigma;
   int32_t B;
   int32_t nwarps;          // tile warps (each a contiguous tile range)
-  int32_t rows_blocks;     // leading blocks that run the rows part
+  int32_t stages;          // TMA ring depth per warp
+  int32_t stage_bytes;     // one tile: val | col_idx | descriptor words
+  int32_t bar_bytes;       // mbarrier area at the start of shared memory
   int32_t atomic;          // SpmvMode::atomic
 };
 
@@ -78,6 +81,7 @@ struct Handle {
   int64_t first_row = 0, last_row = 0;
   bool first_owned = true, is_last = true, has_tail_item = false;
   int nwarps = 0, tile_blocks = 0, rows_blocks = 0;
+  int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
 };
 
 // ---- errors --------------------------------------------------------------
@@ -102,7 +106,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
 int launch_fixup(Handle* h, const csr5g_partial* d_all, int world, int rank, double* d_y,
                  cudaStream_t stream);
 int launch_to_csr(Handle* h, int32_t* d_col, double* d_val, cudaStream_t stream);
-int spmv_occupancy(bool wide, int* blocks_per_sm);
+int spmv_plan(Handle* h, int sms);
 
 // ---- device helpers ----------------------------------------------------------
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -1,28 +1,70 @@
 // spmv.cu -- CSR5 SpMV (reference: spmv.cpp:42-124, 224-298).
 //
-// k_spmv: persistent grid, one warp = one contiguous range of tiles (CSR5
-//   tiles are equal-work units, so a static split balances).  Per tile the
-//   warp runs Algorithm 8 with lane i = column i (spmv.cpp:61-95): sigma
-//   coalesced depth steps of col/val, x gathered through L1/L2, segment
-//   closes at each bit flag.  The cross-column splice (fast segmented sum,
-//   spmv.cpp:97-105) is a 5-step shuffle segmented suffix scan driven by a
-//   ballot of head-bearing lanes -- no shared memory, no scan-and-subtract.
-//   Rows wholly inside the warp's range are stored straight to y; only the
-//   first and the last row run of each warp can be shared with a neighbour,
-//   so each warp emits exactly two (row, partial) items.  Empty rows are
-//   zeroed here from the empty_offset gaps (no memset of y).
-//   Leading blocks ("rows part") compute the CSR tail rows (spmv.cpp:110-124)
-//   and zero leading/trailing empty rows.
+// k_spmv<SIGMA>: persistent grid (one CTA per SM), one warp = one contiguous
+//   range of tiles (CSR5 tiles are equal-work units, so a static split
+//   balances).  Specialised per sigma so the depth loop is fully unrolled.
+//   * TMA ring: each warp streams its tiles through an S-stage shared-memory
+//     ring with bulk copies (cp.async.bulk, completion on one mbarrier per
+//     stage).  A tile's val (B*8 bytes), col_idx (B*4) and descriptor words
+//     (32*W) are contiguous in HBM thanks to the CSR5 transposition, so a tile
+//     is three bulk copies issued by lane 0, S-1 tiles ahead of the one being
+//     computed: the matrix stream never waits on the dependent x gathers.
+//   * Depth loop (Algorithm 8, spmv.cpp:61-95, lane i = column i): all x
+//     gathers of the tile are issued first (L1/L2, evict-last), then sigma
+//     FMAs; a warp-uniform test on the OR of the lanes' bit flags guards the
+//     rare segment-close path, which only writes the closed sum to a per-warp
+//     shared-memory slot indexed by its segment head.
+//   * Splice (fast segmented sum, spmv.cpp:97-105): 5-step shuffle segmented
+//     suffix scan over a ballot of head-bearing lanes -- no scan-and-subtract.
+//   * Write-back: lanes walk the tile's heads in order (coalesced
+//     empty_offset reads, near-coalesced y stores) and zero the empty rows
+//     between heads.  Rows wholly inside the warp's range are final; only the
+//     first and last row runs of a warp can be shared, so each warp emits two
+//     (row, partial) items.
+//   * Before its tiles every thread takes a grid-stride share of the "rows
+//     part": CSR tail rows (spmv.cpp:110-124), leading/trailing empty rows.
 // k_calibrate: deterministic merge of the 2*warps+1 items (keys are
 //   non-decreasing rows): segmented reduction per warp window, forward walk
 //   for runs crossing windows; y[row] = run total.  Atomic mode instead adds
 //   items with fp64 atomics into a zeroed y (spmv.cpp:273-295).
+#include <algorithm>
 #include <climits>
+#include <type_traits>
 
 #include "internal.cuh"
 
 namespace csr5g {
 namespace {
+
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(saddr(bar)), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+
+// One TMA bulk copy global -> shared, completion counted on `bar`.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                          uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar)), "l"(pol)
+      : "memory");
+}
 
 __device__ __forceinline__ void put_item(const SpmvArgs& a, int64_t idx, int64_t row, double v) {
   if (a.atomic) {
@@ -33,10 +75,11 @@ __device__ __forceinline__ void put_item(const SpmvArgs& a, int64_t idx, int64_t
   }
 }
 
+// Tail rows and leading/trailing empty rows, grid-stride over all threads.
 __device__ void rows_part(const SpmvArgs& a) {
   const int64_t tail_rows = a.m - a.tail_row_begin;
   const int64_t total = a.lead_rows + tail_rows;
-  const int64_t stride = (int64_t)a.rows_blocks * blockDim.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
     if (idx < a.lead_rows) {
       a.y[idx] = 0.0;
@@ -55,100 +98,137 @@ __device__ void rows_part(const SpmvArgs& a) {
   }
 }
 
-template <typename W>
-__global__ void __launch_bounds__(kSpmvThreads) k_spmv(SpmvArgs a) {
-  if ((int)blockIdx.x < a.rows_blocks) {
-    rows_part(a);
-    return;
-  }
-  const int lane = threadIdx.x & 31;
-  const int w = ((int)blockIdx.x - a.rows_blocks) * kSpmvWarpsPerBlock + (threadIdx.x >> 5);
-  if (w >= a.nwarps) return;
-  const int64_t kb = (int64_t)w * a.pcs / a.nwarps;
-  const int64_t ke = (int64_t)(w + 1) * a.pcs / a.nwarps;
+__device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
+  const uint32_t lo = __reduce_or_sync(kFull, (uint32_t)v);
+  const uint32_t hi = __reduce_or_sync(kFull, (uint32_t)(v >> 32));
+  return ((uint64_t)hi << 32) | lo;
+}
+
+}  // namespace
+
+// Outside the anonymous namespace: the sigma instantiations are reached
+// through a function-pointer switch, and the runtime must register each one.
+template <int SIG>
+__global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
+  using W = typename std::conditional<(SIG <= 17), uint32_t, uint64_t>::type;
+  constexpr int B = 32 * SIG;
+  constexpr int CH = SIG <= 32 ? SIG : (SIG + 1) / 2;  // x gathers in flight per lane
+  constexpr uint64_t FMASK = (1ull << SIG) - 1;
+  constexpr uint32_t COL_OFF = B * 8, DESC_OFF = B * 12;
+  constexpr uint32_t TILE_BYTES = B * 12 + 32 * sizeof(W);
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int NW = blockDim.x >> 5;
+  const int S = a.stages;
+  const int w = blockIdx.x * NW + wib;
+  const bool has_tiles = w < a.nwarps;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + wib * S;
+  double* closed = reinterpret_cast<double*>(smem + a.bar_bytes) + (size_t)wib * B;
+  unsigned char* ring = smem + a.bar_bytes + (size_t)NW * B * 8 + (size_t)wib * S * a.stage_bytes;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_x = policy_evict_last();
-  const int sigma = a.sigma;
-  const int64_t B = a.B;
-  const uint64_t fmask = (1ull << sigma) - 1;
   const W* __restrict__ desc = static_cast<const W*>(a.desc);
-  double* __restrict__ y = a.y;
 
+  int64_t kb = 0, ke = 0;
+  if (has_tiles) {
+    kb = (int64_t)w * a.pcs / a.nwarps;
+    ke = (int64_t)(w + 1) * a.pcs / a.nwarps;
+  }
+  auto issue = [&](int64_t k, int s) {  // lane 0 only
+    unsigned char* st = ring + (size_t)s * a.stage_bytes;
+    uint64_t* bar = bars + s;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)),
+                 "r"(TILE_BYTES)
+                 : "memory");
+    bulk_load(st, a.val + k * B, B * 8, bar, pol_s);
+    bulk_load(st + COL_OFF, a.col + k * B, B * 4, bar, pol_s);
+    bulk_load(st + DESC_OFF, desc + k * 32, 32 * sizeof(W), bar, pol_s);
+  };
+  if (has_tiles && lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(bars + s);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < S && kb + s < ke; ++s) issue(kb + s, s);
+  }
+  __syncwarp();
+
+  rows_part(a);
+  if (!has_tiles) return;
+
+  double* __restrict__ y = a.y;
   int64_t pend_row = -1;
   double pend_val = 0.0;
   bool pend_first = true;
+  uint32_t tpv = 0, tpv_next = 0;
+  int64_t eov = 0;
+  int s = 0;
+  uint32_t phase = 0;
 
   for (int64_t k = kb; k < ke; ++k) {
-    const uint32_t tp = a.tile_ptr[k];
+    const int slot = (int)((k - kb) & 31);
+    if (slot == 0) {  // per-tile scalars, 32 tiles per batch
+      const int64_t last = a.tile_ptr_len - 1;
+      tpv = a.tile_ptr[k + lane < last ? k + lane : last];
+      tpv_next = a.tile_ptr[k + 32 < last ? k + 32 : last];
+      eov = a.eo_ptr[k + lane < a.pcs ? k + lane : a.pcs];
+    }
+    const uint32_t tp = __shfl_sync(kFull, tpv, slot);
+    const uint32_t tpn_s = __shfl_sync(kFull, tpv, (slot + 1) & 31);
+    const uint32_t tpn = slot == 31 ? tpv_next : tpn_s;
+    const int64_t eo_base = __shfl_sync(kFull, eov, slot);
     const int64_t tile_row = tp & 0x7fffffffu;
     const bool flagged = (tp >> 31) != 0;
-    const int64_t next_row =
-        (k + 1 == a.pcs) ? a.next_row_after : (int64_t)(a.tile_ptr[k + 1] & 0x7fffffffu);
-    const uint64_t wd = (uint64_t)ld_stream(desc + k * 32 + lane, pol_s);
-    const uint64_t fr = __brevll(wd & fmask) >> (64 - sigma);  // bit j = depth j
-    const int yoff = (int)(wd >> (kSegBits + sigma));
+    const int64_t next_row = (k + 1 == a.pcs) ? a.next_row_after : (int64_t)(tpn & 0x7fffffffu);
+    const int32_t* __restrict__ eo = a.eo + eo_base;
+
+    mbar_wait(bars + s, phase);
+    const unsigned char* st = ring + (size_t)s * a.stage_bytes;
+    const double* sv = reinterpret_cast<const double*>(st);
+    const int32_t* sc = reinterpret_cast<const int32_t*>(st + COL_OFF);
+    const uint64_t wd = (uint64_t)reinterpret_cast<const W*>(st + DESC_OFF)[lane];
+    const uint64_t fr = __brevll(wd & FMASK) >> (64 - SIG);  // bit j = depth j
+    const int yoff = (int)(wd >> (kSegBits + SIG));
     const int cnt = __popcll(fr);
     const int H = __shfl_sync(kFull, yoff + cnt, 31);
-    const int32_t* __restrict__ eo = flagged ? a.eo + a.eo_ptr[k] : nullptr;
+    const uint64_t anyf = warp_or64(fr);
 
-    // rows of heads h and h+1 (h+1 == H means "the next tile's first row")
-    auto head_row = [&](int h) -> int64_t { return tile_row + (eo ? (int64_t)eo[h] : (int64_t)h); };
-    int64_t defer_lo = 0, defer_hi = 0;
-    // zero the empty rows strictly between row(h) and the next head's row
-    auto gap = [&](int h, int64_t r) {
-      if (!eo && h + 1 < H) return;  // unflagged tile: consecutive heads are adjacent rows
-      const int64_t nr = (h + 1 < H) ? head_row(h + 1) : next_row;
-      const int64_t lo = r + 1;
-      if (nr - lo <= 8) {
-        for (int64_t q = lo; q < nr; ++q) y[q] = 0.0;
-      } else if (defer_hi == defer_lo) {
-        defer_lo = lo;
-        defer_hi = nr;
-      } else {
-        for (int64_t q = lo; q < nr; ++q) y[q] = 0.0;
-      }
-    };
-
-    const int64_t base = k * B + lane;
-    double sum = 0.0, red = 0.0, c0 = 0.0;
+    // ---- depth loop: gathers first, then FMAs; closes go to closed[head] ----
+    double sum = 0.0, red = 0.0;
     bool seen = false;
     int head = yoff;
-    for (int j0 = 0; j0 < sigma; j0 += 8) {
-      int32_t c[8];
-      double v[8], xv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (j0 + u < sigma) {
-          c[u] = ld_stream(a.col + base + (int64_t)(j0 + u) * 32, pol_s);
-          v[u] = ld_stream(a.val + base + (int64_t)(j0 + u) * 32, pol_s);
-        }
-      }
+    for (int j0 = 0; j0 < SIG; j0 += CH) {
+      double xv[CH];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (j0 + u < sigma) xv[u] = ld_keep(a.x + c[u], pol_x);
+      for (int u = 0; u < CH; ++u)
+        if (j0 + u < SIG) xv[u] = ld_keep(a.x + sc[(j0 + u) * 32 + lane], pol_x);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < CH; ++u) {
         const int j = j0 + u;
-        if (j < sigma) {
-          if ((fr >> j) & 1ull) {
-            if (!seen) {
-              red = sum;  // piece continuing the column to the left (spmv.cpp:75-77)
-              seen = true;
-            } else {      // segment sealed inside this column
-              const int64_t r = head_row(head);
-              if (head == 0)
-                c0 = sum;
-              else
-                y[r] = sum;
-              gap(head, r);
-              ++head;
+        if (j < SIG) {
+          if ((anyf >> j) & 1ull) {  // warp-uniform: some lane closes a segment here
+            if ((fr >> j) & 1ull) {
+              if (seen) {
+                closed[head++] = sum;  // segment sealed inside this column
+              } else {
+                red = sum;  // piece continuing the column to the left (spmv.cpp:75-77)
+                seen = true;
+              }
+              sum = 0.0;
             }
-            sum = 0.0;
           }
-          sum = fma(v[u], xv[u], sum);
+          sum = fma(sv[j * 32 + lane], xv[u], sum);
         }
       }
     }
+    __syncwarp();
+    if (lane == 0 && k + S < ke) issue(k + S, s);  // refill this stage
+    if (++s == S) {
+      s = 0;
+      phase ^= 1u;
+    }
+
     // ---- splice across columns: tmp[i] = piece handed left by column i+1 ----
     const double give = seen ? red : sum;
     double tmp = __shfl_down_sync(kFull, give, 1);
@@ -162,33 +242,38 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(SpmvArgs a) {
       const double o = __shfl_down_sync(kFull, acc, d);
       if (lane + d <= end) acc += o;
     }
-    double cL = 0.0;
-    int64_t rL = 0;
-    if (seen) {
-      const int hbh = yoff + cnt - 1;  // head owning this column's bottom piece
-      const double blue = sum + acc;
-      const int64_t r = head_row(hbh);
-      if (hbh == 0) c0 = blue;
-      if (hbh == H - 1) {
-        cL = blue;
-        rL = r;
+    if (seen) closed[yoff + cnt - 1] = sum + acc;  // the column's bottom piece
+    __syncwarp();
+
+    // ---- write-back of the tile's heads in order ----
+    const double c0 = closed[0];
+    const double cL = closed[H - 1];
+    const int64_t rL = tile_row + (flagged ? (int64_t)eo[H - 1] : (int64_t)(H - 1));
+    int64_t defer_lo = 0, defer_hi = 0;
+    for (int h = lane; h < H; h += 32) {
+      const int64_t r = tile_row + (flagged ? (int64_t)eo[h] : (int64_t)h);
+      if (h != 0 && h != H - 1) y[r] = closed[h];
+      if (flagged || h == H - 1) {  // empty rows up to the next head (or next tile)
+        const int64_t nr = h + 1 < H ? tile_row + (int64_t)eo[h + 1] : next_row;
+        if (nr - r - 1 <= 8) {
+          for (int64_t q = r + 1; q < nr; ++q) y[q] = 0.0;
+        } else if (defer_hi == defer_lo) {
+          defer_lo = r + 1;
+          defer_hi = nr;
+        } else {
+          for (int64_t q = r + 1; q < nr; ++q) y[q] = 0.0;
+        }
       }
-      if (hbh != 0 && hbh != H - 1) y[r] = blue;
-      gap(hbh, r);
     }
-    // long empty-row runs: zero cooperatively
     uint32_t dm = __ballot_sync(kFull, defer_hi > defer_lo);
-    while (dm) {
+    while (dm) {  // long empty-row runs: zero cooperatively
       const int src = __ffs(dm) - 1;
       dm &= dm - 1;
       const int64_t lo = __shfl_sync(kFull, defer_lo, src);
       const int64_t hi = __shfl_sync(kFull, defer_hi, src);
       for (int64_t q = lo + lane; q < hi; q += 32) y[q] = 0.0;
     }
-    const int L = 31 - __clz(hb);
-    c0 = __shfl_sync(kFull, c0, 0);
-    cL = __shfl_sync(kFull, cL, L);
-    rL = __shfl_sync(kFull, rL, L);
+    __syncwarp();  // closed[] is rewritten by the next tile
 
     // ---- row runs across the warp's consecutive tiles ----
     auto flush = [&]() {
@@ -227,6 +312,8 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(SpmvArgs a) {
     }
   }
 }
+
+namespace {
 
 __device__ __forceinline__ void write_run(int64_t row, double v, double* y, int64_t first_row,
                                           int first_owned, csr5g_partial* send) {
@@ -299,16 +386,54 @@ __global__ void k_fixup(const csr5g_partial* __restrict__ all, int world, int ra
   y[row] = acc;
 }
 
-template <typename W>
-int occ(int* bps) {
-  CSR5G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_spmv<W>, kSpmvThreads, 0));
-  if (*bps < 1) *bps = 1;
-  return CSR5G_OK;
+using SpmvFn = void (*)(SpmvArgs);
+
+// sigma is 1..48 at omega = 32 (the 64-bit descriptor limit, descriptor.cpp:22-36)
+SpmvFn spmv_fn(int sigma) {
+  switch (sigma) {
+#define CSR5G_K(S) \
+  case S:          \
+    return k_spmv<S>;
+    CSR5G_K(1) CSR5G_K(2) CSR5G_K(3) CSR5G_K(4) CSR5G_K(5) CSR5G_K(6) CSR5G_K(7) CSR5G_K(8)
+    CSR5G_K(9) CSR5G_K(10) CSR5G_K(11) CSR5G_K(12) CSR5G_K(13) CSR5G_K(14) CSR5G_K(15)
+    CSR5G_K(16) CSR5G_K(17) CSR5G_K(18) CSR5G_K(19) CSR5G_K(20) CSR5G_K(21) CSR5G_K(22)
+    CSR5G_K(23) CSR5G_K(24) CSR5G_K(25) CSR5G_K(26) CSR5G_K(27) CSR5G_K(28) CSR5G_K(29)
+    CSR5G_K(30) CSR5G_K(31) CSR5G_K(32) CSR5G_K(33) CSR5G_K(34) CSR5G_K(35) CSR5G_K(36)
+    CSR5G_K(37) CSR5G_K(38) CSR5G_K(39) CSR5G_K(40) CSR5G_K(41) CSR5G_K(42) CSR5G_K(43)
+    CSR5G_K(44) CSR5G_K(45) CSR5G_K(46) CSR5G_K(47) CSR5G_K(48)
+#undef CSR5G_K
+    default:
+      return nullptr;
+  }
 }
 
 }  // namespace
 
-int spmv_occupancy(bool wide, int* bps) { return wide ? occ<uint64_t>(bps) : occ<uint32_t>(bps); }
+int spmv_plan(Handle* h, int sms) {
+  // Shared memory per warp: closed-segment slots (B doubles) + S ring stages.
+  // 8 warps per CTA, one CTA per SM, as many stages as fit (2..4); for very
+  // tall tiles drop warps rather than stages.
+  const int wbytes = h->wide ? 8 : 4;
+  const int64_t tile_bytes = h->B * 12 + 32 * wbytes;
+  const int stage_bytes = (int)((tile_bytes + 127) / 128 * 128);
+  const int closed_bytes = (int)(h->B * 8);
+  const int budget = 224 * 1024;
+  int nw = kSpmvWarpsPerBlock, stages = 4;
+  auto need = [&](int w, int st) { return 256 + w * (closed_bytes + st * stage_bytes); };
+  while (stages > 2 && need(nw, stages) > budget) --stages;
+  while (nw > 1 && need(nw, stages) > budget) --nw;
+  h->warps_per_block = nw;
+  h->stages = stages;
+  h->stage_bytes = stage_bytes;
+  h->bar_bytes = 256;  // nw * stages * 8 <= 256
+  h->smem_bytes = need(nw, stages);
+  CSR5G_CUDA(cudaFuncSetAttribute(spmv_fn((int)h->info.sigma),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
+  const int64_t max_warps = (int64_t)sms * nw;
+  h->nwarps = (int)std::min<int64_t>(max_warps, h->pcs);
+  h->tile_blocks = (h->nwarps + nw - 1) / nw;
+  return CSR5G_OK;
+}
 
 int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_t stream,
                 cudaEvent_t ev0, cudaEvent_t ev1) {
@@ -345,21 +470,22 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.tail_row_begin = h->tail_row_begin;
   a.tail_pos = h->tail_pos;
   a.m = in.m;
+  a.tile_ptr_len = in.tile_ptr_len;
   a.first_row = h->first_row;
   a.first_owned = h->first_owned;
   a.has_tail_item = h->has_tail_item;
   a.sigma = (int)in.sigma;
   a.B = (int)h->B;
   a.nwarps = h->nwarps;
-  a.rows_blocks = h->rows_blocks;
+  a.stages = h->stages;
+  a.stage_bytes = h->stage_bytes;
+  a.bar_bytes = h->bar_bytes;
   a.atomic = atomic;
-  const int grid = h->rows_blocks + h->tile_blocks;
+  const int grid = std::max(h->tile_blocks, h->rows_blocks);
+  const int threads = 32 * h->warps_per_block;
   if (ev0) CSR5G_CUDA(cudaEventRecord(ev0, stream));
   if (grid > 0) {
-    if (h->wide)
-      k_spmv<uint64_t><<<grid, kSpmvThreads, 0, stream>>>(a);
-    else
-      k_spmv<uint32_t><<<grid, kSpmvThreads, 0, stream>>>(a);
+    spmv_fn(a.sigma)<<<grid, threads, h->smem_bytes, stream>>>(a);
     CSR5G_CUDA(cudaGetLastError());
   }
   if (ev1) CSR5G_CUDA(cudaEventRecord(ev1, stream));
@@ -386,3 +512,4 @@ int launch_fixup(Handle* h, const csr5g_partial* d_all, int world, int rank, dou
 }
 
 }  // namespace csr5g
+
