@@ -164,6 +164,17 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
   int64_t eov = 0;
   int s = 0;
   uint32_t phase = 0;
+  // x gathers run one tile ahead: while tile k is reduced, the first CH
+  // gathers of tile k+1 (whose col_idx already sit in the next ring stage)
+  // are in flight.
+  auto gather = [&](int st_idx, double(&xv)[CH]) {
+    const int32_t* sc = reinterpret_cast<const int32_t*>(ring + (size_t)st_idx * a.stage_bytes + COL_OFF);
+#pragma unroll
+    for (int u = 0; u < CH; ++u) xv[u] = ld_keep(a.x + sc[u * 32 + lane], pol_x);
+  };
+  double xa[CH];
+  mbar_wait(bars, 0);
+  gather(0, xa);
 
   for (int64_t k = kb; k < ke; ++k) {
     const int slot = (int)((k - kb) & 31);
@@ -182,7 +193,13 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
     const int64_t next_row = (k + 1 == a.pcs) ? a.next_row_after : (int64_t)(tpn & 0x7fffffffu);
     const int32_t* __restrict__ eo = a.eo + eo_base;
 
-    mbar_wait(bars + s, phase);
+    const int sn = s + 1 == S ? 0 : s + 1;
+    const uint32_t pn = s + 1 == S ? phase ^ 1u : phase;
+    double xb[CH];
+    if (k + 1 < ke) {
+      mbar_wait(bars + sn, pn);
+      gather(sn, xb);
+    }
     const unsigned char* st = ring + (size_t)s * a.stage_bytes;
     const double* sv = reinterpret_cast<const double*>(st);
     const int32_t* sc = reinterpret_cast<const int32_t*>(st + COL_OFF);
@@ -200,9 +217,14 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
 #pragma unroll
     for (int j0 = 0; j0 < SIG; j0 += CH) {
       double xv[CH];
+      if (j0 == 0) {
 #pragma unroll
-      for (int u = 0; u < CH; ++u)
-        if (j0 + u < SIG) xv[u] = ld_keep(a.x + sc[(j0 + u) * 32 + lane], pol_x);
+        for (int u = 0; u < CH; ++u) xv[u] = xa[u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < CH; ++u)
+          if (j0 + u < SIG) xv[u] = ld_keep(a.x + sc[(j0 + u) * 32 + lane], pol_x);
+      }
 #pragma unroll
       for (int u = 0; u < CH; ++u) {
         const int j = j0 + u;
@@ -224,10 +246,10 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
     }
     __syncwarp();
     if (lane == 0 && k + S < ke) issue(k + S, s);  // refill this stage
-    if (++s == S) {
-      s = 0;
-      phase ^= 1u;
-    }
+    s = sn;
+    phase = pn;
+#pragma unroll
+    for (int u = 0; u < CH; ++u) xa[u] = xb[u];
 
     // ---- splice across columns: tmp[i] = piece handed left by column i+1 ----
     const double give = seen ? red : sum;
