@@ -155,6 +155,25 @@ CSR5G_API int csr5g_stencil_size(int32_t kind, int64_t a, int64_t *m, int64_t *n
 CSR5G_API int csr5g_stencil_fill(int32_t kind, int64_t a, int64_t *d_row_ptr, int32_t *d_col_idx,
                        double *d_val, void *stream);
 
+/* Irregular synthetic matrices on the device (BASELINE configs 3-5).  Two
+ * phases: *_create generates and sizes the matrix (m, nnz) and keeps it in a
+ * generator object; csr5g_gen_fill writes the CSR into caller buffers
+ * (row_ptr int64[m+1], col_idx int32[nnz], val f64[nnz]).
+ *  - R-MAT, Graph500 a,b,c,d = .57,.19,.19,.05, edge_factor * 2^scale edges,
+ *    duplicates removed, vertex labels permuted by a keyed bijection when
+ *    `permute` is set.
+ *  - mixed: m = n = 2^log2_m, rows empty with probability p_empty, n_long
+ *    rows of long_len nonzeros, the rest U[min_len, max_len] nonzeros. */
+typedef struct csr5g_gen_s *csr5g_gen;
+CSR5G_API int csr5g_rmat_create(int32_t scale, int32_t edge_factor, uint64_t seed, int32_t permute,
+                                void *stream, csr5g_gen *out, int64_t *m, int64_t *nnz);
+CSR5G_API int csr5g_mixed_create(int32_t log2_m, double p_empty, int32_t n_long, int64_t long_len,
+                                 int32_t min_len, int32_t max_len, uint64_t seed, void *stream,
+                                 csr5g_gen *out, int64_t *m, int64_t *nnz);
+CSR5G_API int csr5g_gen_fill(csr5g_gen g, int64_t *d_row_ptr, int32_t *d_col_idx, double *d_val,
+                             void *stream);
+CSR5G_API int csr5g_gen_release(csr5g_gen g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,12 @@ SIGNATURES = {
     "csr5g_event_destroy": (C.c_int, [_vp]),
     "csr5g_stencil_size": (C.c_int, [_i32, _i64, C.POINTER(_i64), C.POINTER(_i64)]),
     "csr5g_stencil_fill": (C.c_int, [_i32, _i64, _vp, _vp, _vp, _vp]),
+    "csr5g_rmat_create": (C.c_int, [_i32, _i32, C.c_uint64, _i32, _vp, C.POINTER(_vp),
+                                    C.POINTER(_i64), C.POINTER(_i64)]),
+    "csr5g_mixed_create": (C.c_int, [_i32, C.c_double, _i32, _i64, _i32, _i32, C.c_uint64, _vp,
+                                     C.POINTER(_vp), C.POINTER(_i64), C.POINTER(_i64)]),
+    "csr5g_gen_fill": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "csr5g_gen_release": (C.c_int, [_vp]),
 }
 
 _LIB = None

@@ -263,6 +263,41 @@ def stencil(kind: int, a: int, device="cuda", stream=None) -> CsrMatrix:
     return CsrMatrix(m.value, m.value, rp, ci, va)
 
 
+def _from_generator(gen: C.c_void_p, m: int, nnz: int, device, stream) -> CsrMatrix:
+    try:
+        rp = torch.empty(m + 1, dtype=torch.int64, device=device)
+        ci = torch.empty(nnz, dtype=torch.int32, device=device)
+        va = torch.empty(nnz, dtype=torch.float64, device=device)
+        check(lib().csr5g_gen_fill(gen, rp.data_ptr(), ci.data_ptr(), va.data_ptr(),
+                                   _stream_ptr(stream)))
+        torch.cuda.synchronize(device)
+    finally:
+        lib().csr5g_gen_release(gen)
+    return CsrMatrix(m, m, rp, ci, va)
+
+
+def rmat(scale: int, edge_factor: int = 16, seed: int = 1, permute: bool = True,
+         device="cuda", stream=None) -> CsrMatrix:
+    """Graph500 R-MAT (a,b,c,d = .57,.19,.19,.05), duplicates removed."""
+    g, m, nnz = C.c_void_p(), C.c_int64(), C.c_int64()
+    with torch.cuda.device(torch.device(device)):
+        check(lib().csr5g_rmat_create(scale, edge_factor, seed, int(permute), _stream_ptr(stream),
+                                      C.byref(g), C.byref(m), C.byref(nnz)))
+        return _from_generator(g, m.value, nnz.value, device, stream)
+
+
+def mixed(log2_m: int = 23, p_empty: float = 0.4, n_long: int = 4, long_len: int = 1 << 20,
+          min_len: int = 1, max_len: int = 32, seed: int = 1, device="cuda",
+          stream=None) -> CsrMatrix:
+    """40% empty rows plus a few 1M-nnz rows."""
+    g, m, nnz = C.c_void_p(), C.c_int64(), C.c_int64()
+    with torch.cuda.device(torch.device(device)):
+        check(lib().csr5g_mixed_create(log2_m, p_empty, n_long, long_len, min_len, max_len, seed,
+                                       _stream_ptr(stream), C.byref(g), C.byref(m),
+                                       C.byref(nnz)))
+        return _from_generator(g, m.value, nnz.value, device, stream)
+
+
 class Event:
     """cudaEvent from libcsr5g (timing on the launching stream)."""
 

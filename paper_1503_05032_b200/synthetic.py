@@ -62,8 +62,32 @@ def bench_x(n: int, seed: int = 1) -> np.ndarray:
 
 
 WORKLOADS = {
-    "st27_200": dict(kind=1, a=200, desc="3D 27-point stencil 200^3 (8M rows, 213.8M nnz), "
-                                          "values 26/-1"),
-    "lap5_1000": dict(kind=0, a=1000, desc="2D 5-point Laplacian 1000^2 (1M rows, 4.996M nnz), "
-                                            "values 4/-1"),
+    "st27_200": dict(gen="stencil", kind=1, a=200,
+                     desc="3D 27-point stencil 200^3 (8M rows, 213.8M nnz), values 26/-1"),
+    "lap5_1000": dict(gen="stencil", kind=0, a=1000,
+                      desc="2D 5-point Laplacian 1000^2 (1M rows, 4.996M nnz), values 4/-1"),
+    "rmat24": dict(gen="rmat", scale=24, edge_factor=16, permute=True, seed=1,
+                   desc="R-MAT scale 24, edge factor 16, Graph500 .57/.19/.19/.05, dedup, "
+                        "vertices permuted, values U[0.5,1.5)"),
+    "rmat24_raw": dict(gen="rmat", scale=24, edge_factor=16, permute=False, seed=1,
+                       desc="R-MAT scale 24, edge factor 16, Graph500, dedup, unpermuted"),
+    "mixed23": dict(gen="mixed", log2_m=23, p_empty=0.4, n_long=4, long_len=1 << 20,
+                    min_len=1, max_len=32, seed=1,
+                    desc="mixed 2^23 x 2^23: 40% empty rows, 4 rows of 1,048,576 nnz, others "
+                         "U[1,32] nnz, values U[0.5,1.5)"),
+    "rmat27": dict(gen="rmat", scale=27, edge_factor=16, permute=True, seed=1,
+                   desc="R-MAT scale 27, edge factor 16, Graph500, dedup, vertices permuted"),
 }
+
+
+def make_matrix(wl: dict, device="cuda"):
+    """The workload's CSR, generated on the device by libcsr5g."""
+    from . import csr5
+    if wl["gen"] == "stencil":
+        return csr5.stencil(wl["kind"], wl["a"], device=device)
+    if wl["gen"] == "rmat":
+        return csr5.rmat(wl["scale"], wl["edge_factor"], wl["seed"], wl["permute"], device=device)
+    if wl["gen"] == "mixed":
+        return csr5.mixed(wl["log2_m"], wl["p_empty"], wl["n_long"], wl["long_len"],
+                          wl["min_len"], wl["max_len"], wl["seed"], device=device)
+    raise ValueError(f"unknown generator {wl['gen']!r}")
