@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <new>
 
 #include "internal.cuh"
@@ -206,11 +208,28 @@ __global__ void k_untranspose(const int32_t* __restrict__ col_in, const double* 
   val_out[idx] = val_in[src];
 }
 
+// Handle memory comes from the device's stream-ordered pool with an unbounded
+// release threshold: a rebuild after a release reuses the pages instead of
+// paying cudaMalloc's page mapping again (allocation is reported separately,
+// as the paper separates it from conversion).
+thread_local cudaStream_t t_alloc_stream = nullptr;
+
+int ensure_pool(int device) {
+  static bool done[64] = {};
+  if (device < 64 && done[device]) return CSR5G_OK;
+  cudaMemPool_t pool;
+  CSR5G_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = ~uint64_t(0);
+  CSR5G_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  if (device < 64) done[device] = true;
+  return CSR5G_OK;
+}
+
 template <typename T>
 int dev_alloc(T** p, size_t count, double* alloc_ms, int64_t* bytes) {
   const auto t0 = std::chrono::steady_clock::now();
   const size_t nb = std::max<size_t>(count * sizeof(T), 16);
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), nb);
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), nb, t_alloc_stream);
   *alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -220,6 +239,31 @@ int dev_alloc(T** p, size_t count, double* alloc_ms, int64_t* bytes) {
   *bytes += (int64_t)nb;
   return CSR5G_OK;
 }
+
+// CSR5G_TRACE=1: synchronise after each build phase and print the phase times
+// to stderr (a profiling aid; off by default, no syncs added when off).
+struct BuildTrace {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point last;
+  std::string log;
+  explicit BuildTrace(cudaStream_t s) : on(std::getenv("CSR5G_TRACE") != nullptr), st(s) {
+    last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    char buf[96];
+    std::snprintf(buf, sizeof buf, " %s=%.3fms", what,
+                  std::chrono::duration<double, std::milli>(t - last).count());
+    log += buf;
+    last = t;
+  }
+  ~BuildTrace() {
+    if (on) std::fprintf(stderr, "[csr5g build]%s\n", log.c_str());
+  }
+};
 
 int check_params(const csr5g_params* pr, int64_t m, int64_t nnz, bool shard, int64_t* sigma_out,
                  int32_t* yb, int32_t* sb, int32_t* wb) {
@@ -258,16 +302,11 @@ void free_handle(Handle* h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
-  cudaFree(h->row_ptr);
-  cudaFree(h->tile_ptr);
-  cudaFree(h->desc);
-  cudaFree(h->eo_ptr);
-  cudaFree(h->eo);
-  cudaFree(h->col);
-  cudaFree(h->val);
-  cudaFree(h->item_row);
-  cudaFree(h->item_val);
-  cudaFree(h->send);
+  for (void* p : {(void*)h->row_ptr, (void*)h->tile_ptr, h->desc, (void*)h->eo_ptr, (void*)h->eo,
+                  (void*)h->col, (void*)h->val, (void*)h->item_row, (void*)h->item_val,
+                  (void*)h->send, (void*)h->spill})
+    if (p) cudaFreeAsync(p, 0);
+  cudaDeviceSynchronize();
   cudaSetDevice(prev);
   delete h;
 }
@@ -315,6 +354,12 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   const int64_t last_ptr = is_last ? p : tile_end;
   const int64_t tile_ptr_len = m > 0 ? last_ptr - tile_begin + 1 : 1;
 
+  BuildTrace trace(stream);
+  {
+    const int prc = ensure_pool(device);
+    if (prc) return prc;
+  }
+  t_alloc_stream = stream;
   auto* h = new (std::nothrow) Handle();
   if (!h) return fail(CSR5G_ENOMEM, "csr5g: host allocation failed");
   h->device = device;
@@ -330,11 +375,8 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   int64_t* scal = nullptr;
   void* cub_tmp = nullptr;
   auto cleanup = [&](int code) {
-    cudaFree(head_bits);
-    cudaFree(empty_bits);
-    cudaFree(eo_cnt);
-    cudaFree(scal);
-    cudaFree(cub_tmp);
+    for (void* p : {(void*)head_bits, (void*)empty_bits, (void*)eo_cnt, (void*)scal, cub_tmp})
+      if (p) cudaFreeAsync(p, stream);
     if (code) free_handle(h);
     return code;
   };
@@ -365,6 +407,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRY(dev_alloc(&eo_cnt, (size_t)pcs + 1, &alloc_ms, &tmp_bytes));
   TRY(dev_alloc(&scal, 8, &alloc_ms, &tmp_bytes));
 
+  trace.mark("alloc");
   if (m > 0) TRYC(cudaMemcpyAsync(h->row_ptr, d_row_ptr, sizeof(int64_t) * (m + 1),
                                   cudaMemcpyDeviceToDevice, stream));
   TRYC(cudaMemsetAsync(head_bits, 0, sizeof(uint32_t) * head_words, stream));
@@ -374,16 +417,19 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRYC(cudaMemcpyAsync(h->send, &none, sizeof none, cudaMemcpyHostToDevice, stream));
 
   const int64_t pos0 = tile_begin * B;
+  trace.mark("init");
   if (m > 0) {
     k_rowscan<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(h->row_ptr, m, pos0, pos0 + pcs * B,
                                                                empty_bits, head_bits);
     TRYC(cudaGetLastError());
+    trace.mark("rowscan");
     k_tile_ptr<<<(unsigned)((tile_ptr_len + 255) / 256), 256, 0, stream>>>(
         h->row_ptr, m, B, p, tile_begin, tile_ptr_len, empty_bits, h->tile_ptr);
     TRYC(cudaGetLastError());
   } else {
     TRYC(cudaMemsetAsync(h->tile_ptr, 0, sizeof(uint32_t), stream));  // encode_tile_ptr(0)
   }
+  trace.mark("tile_ptr");
   if (pcs > 0) {
     const size_t smem = (size_t)4 * sigma * 33 * sizeof(double);
     const unsigned grid = (unsigned)((pcs + 3) / 4);
@@ -408,6 +454,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     TRYC(cudaMemcpyAsync(h->val + pcs * B, d_val + pcs * B, sizeof(double) * tail,
                          cudaMemcpyDeviceToDevice, stream));
   }
+  trace.mark("desc_transpose");
   // empty_offset_ptr: exclusive scan of per-tile head counts (format.cpp:213-217)
   size_t cub_bytes = 0;
   TRYC(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, eo_cnt, h->eo_ptr, (int)(pcs + 1), stream));
@@ -422,6 +469,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRYC(cudaMemcpyAsync(&tpc, h->tile_ptr + (pcs < tile_ptr_len ? pcs : tile_ptr_len - 1),
                        sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
   TRYC(cudaStreamSynchronize(stream));
+  trace.mark("scan");
   ptr_first = tp0 & 0x7fffffffu;
   ptr_close = tpc & 0x7fffffffu;
   // queries: g0 = last position of the held complete tiles, g1 = nnz - 1;
@@ -442,6 +490,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     TRYC(cudaGetLastError());
   }
   TRYC(cudaStreamSynchronize(stream));
+  trace.mark("eo");
 
   // ---- SpMV plan ----
   const bool is_first = tile_begin == 0;
@@ -467,6 +516,8 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   const int64_t items = 2 * (int64_t)h->nwarps + 1;
   TRY(dev_alloc(&h->item_row, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->item_val, (size_t)items, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->spill, (size_t)std::max(h->nwarps, 1) * B, &alloc_ms, &bytes));
+  trace.mark("plan");
 
   // ---- info ----
   csr5g_info& in = h->info;

@@ -41,6 +41,7 @@ struct SpmvArgs {
   int64_t* item_row;
   double* item_val;
   csr5g_partial* send;
+  double* spill;           // per-warp overflow slots for closed segment sums
   int64_t pcs;             // complete tiles held
   int64_t pos0;            // global nonzero position of local index 0
   int64_t next_row_after;  // first row after the last held complete tile's range
@@ -77,6 +78,7 @@ struct Handle {
   double* item_val = nullptr;
   csr5g_partial* send = nullptr;
   csr5g_partial* send_ext = nullptr;  // caller-provided record slot
+  double* spill = nullptr;            // nwarps * B doubles
   int64_t next_row_after = 0, lead_rows = 0, tail_row_begin = 0, tail_pos = 0;
   int64_t first_row = 0, last_row = 0;
   bool first_owned = true, is_last = true, has_tail_item = false;

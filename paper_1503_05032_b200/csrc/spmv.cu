@@ -209,6 +209,13 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
     const int cnt = __popcll(fr);
     const int H = __shfl_sync(kFull, yoff + cnt, 31);
     const uint64_t anyf = warp_or64(fr);
+    // the first 64 empty_offset entries of a flagged tile, in flight during
+    // the depth loop and consumed by the write-back
+    int32_t eo_0 = 0, eo_1 = 0;
+    if (flagged) {
+      if (lane < H) eo_0 = eo[lane];
+      if (lane + 32 < H) eo_1 = eo[lane + 32];
+    }
 
     // ---- depth loop: gathers first, then FMAs; closes go to closed[head] ----
     double sum = 0.0, red = 0.0;
@@ -270,13 +277,28 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
     // ---- write-back of the tile's heads in order ----
     const double c0 = closed[0];
     const double cL = closed[H - 1];
-    const int64_t rL = tile_row + (flagged ? (int64_t)eo[H - 1] : (int64_t)(H - 1));
+    int64_t rL = 0;
     int64_t defer_lo = 0, defer_hi = 0;
-    for (int h = lane; h < H; h += 32) {
-      const int64_t r = tile_row + (flagged ? (int64_t)eo[h] : (int64_t)h);
+    const int nch = (H + 31) >> 5;
+#pragma unroll 1
+    for (int c = 0; c < nch; ++c) {  // warp-uniform trip count
+      const int h = lane + 32 * c;
+      // empty_offset of heads h and h+1: the first 64 come from registers
+      // loaded before the depth loop, later ones from memory
+      int32_t e_here = 0, e_next = 0;
+      if (flagged) {
+        const int32_t cur = c == 0 ? eo_0 : (c == 1 ? eo_1 : (h < H ? eo[h] : 0));
+        const int32_t nxt0 = c == 0 ? __shfl_sync(kFull, eo_1, 0) : 0;
+        const int32_t dn = __shfl_down_sync(kFull, cur, 1);
+        e_here = cur;
+        e_next = lane < 31 ? dn : (c == 0 ? nxt0 : (h + 1 < H ? eo[h + 1] : 0));
+      }
+      if (h >= H) continue;
+      const int64_t r = tile_row + (flagged ? (int64_t)e_here : (int64_t)h);
+      if (h == H - 1) rL = r;
       if (h != 0 && h != H - 1) y[r] = closed[h];
       if (flagged || h == H - 1) {  // empty rows up to the next head (or next tile)
-        const int64_t nr = h + 1 < H ? tile_row + (int64_t)eo[h + 1] : next_row;
+        const int64_t nr = h + 1 < H ? tile_row + (int64_t)e_next : next_row;
         if (nr - r - 1 <= 8) {
           for (int64_t q = r + 1; q < nr; ++q) y[q] = 0.0;
         } else if (defer_hi == defer_lo) {
@@ -287,6 +309,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
         }
       }
     }
+    rL = __shfl_sync(kFull, rL, (H - 1) & 31);
     uint32_t dm = __ballot_sync(kFull, defer_hi > defer_lo);
     while (dm) {  // long empty-row runs: zero cooperatively
       const int src = __ffs(dm) - 1;
