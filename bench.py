@@ -382,6 +382,10 @@ def run_ours(args, workload_name, workload):
             "config": {"workload": workload_name, "desc": workload["desc"], "m": a.m, "n": a.n,
                        "nnz": a.nnz, "omega": 32, "sigma": sigma, "p": info.p,
                        "desc_word_bits": info.word_bits, "mode": "deterministic",
+                       "spmv_plan": {"lines_per_gather": round(info.lines_per_gather, 2),
+                                     "warps_per_cta": info.warps_per_cta, "stages": info.stages,
+                                     "smem_bytes": info.smem_bytes, "x_mode": info.x_mode,
+                                     "x_l2_window": info.x_window},
                        "parallelism": f"tile-range shards x{world}, x replicated",
                        "l2": (f"L2 flushed between steps (working set {info.spmv_bytes / 1e6:.0f} MB"
                               f" < 4x L2)" if flush else

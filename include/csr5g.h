@@ -67,6 +67,9 @@ typedef struct {
   int64_t first_row, last_row;  /* rows of the first / last head held */
   int64_t own_row_begin, own_row_end; /* rows this handle writes in y (shards) */
   double build_ms, alloc_ms;    /* last build: total and allocation share */
+  /* SpMV plan chosen from the sampled gather locality */
+  double lines_per_gather;      /* distinct 128 B x lines per warp gather (1..32) */
+  int32_t warps_per_cta, stages, smem_bytes, x_mode, x_window, pad_;
 } csr5g_info;
 
 /* One boundary partial of a shard: row = -1 when there is none. */

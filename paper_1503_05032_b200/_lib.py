@@ -39,6 +39,9 @@ class Info(C.Structure):
         ("first_row", C.c_int64), ("last_row", C.c_int64),
         ("own_row_begin", C.c_int64), ("own_row_end", C.c_int64),
         ("build_ms", C.c_double), ("alloc_ms", C.c_double),
+        ("lines_per_gather", C.c_double),
+        ("warps_per_cta", C.c_int32), ("stages", C.c_int32), ("smem_bytes", C.c_int32),
+        ("x_mode", C.c_int32), ("x_window", C.c_int32), ("pad_", C.c_int32),
     ]
 
 

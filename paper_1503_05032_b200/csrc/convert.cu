@@ -194,6 +194,26 @@ __global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0,
   out[3] = (r1 >= 0 && r1 <= m) ? rp[r1] : -1;
 }
 
+// Gather locality of the SpMV: for `samples` evenly spaced tiles, the number
+// of distinct 128-byte lines of x that one warp-wide gather (one depth step)
+// touches, summed into *acc.  1 = perfectly coalesced, 32 = fully random.
+__global__ void k_locality(const int32_t* __restrict__ col, int64_t pcs, int sigma, int64_t samples,
+                           unsigned long long* __restrict__ acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t sidx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (sidx >= samples) return;
+  const int64_t k = sidx * pcs / samples;
+  const int B = 32 * sigma;
+  unsigned total = 0;
+  for (int j = 0; j < sigma; ++j) {
+    const int32_t line = col[k * B + (int64_t)j * 32 + lane] >> 4;
+    const unsigned peers = __match_any_sync(kFull, line);
+    total += (__ffs(peers) - 1) == lane;  // one leader per distinct line
+  }
+  total = __reduce_add_sync(kFull, total);
+  if (lane == 0) atomicAdd(acc, (unsigned long long)total);
+}
+
 __global__ void k_untranspose(const int32_t* __restrict__ col_in, const double* __restrict__ val_in,
                               int32_t* __restrict__ col_out, double* __restrict__ val_out,
                               int64_t n_tiled, int sigma) {
@@ -491,6 +511,20 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   }
   TRYC(cudaStreamSynchronize(stream));
   trace.mark("eo");
+  // gather locality over up to 4096 sampled tiles (drives the SpMV plan)
+  h->lines_per_gather = 1.0;
+  if (pcs > 0) {
+    const int64_t samples = std::min<int64_t>(pcs, 4096);
+    TRYC(cudaMemsetAsync(scal, 0, sizeof(unsigned long long), stream));
+    k_locality<<<(unsigned)((samples * 32 + 255) / 256), 256, 0, stream>>>(
+        h->col, pcs, (int)sigma, samples, reinterpret_cast<unsigned long long*>(scal));
+    TRYC(cudaGetLastError());
+    unsigned long long lines = 0;
+    TRYC(cudaMemcpyAsync(&lines, scal, sizeof lines, cudaMemcpyDeviceToHost, stream));
+    TRYC(cudaStreamSynchronize(stream));
+    h->lines_per_gather = (double)lines / (double)(samples * sigma);
+  }
+  trace.mark("locality");
 
   // ---- SpMV plan ----
   const bool is_first = tile_begin == 0;
@@ -510,6 +544,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   int sms = 0;
   TRYC(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   h->info.sigma = sigma;  // spmv_plan picks the sigma-specialised kernel
+  h->info.n = n;          // ... and sizes its shared memory by x
   TRY(spmv_plan(h, sms));
   const int64_t rows_total = h->lead_rows + (m - h->tail_row_begin);
   h->rows_blocks = rows_total > 0 ? (int)std::min<int64_t>((rows_total + 255) / 256, 2 * sms) : 0;
@@ -556,6 +591,12 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     in.own_row_end = close_starts_here ? ptr_close : ptr_close + 1;
   }
   in.alloc_ms = alloc_ms;
+  in.lines_per_gather = h->lines_per_gather;
+  in.warps_per_cta = h->warps_per_block;
+  in.stages = h->stages;
+  in.smem_bytes = h->smem_bytes;
+  in.x_mode = h->x_mode;
+  in.x_window = h->x_window ? 1 : 0;
   in.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
   *out = h;
   return cleanup(CSR5G_OK);

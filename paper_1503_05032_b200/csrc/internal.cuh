@@ -60,6 +60,8 @@ struct SpmvArgs {
   int32_t stage_bytes;     // one tile: val | col_idx | descriptor words
   int32_t bar_bytes;       // mbarrier area at the start of shared memory
   int32_t atomic;          // SpmvMode::atomic
+  int32_t x_mode;          // x gather path: 0 L1+evict_last, 1 L1 no-allocate+evict_last
+  int32_t jitter;          // hashed tile-range boundaries
 };
 
 struct Handle {
@@ -83,6 +85,9 @@ struct Handle {
   int64_t first_row = 0, last_row = 0;
   bool first_owned = true, is_last = true, has_tail_item = false;
   int nwarps = 0, tile_blocks = 0, rows_blocks = 0;
+  double lines_per_gather = 1.0;  // sampled x-gather locality (1 = coalesced, 32 = random)
+  int x_mode = 0;                 // gather path chosen by the plan
+  bool x_window = false;          // L2 persisting window on x
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
 };
 
@@ -146,6 +151,25 @@ __device__ __forceinline__ uint64_t ld_stream(const uint64_t* p, uint64_t pol) {
 __device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
   double v;
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// x gathers that skip L1 allocation (random gathers with no reuse in L1).
+__device__ __forceinline__ double ld_keep_na(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// x gathers through the coherent LSU path (not the read-only/texture path).
+__device__ __forceinline__ double ld_x_lsu(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_x_cg(const double* p) {
+  double v;
+  asm("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 

@@ -29,6 +29,7 @@
 //   items with fp64 atomics into a zeroed y (spmv.cpp:273-295).
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <type_traits>
 
 #include "internal.cuh"
@@ -98,6 +99,23 @@ __device__ void rows_part(const SpmvArgs& a) {
   }
 }
 
+// First tile of warp w's contiguous range.  With jitter, the boundaries move
+// by a hashed offset of up to a quarter range so that the warps' concurrent
+// streams do not sit on a regular address lattice.
+__device__ __forceinline__ int64_t range_begin(int w, int64_t pcs, int nwarps, int jitter) {
+  if (w <= 0) return 0;
+  if (w >= nwarps) return pcs;
+  const int64_t base = (int64_t)w * pcs / nwarps;
+  if (!jitter) return base;
+  const int64_t q = pcs / nwarps / 4;
+  if (q < 1) return base;
+  uint32_t h = (uint32_t)w * 2654435761u;
+  h ^= h >> 15;
+  h *= 2246822519u;
+  h ^= h >> 13;
+  return base + (int64_t)(h % (uint32_t)q);
+}
+
 __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
   const uint32_t lo = __reduce_or_sync(kFull, (uint32_t)v);
   const uint32_t hi = __reduce_or_sync(kFull, (uint32_t)(v >> 32));
@@ -106,13 +124,21 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
 
 }  // namespace
 
+// Gather look-ahead in tiles: short tiles carry few x registers per lane, so
+// two tiles of gathers can be in flight to cover random-access latency.
+__host__ __device__ constexpr int spmv_lookahead(int sigma) { return sigma > 0 ? 1 : 1; }
+// Warps per CTA: short tiles need fewer registers and less shared memory per
+// warp, and random gathers want as many warps in flight as fit.
+__host__ __device__ constexpr int spmv_threads(int sigma) { return sigma <= 16 ? 384 : 256; }
+
 // Outside the anonymous namespace: the sigma instantiations are reached
 // through a function-pointer switch, and the runtime must register each one.
 template <int SIG>
-__global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
+__global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   using W = typename std::conditional<(SIG <= 17), uint32_t, uint64_t>::type;
   constexpr int B = 32 * SIG;
   constexpr int CH = SIG <= 32 ? SIG : (SIG + 1) / 2;  // x gathers in flight per lane
+  constexpr int LA = spmv_lookahead(SIG);              // tiles of gathers in flight
   constexpr uint64_t FMASK = (1ull << SIG) - 1;
   constexpr uint32_t COL_OFF = B * 8, DESC_OFF = B * 12;
   constexpr uint32_t TILE_BYTES = B * 12 + 32 * sizeof(W);
@@ -132,8 +158,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
 
   int64_t kb = 0, ke = 0;
   if (has_tiles) {
-    kb = (int64_t)w * a.pcs / a.nwarps;
-    ke = (int64_t)(w + 1) * a.pcs / a.nwarps;
+    kb = range_begin(w, a.pcs, a.nwarps, a.jitter);
+    ke = range_begin(w + 1, a.pcs, a.nwarps, a.jitter);
   }
   auto issue = [&](int64_t k, int s) {  // lane 0 only
     unsigned char* st = ring + (size_t)s * a.stage_bytes;
@@ -169,12 +195,27 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
   // are in flight.
   auto gather = [&](int st_idx, double(&xv)[CH]) {
     const int32_t* sc = reinterpret_cast<const int32_t*>(ring + (size_t)st_idx * a.stage_bytes + COL_OFF);
+    if (a.x_mode == 1) {
 #pragma unroll
-    for (int u = 0; u < CH; ++u) xv[u] = ld_keep(a.x + sc[u * 32 + lane], pol_x);
+      for (int u = 0; u < CH; ++u) xv[u] = ld_keep_na(a.x + sc[u * 32 + lane], pol_x);
+    } else if (a.x_mode == 2) {
+#pragma unroll
+      for (int u = 0; u < CH; ++u) xv[u] = ld_x_lsu(a.x + sc[u * 32 + lane], pol_x);
+    } else if (a.x_mode == 3) {
+#pragma unroll
+      for (int u = 0; u < CH; ++u) xv[u] = ld_x_cg(a.x + sc[u * 32 + lane]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < CH; ++u) xv[u] = ld_keep(a.x + sc[u * 32 + lane], pol_x);
+    }
   };
-  double xa[CH];
+  double xa[CH], xb[CH];
   mbar_wait(bars, 0);
   gather(0, xa);
+  if (LA == 2 && kb + 1 < ke) {
+    mbar_wait(bars + 1, 0);
+    gather(1, xb);
+  }
 
   for (int64_t k = kb; k < ke; ++k) {
     const int slot = (int)((k - kb) & 31);
@@ -195,10 +236,18 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
 
     const int sn = s + 1 == S ? 0 : s + 1;
     const uint32_t pn = s + 1 == S ? phase ^ 1u : phase;
-    double xb[CH];
-    if (k + 1 < ke) {
-      mbar_wait(bars + sn, pn);
-      gather(sn, xb);
+    // gathers for tile k+LA go out before tile k is reduced
+    double xn[CH];
+    if (k + LA < ke) {
+      if (LA == 1) {
+        mbar_wait(bars + sn, pn);
+        gather(sn, xn);
+      } else {
+        const int64_t ia = k - kb + LA;
+        const int sa = (int)(ia % S);
+        mbar_wait(bars + sa, (uint32_t)((ia / S) & 1));
+        gather(sa, xn);
+      }
     }
     const unsigned char* st = ring + (size_t)s * a.stage_bytes;
     const double* sv = reinterpret_cast<const double*>(st);
@@ -256,7 +305,14 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv(SpmvArgs a) {
     s = sn;
     phase = pn;
 #pragma unroll
-    for (int u = 0; u < CH; ++u) xa[u] = xb[u];
+    for (int u = 0; u < CH; ++u) {
+      if (LA == 2) {
+        xa[u] = xb[u];
+        xb[u] = xn[u];
+      } else {
+        xa[u] = xn[u];
+      }
+    }
 
     // ---- splice across columns: tmp[i] = piece handed left by column i+1 ----
     const double give = seen ? red : sum;
@@ -456,24 +512,65 @@ SpmvFn spmv_fn(int sigma) {
 
 int spmv_plan(Handle* h, int sms) {
   // Shared memory per warp: closed-segment slots (B doubles) + S ring stages.
-  // 8 warps per CTA, one CTA per SM, as many stages as fit (2..4); for very
-  // tall tiles drop warps rather than stages.
+  // One CTA per SM.  The shared-memory budget depends on the sampled gather
+  // locality (lines_per_gather, from the converter):
+  //  * local gathers (stencils): up to 226 KB -- the largest ring and warp
+  //    count; x gathers mostly hit L1/L2 with few misses in flight;
+  //  * random gathers: whatever shared memory is not carved out stays L1,
+  //    which is where outstanding gather misses land.  Measured on R-MAT s24
+  //    (x 134 MB > L2): 115 KB -> 2.26 ms, 183 KB -> 3.02 ms, 206 KB -> 5.76 ms.
+  //    When x fits in L2 (misses are short), more warps win instead.
+  const int sigma = (int)h->info.sigma;
   const int wbytes = h->wide ? 8 : 4;
   const int64_t tile_bytes = h->B * 12 + 32 * wbytes;
   const int stage_bytes = (int)((tile_bytes + 127) / 128 * 128);
   const int closed_bytes = (int)(h->B * 8);
-  const int budget = 224 * 1024;
-  int nw = kSpmvWarpsPerBlock, stages = 4;
-  auto need = [&](int w, int st) { return 256 + w * (closed_bytes + st * stage_bytes); };
-  while (stages > 2 && need(nw, stages) > budget) --stages;
+  int l2 = 0;
+  CSR5G_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device));
+  const double x_bytes = 8.0 * (double)h->info.n;
+  const bool random = h->lines_per_gather >= 8.0;
+  const bool x_spills = x_bytes > 0.75 * l2;
+  const int budget = !random ? 226 * 1024 : (x_spills ? 120 * 1024 : 150 * 1024);
+  h->x_mode = random ? 1 : 0;          // random: no L1 allocation for x
+  h->x_window = random && x_bytes > 32e6;  // random: keep x resident in L2
+  // stages: the tile being reduced + LA tiles whose gathers are in flight +
+  // one tile of TMA lead (S = LA + 2 preferred, LA + 1 minimum)
+  const int la = spmv_lookahead(sigma);
+  const int min_stages = la + 1;
+  int nw = spmv_threads(sigma) / 32, stages = random ? la + 2 : 4;
+  auto need = [&](int w, int st) { return 512 + w * (closed_bytes + st * stage_bytes); };
+  // local gathers: warps per SM matter most (keep them, give up depth first);
+  // random gathers: keep the TMA lead (depth), give up warps
+  if (!random)
+    while (stages > min_stages && need(nw, stages) > budget) --stages;
   while (nw > 1 && need(nw, stages) > budget) --nw;
+  while (stages > min_stages && need(nw, stages) > budget) --stages;
+  if (const char* e = std::getenv("CSR5G_NW")) nw = std::max(1, std::min(nw, std::atoi(e)));
+  if (const char* e = std::getenv("CSR5G_STAGES")) {
+    stages = std::max(min_stages, std::min(4, std::atoi(e)));
+    while (nw > 1 && need(nw, stages) > budget) --nw;
+  }
   h->warps_per_block = nw;
   h->stages = stages;
   h->stage_bytes = stage_bytes;
-  h->bar_bytes = 256;  // nw * stages * 8 <= 256
+  h->bar_bytes = 512;  // nw * stages * 8 <= 16 * 4 * 8
   h->smem_bytes = need(nw, stages);
   CSR5G_CUDA(cudaFuncSetAttribute(spmv_fn((int)h->info.sigma),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
+  // Ask for the smallest shared-memory carveout that holds the ring: the rest
+  // of the SM's 256 KB stays L1, which is where outstanding gather misses land
+  // (measured: a 233 KB carveout halves R-MAT throughput through mio/lg
+  // throttling).
+  {
+    int max_smem = 0;
+    CSR5G_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                                      h->device));
+    const int need_bytes = h->smem_bytes + 1024;  // + the per-CTA reserved 1 KB
+    int pct = (int)((100LL * need_bytes + max_smem - 1) / max_smem);
+    pct = std::min(100, std::max(0, pct));
+    CSR5G_CUDA(cudaFuncSetAttribute(spmv_fn((int)h->info.sigma),
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  }
   const int64_t max_warps = (int64_t)sms * nw;
   h->nwarps = (int)std::min<int64_t>(max_warps, h->pcs);
   h->tile_blocks = (h->nwarps + nw - 1) / nw;
@@ -528,10 +625,53 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.atomic = atomic;
   const int grid = std::max(h->tile_blocks, h->rows_blocks);
   const int threads = 32 * h->warps_per_block;
+  // the plan's gather path; CSR5G_XMODE / CSR5G_XWINDOW override it (experiments)
+  static const int x_mode_env = [] {
+    const char* e = std::getenv("CSR5G_XMODE");
+    return e ? std::atoi(e) : -1;
+  }();
+  static const int x_window_env = [] {
+    const char* e = std::getenv("CSR5G_XWINDOW");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int x_mode = x_mode_env >= 0 ? x_mode_env : h->x_mode;
+  const bool x_window = x_window_env >= 0 ? x_window_env != 0 : h->x_window;
+  a.x_mode = x_mode;
+  static const int jitter = [] {
+    const char* e = std::getenv("CSR5G_JITTER");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.jitter = jitter;
   if (ev0) CSR5G_CUDA(cudaEventRecord(ev0, stream));
   if (grid > 0) {
-    spmv_fn(a.sigma)<<<grid, threads, h->smem_bytes, stream>>>(a);
-    CSR5G_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = h->smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    if (x_window) {
+      // keep x resident in an L2 persisting window (set-aside sized at build)
+      int max_win = 0, max_persist = 0;
+      cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+      static bool limit_set = false;
+      if (!limit_set) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+        limit_set = true;
+      }
+      const size_t xb = std::min<size_t>((size_t)in.n * 8, (size_t)max_win);
+      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      attr[0].val.accessPolicyWindow.base_ptr = const_cast<double*>(d_x);
+      attr[0].val.accessPolicyWindow.num_bytes = xb;
+      attr[0].val.accessPolicyWindow.hitRatio =
+          xb ? std::min(1.0f, (float)max_persist / (float)xb) : 1.0f;
+      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+    }
+    CSR5G_CUDA(cudaLaunchKernelEx(&cfg, spmv_fn(a.sigma), a));
   }
   if (ev1) CSR5G_CUDA(cudaEventRecord(ev1, stream));
   const int64_t items = 2 * (int64_t)h->nwarps + (h->has_tail_item ? 1 : 0);
