@@ -67,6 +67,16 @@ def owned_ranges(infos) -> list[tuple[int, int]]:
     return [(int(i.own_row_begin), int(i.own_row_end)) for i in infos]
 
 
+def exchange_records(dist, send, world: int, group=None):
+    """All-gather every rank's 16-byte boundary record (int64 row, f64 value
+    bits) -> [world, 2] int64 on send's device.  Backend-agnostic (NCCL on the
+    GPU box, gloo in the CPU tests)."""
+    import torch
+    parts = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(parts, send, group=group)
+    return torch.stack(parts)
+
+
 class Csr5Sharded:
     """Rank-local shard of a CSR5 matrix plus the exchange (torch.distributed)."""
 
