@@ -10,7 +10,7 @@ SRCS     := $(wildcard $(PKG)/csrc/*.cu)
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 HDRS     := $(wildcard $(PKG)/csrc/*.cuh) include/csr5g.h
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle shim clean
 all: lib oracle
 
 lib: $(PKG)/libcsr5g.so
@@ -24,6 +24,14 @@ $(PKG)/libcsr5g.so: $(OBJS)
 
 oracle:
 	$(MAKE) -C oracle
+
+# C++ drop-in shim test (include/csr5g.hpp); needs a GPU to run
+CXX_SYS  := $(if $(wildcard /usr/bin/g++),/usr/bin/g++,g++)
+shim: build/shim_test
+build/shim_test: tests/cpp/shim_test.cpp include/csr5g.hpp include/csr5g.h $(PKG)/libcsr5g.so
+	@mkdir -p build
+	$(CXX_SYS) -std=c++20 -O2 -Wall -Iinclude $< -L$(PKG) -lcsr5g \
+	  -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
 
 clean:
 	rm -rf build $(PKG)/libcsr5g.so

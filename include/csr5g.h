@@ -141,6 +141,18 @@ CSR5G_API int csr5g_fixup(csr5g_matrix h, const csr5g_partial *d_all, int32_t wo
  * caller's device buffers (col_idx int32[nnz_held], val f64[nnz_held]). */
 CSR5G_API int csr5g_to_csr(csr5g_matrix h, int32_t *d_col_idx, double *d_val, void *stream);
 
+/* Host-vector overloads (drop-in for the reference's std::vector API; they
+ * stage through the device and synchronise -- not the timed path).
+ * csr_to_csr5 from a host CSR with the reference's int64 col_idx
+ * (format.hpp:182); spmv_csr5 with host x / y (spmv.hpp:58-61);
+ * csr5_to_csr into host buffers (format.hpp:186). */
+CSR5G_API int csr5g_build_host(int device, int64_t m, int64_t n, int64_t nnz,
+                               const int64_t *h_row_ptr, const int64_t *h_col_idx,
+                               const double *h_val, const csr5g_params *params,
+                               csr5g_matrix *out);
+CSR5G_API int csr5g_spmv_host(csr5g_matrix h, const double *h_x, double *h_y, int32_t mode);
+CSR5G_API int csr5g_to_csr_host(csr5g_matrix h, int64_t *h_col_idx, double *h_val);
+
 /* Implicit destruction of Csr5Matrix (value type) -> explicit release. */
 CSR5G_API int csr5g_release(csr5g_matrix h);
 

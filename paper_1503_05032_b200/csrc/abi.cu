@@ -1,9 +1,11 @@
 // abi.cu -- the extern "C" boundary (include/csr5g.h).  Argument checking and
 // error text follow the reference (tuning.cpp, descriptor.cpp, spmv.cpp:17-27);
 // everything else forwards to convert.cu / spmv.cu.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -188,6 +190,100 @@ int csr5g_to_csr(csr5g_matrix h, int32_t* d_col_idx, double* d_val, void* stream
   if (h->h->info.nnz_held > 0 && (!d_col_idx || !d_val))
     return fail(CSR5G_EINVAL, "csr5g: NULL output");
   return launch_to_csr(h->h, d_col_idx, d_val, static_cast<cudaStream_t>(stream));
+}
+
+int csr5g_build_host(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* h_row_ptr,
+                     const int64_t* h_col_idx, const double* h_val, const csr5g_params* params,
+                     csr5g_matrix* out) {
+  if (!out) return fail(CSR5G_EINVAL, "csr5g: out is NULL");
+  *out = nullptr;
+  if (m < 0 || n < 0 || nnz < 0) return fail(CSR5G_EINVAL, "csr: negative dimension");
+  if (n >= (int64_t(1) << 31))
+    return fail(CSR5G_ERANGE, "csr5g: n >= 2^31 columns does not fit the int32 col_idx");
+  if (m > 0 && !h_row_ptr) return fail(CSR5G_EINVAL, "csr5g: row_ptr is NULL");
+  if (m > 0 && h_row_ptr[m] != nnz)
+    return fail(CSR5G_EINVAL, "csr: col_idx/val size does not match row_ptr[m]");
+  int ndev = 0;
+  CSR5G_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(CSR5G_ECUDA, "csr5g: no such CUDA device");
+  CSR5G_CUDA(cudaSetDevice(device));
+  std::vector<int32_t> c32((size_t)nnz);
+  for (int64_t i = 0; i < nnz; ++i) c32[(size_t)i] = (int32_t)h_col_idx[i];
+  int64_t* d_rp = nullptr;
+  int32_t* d_ci = nullptr;
+  double* d_va = nullptr;
+  auto done = [&](int rc) {
+    cudaFree(d_rp);
+    cudaFree(d_ci);
+    cudaFree(d_va);
+    return rc;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&d_rp, sizeof(int64_t) * (m + 1))) != cudaSuccess ||
+      (e = cudaMalloc(&d_ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1))) != cudaSuccess ||
+      (e = cudaMalloc(&d_va, sizeof(double) * std::max<int64_t>(nnz, 1))) != cudaSuccess)
+    return done(cuda_fail(e, "cudaMalloc(staging)"));
+  if (m > 0 && (e = cudaMemcpy(d_rp, h_row_ptr, sizeof(int64_t) * (m + 1),
+                               cudaMemcpyHostToDevice)) != cudaSuccess)
+    return done(cuda_fail(e, "cudaMemcpy(row_ptr)"));
+  if (nnz > 0 && ((e = cudaMemcpy(d_ci, c32.data(), sizeof(int32_t) * nnz,
+                                  cudaMemcpyHostToDevice)) != cudaSuccess ||
+                  (e = cudaMemcpy(d_va, h_val, sizeof(double) * nnz, cudaMemcpyHostToDevice)) !=
+                      cudaSuccess))
+    return done(cuda_fail(e, "cudaMemcpy(col_idx/val)"));
+  return done(csr5g_build(device, m, n, nnz, d_rp, d_ci, d_va, params, nullptr, out));
+}
+
+int csr5g_spmv_host(csr5g_matrix h, const double* h_x, double* h_y, int32_t mode) {
+  if (!h) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
+  const csr5g_info& in = h->h->info;
+  CSR5G_CUDA(cudaSetDevice(h->h->device));
+  double *dx = nullptr, *dy = nullptr;
+  auto done = [&](int rc) {
+    cudaFree(dx);
+    cudaFree(dy);
+    return rc;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&dx, sizeof(double) * std::max<int64_t>(in.n, 1))) != cudaSuccess ||
+      (e = cudaMalloc(&dy, sizeof(double) * std::max<int64_t>(in.m, 1))) != cudaSuccess)
+    return done(cuda_fail(e, "cudaMalloc(x/y)"));
+  if (in.n > 0 &&
+      (e = cudaMemcpy(dx, h_x, sizeof(double) * in.n, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return done(cuda_fail(e, "cudaMemcpy(x)"));
+  int rc = csr5g_spmv(h, dx, dy, mode, nullptr);
+  if (rc) return done(rc);
+  if (in.m > 0 &&
+      (e = cudaMemcpy(h_y, dy, sizeof(double) * in.m, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return done(cuda_fail(e, "cudaMemcpy(y)"));
+  return done(CSR5G_OK);
+}
+
+int csr5g_to_csr_host(csr5g_matrix h, int64_t* h_col_idx, double* h_val) {
+  if (!h) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
+  const int64_t nz = h->h->info.nnz_held;
+  CSR5G_CUDA(cudaSetDevice(h->h->device));
+  int32_t* dc = nullptr;
+  double* dv = nullptr;
+  auto done = [&](int rc) {
+    cudaFree(dc);
+    cudaFree(dv);
+    return rc;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&dc, sizeof(int32_t) * std::max<int64_t>(nz, 1))) != cudaSuccess ||
+      (e = cudaMalloc(&dv, sizeof(double) * std::max<int64_t>(nz, 1))) != cudaSuccess)
+    return done(cuda_fail(e, "cudaMalloc(csr)"));
+  int rc = csr5g_to_csr(h, dc, dv, nullptr);
+  if (rc) return done(rc);
+  std::vector<int32_t> c32((size_t)nz);
+  if (nz > 0 && ((e = cudaMemcpy(c32.data(), dc, sizeof(int32_t) * nz, cudaMemcpyDeviceToHost)) !=
+                     cudaSuccess ||
+                 (e = cudaMemcpy(h_val, dv, sizeof(double) * nz, cudaMemcpyDeviceToHost)) !=
+                     cudaSuccess))
+    return done(cuda_fail(e, "cudaMemcpy(csr)"));
+  for (int64_t i = 0; i < nz; ++i) h_col_idx[i] = c32[(size_t)i];
+  return done(CSR5G_OK);
 }
 
 int csr5g_release(csr5g_matrix h) {

@@ -1,0 +1,136 @@
+// Exercises include/csr5g.hpp (the C++ drop-in for the reference's csr5:: API)
+// on the GPU: conversion, host-vector SpMV in both modes, round trip,
+// dump_format and the reference's error behaviour.  Run by
+// tests/test_gpu_shim.py; prints "SHIM OK" on success.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+
+#include "csr5g.hpp"
+
+using namespace csr5g;
+
+static int failures = 0;
+#define CHECK(c)                                                     \
+  do {                                                               \
+    if (!(c)) {                                                      \
+      std::printf("CHECK failed: %s (line %d)\n", #c, __LINE__);     \
+      ++failures;                                                    \
+    }                                                                \
+  } while (0)
+
+// sequential row-order oracle (the reference's dense_spmv_oracle, csr.cpp:85-98)
+static DenseVector oracle(const CsrMatrix& a, const DenseVector& x) {
+  DenseVector y((std::size_t)a.m, 0.0);
+  for (index_t i = 0; i < a.m; ++i) {
+    double s = 0.0;
+    for (index_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) s += a.val[k] * x[a.col_idx[k]];
+    y[i] = s;
+  }
+  return y;
+}
+
+static double max_rel(const DenseVector& y, const DenseVector& r) {
+  double w = 0.0;
+  for (std::size_t i = 0; i < y.size(); ++i)
+    w = std::max(w, std::abs(y[i] - r[i]) / std::max(1.0, std::abs(r[i])));
+  return w;
+}
+
+static CsrMatrix random_csr(unsigned long long seed, index_t m, index_t n, double density) {
+  CsrMatrix a;
+  a.m = m;
+  a.n = n;
+  a.row_ptr.push_back(0);
+  unsigned long long s = seed;
+  auto next = [&] {
+    s = s * 6364136223846793005ULL + 1442695040888963407ULL;
+    return s >> 11;
+  };
+  for (index_t i = 0; i < m; ++i) {
+    for (index_t j = 0; j < n; ++j)
+      if ((next() % 1000000) < density * 1e6) {
+        a.col_idx.push_back(j);
+        a.val.push_back(0.5 + (double)(next() % 1000000) * 1e-6);
+      }
+    a.row_ptr.push_back((index_t)a.col_idx.size());
+  }
+  return a;
+}
+
+int main() {
+  // 8x8 with 34 nonzeros (test_format.cpp:30-44)
+  {
+    const std::vector<std::vector<index_t>> cols = {{0, 1, 2, 3, 4, 5}, {}, {0, 2, 4, 6, 7},
+                                                    {1, 3, 5, 6, 7}, {0, 1, 2, 3, 4, 5, 6},
+                                                    {1, 2, 3, 5, 6, 7}, {0, 3, 6}, {2, 5}};
+    CsrMatrix a;
+    a.m = a.n = 8;
+    a.row_ptr.push_back(0);
+    double v = 1.0;
+    for (auto& r : cols) {
+      for (index_t c : r) {
+        a.col_idx.push_back(c);
+        a.val.push_back(v++);
+      }
+      a.row_ptr.push_back((index_t)a.col_idx.size());
+    }
+    Csr5Matrix a5 = csr_to_csr5(a, TuningParams{.sigma = 1});  // B = 32: 1 tile + tail 2
+    CHECK(a5.p() == 2 && a5.p_complete() == 1 && a5.tail_len() == 2);
+    const DenseVector x(8, 1.0);
+    CHECK(max_rel(spmv_csr5(a5, x), oracle(a, x)) <= 1e-12);
+    CHECK(csr5_to_csr(a5, a.row_ptr) == a);
+    std::ostringstream out;
+    dump_format(a5, out);
+    CHECK(out.str().find("tile 0:") != std::string::npos);
+    CHECK(out.str().find("tail nnz=2") != std::string::npos);
+  }
+  // random matrices over sigma, both modes
+  for (index_t sigma : {0, 1, 4, 16, 17, 18, 27, 48}) {
+    const CsrMatrix a = random_csr(1000 + sigma, 700, 500, 0.03);
+    DenseVector x((std::size_t)a.n);
+    for (std::size_t i = 0; i < x.size(); ++i) x[i] = 0.5 + 0.001 * (double)(i % 997);
+    Csr5Matrix a5 = csr_to_csr5(a, TuningParams{.sigma = sigma});
+    const DenseVector ref = oracle(a, x);
+    CHECK(max_rel(spmv_csr5(a5, x), ref) <= 1e-12);
+    CHECK(max_rel(spmv_csr5(a5, x, SpmvMode::atomic), ref) <= 1e-12);
+    CHECK(csr5_to_csr(a5, a.row_ptr) == a);
+    if (sigma == 0) CHECK(a5.sigma() == select_sigma((double)a.nnz() / (double)a.m));
+  }
+  // reference error behaviour
+  {
+    const CsrMatrix a = random_csr(7, 20, 30, 0.2);
+    bool threw = false;
+    try {
+      (void)csr_to_csr5(a, TuningParams{.omega = 4, .sigma = 16});
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    threw = false;
+    try {
+      (void)csr_to_csr5(a, TuningParams{.sigma = 60});
+    } catch (const std::invalid_argument& e) {
+      threw = std::string(e.what()).find("smaller sigma") != std::string::npos;
+    }
+    CHECK(threw);
+    Csr5Matrix a5 = csr_to_csr5(a);
+    threw = false;
+    try {
+      (void)spmv_csr5(a5, DenseVector(29, 1.0));
+    } catch (const std::invalid_argument& e) {
+      threw = std::string(e.what()) == "spmv: x has length 29, expected 30";
+    }
+    CHECK(threw);
+  }
+  if (failures) {
+    std::printf("SHIM FAILED (%d)\n", failures);
+    return 1;
+  }
+  std::printf("SHIM OK\n");
+  return 0;
+}
