@@ -62,6 +62,7 @@ struct SpmvArgs {
   int32_t atomic;          // SpmvMode::atomic
   int32_t x_mode;          // x gather path: 0 L1+evict_last, 1 L1 no-allocate+evict_last
   int32_t jitter;          // hashed tile-range boundaries
+  int32_t stream_only;     // profiling: run the TMA ring without gathers/math
 };
 
 struct Handle {
@@ -165,6 +166,13 @@ __device__ __forceinline__ double ld_keep_na(const double* p, uint64_t pol) {
 __device__ __forceinline__ double ld_x_lsu(const double* p, uint64_t pol) {
   double v;
   asm("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+// plain read-only gather: no L2 policy operand (saves the uniform-register
+// moves a cache_hint needs per load)
+__device__ __forceinline__ double ld_x_plain(const double* p) {
+  double v;
+  asm("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ double ld_x_cg(const double* p) {

@@ -129,7 +129,9 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
 __host__ __device__ constexpr int spmv_lookahead(int sigma) { return sigma > 0 ? 1 : 1; }
 // Warps per CTA: short tiles need fewer registers and less shared memory per
 // warp, and random gathers want as many warps in flight as fit.
-__host__ __device__ constexpr int spmv_threads(int sigma) { return sigma <= 16 ? 384 : 256; }
+__host__ __device__ constexpr int spmv_threads(int sigma) { return sigma <= 32 ? 384 : 256; }
+// closed-segment slots per warp in shared memory (tiles rarely have more heads)
+constexpr int kClosedSlots = 128;
 
 // Outside the anonymous namespace: the sigma instantiations are reached
 // through a function-pointer switch, and the runtime must register each one.
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   constexpr int B = 32 * SIG;
   constexpr int CH = SIG <= 32 ? SIG : (SIG + 1) / 2;  // x gathers in flight per lane
   constexpr int LA = spmv_lookahead(SIG);              // tiles of gathers in flight
+  constexpr int CAPC = B < kClosedSlots ? B : kClosedSlots;
   constexpr uint64_t FMASK = (1ull << SIG) - 1;
   constexpr uint32_t COL_OFF = B * 8, DESC_OFF = B * 12;
   constexpr uint32_t TILE_BYTES = B * 12 + 32 * sizeof(W);
@@ -150,8 +153,12 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   const int w = blockIdx.x * NW + wib;
   const bool has_tiles = w < a.nwarps;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + wib * S;
-  double* closed = reinterpret_cast<double*>(smem + a.bar_bytes) + (size_t)wib * B;
-  unsigned char* ring = smem + a.bar_bytes + (size_t)NW * B * 8 + (size_t)wib * S * a.stage_bytes;
+  // closed-segment slots: the first CAPC heads of a tile in shared memory, any
+  // further ones (tiles of very short rows) in a per-warp global spill area
+  double* closed = reinterpret_cast<double*>(smem + a.bar_bytes) + (size_t)wib * CAPC;
+  unsigned char* ring = smem + a.bar_bytes + (size_t)NW * CAPC * 8 + (size_t)wib * S * a.stage_bytes;
+  double* __restrict__ spill = a.spill + (size_t)w * B;
+  auto cslot = [&](int h) -> double* { return h < CAPC ? closed + h : spill + h; };
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_x = policy_evict_last();
   const W* __restrict__ desc = static_cast<const W*>(a.desc);
@@ -204,6 +211,9 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     } else if (a.x_mode == 3) {
 #pragma unroll
       for (int u = 0; u < CH; ++u) xv[u] = ld_x_cg(a.x + sc[u * 32 + lane]);
+    } else if (a.x_mode == 4) {
+#pragma unroll
+      for (int u = 0; u < CH; ++u) xv[u] = ld_x_plain(a.x + sc[u * 32 + lane]);
     } else {
 #pragma unroll
       for (int u = 0; u < CH; ++u) xv[u] = ld_keep(a.x + sc[u * 32 + lane], pol_x);
@@ -234,13 +244,24 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     const int64_t next_row = (k + 1 == a.pcs) ? a.next_row_after : (int64_t)(tpn & 0x7fffffffu);
     const int32_t* __restrict__ eo = a.eo + eo_base;
 
-    const int sn = s + 1 == S ? 0 : s + 1;
-    const uint32_t pn = s + 1 == S ? phase ^ 1u : phase;
+    // profiling knob 2: compute only -- every tile re-reads the resident
+    // stage 0, no TMA traffic after the prologue (y is garbage)
+    const bool compute_only = a.stream_only == 2;
+    const int sn = compute_only ? 0 : (s + 1 == S ? 0 : s + 1);
+    const uint32_t pn = compute_only ? 0u : (s + 1 == S ? phase ^ 1u : phase);
+    if (a.stream_only == 1) {  // profiling knob 1: the TMA ring alone (y is garbage)
+      mbar_wait(bars + s, phase);
+      __syncwarp();
+      if (lane == 0 && k + S < ke) issue(k + S, s);
+      s = s + 1 == S ? 0 : s + 1;
+      phase = s == 0 ? phase ^ 1u : phase;
+      continue;
+    }
     // gathers for tile k+LA go out before tile k is reduced
     double xn[CH];
     if (k + LA < ke) {
       if (LA == 1) {
-        mbar_wait(bars + sn, pn);
+        if (!compute_only) mbar_wait(bars + sn, pn);
         gather(sn, xn);
       } else {
         const int64_t ia = k - kb + LA;
@@ -286,22 +307,23 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
         const int j = j0 + u;
         if (j < SIG) {
           if ((anyf >> j) & 1ull) {  // warp-uniform: some lane closes a segment here
-            if ((fr >> j) & 1ull) {
-              if (seen) {
-                closed[head++] = sum;  // segment sealed inside this column
-              } else {
-                red = sum;  // piece continuing the column to the left (spmv.cpp:75-77)
-                seen = true;
-              }
-              sum = 0.0;
-            }
+            // branch-free inside: a close at depth j either seals a segment
+            // inside this column (green) or ends the piece continuing the
+            // column to the left (red, spmv.cpp:75-77)
+            const bool f = (fr >> j) & 1ull;
+            const bool green = f && seen;
+            if (green) *cslot(head) = sum;
+            head += green ? 1 : 0;
+            red = (f && !seen) ? sum : red;
+            seen = seen || f;
+            sum = f ? 0.0 : sum;
           }
           sum = fma(sv[j * 32 + lane], xv[u], sum);
         }
       }
     }
     __syncwarp();
-    if (lane == 0 && k + S < ke) issue(k + S, s);  // refill this stage
+    if (lane == 0 && k + S < ke && !compute_only) issue(k + S, s);  // refill this stage
     s = sn;
     phase = pn;
 #pragma unroll
@@ -327,12 +349,12 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       const double o = __shfl_down_sync(kFull, acc, d);
       if (lane + d <= end) acc += o;
     }
-    if (seen) closed[yoff + cnt - 1] = sum + acc;  // the column's bottom piece
+    if (seen) *cslot(yoff + cnt - 1) = sum + acc;  // the column's bottom piece
     __syncwarp();
 
     // ---- write-back of the tile's heads in order ----
-    const double c0 = closed[0];
-    const double cL = closed[H - 1];
+    const double c0 = *cslot(0);
+    const double cL = *cslot(H - 1);
     int64_t rL = 0;
     int64_t defer_lo = 0, defer_hi = 0;
     const int nch = (H + 31) >> 5;
@@ -352,7 +374,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       if (h >= H) continue;
       const int64_t r = tile_row + (flagged ? (int64_t)e_here : (int64_t)h);
       if (h == H - 1) rL = r;
-      if (h != 0 && h != H - 1) y[r] = closed[h];
+      if (h != 0 && h != H - 1) y[r] = *cslot(h);
       if (flagged || h == H - 1) {  // empty rows up to the next head (or next tile)
         const int64_t nr = h + 1 < H ? tile_row + (int64_t)e_next : next_row;
         if (nr - r - 1 <= 8) {
@@ -524,7 +546,7 @@ int spmv_plan(Handle* h, int sms) {
   const int wbytes = h->wide ? 8 : 4;
   const int64_t tile_bytes = h->B * 12 + 32 * wbytes;
   const int stage_bytes = (int)((tile_bytes + 127) / 128 * 128);
-  const int closed_bytes = (int)(h->B * 8);
+  const int closed_bytes = (int)(std::min<int64_t>(h->B, kClosedSlots) * 8);
   int l2 = 0;
   CSR5G_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device));
   const double x_bytes = 8.0 * (double)h->info.n;
@@ -605,6 +627,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.item_row = h->item_row;
   a.item_val = h->item_val;
   a.send = h->send_ext ? h->send_ext : h->send;
+  a.spill = h->spill;
   a.pcs = h->pcs;
   a.pos0 = h->t0 * h->B;
   a.next_row_after = h->next_row_after;
@@ -642,6 +665,11 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     return e ? std::atoi(e) : 0;
   }();
   a.jitter = jitter;
+  static const int stream_only = [] {  // 1: TMA ring only, 2: compute only (profiling)
+    const char* e = std::getenv("CSR5G_STREAM_ONLY");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.stream_only = stream_only;
   if (ev0) CSR5G_CUDA(cudaEventRecord(ev0, stream));
   if (grid > 0) {
     cudaLaunchConfig_t cfg{};
@@ -675,6 +703,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   }
   if (ev1) CSR5G_CUDA(cudaEventRecord(ev1, stream));
   const int64_t items = 2 * (int64_t)h->nwarps + (h->has_tail_item ? 1 : 0);
+  if (stream_only) return CSR5G_OK;  // no items were produced
   if (!atomic && items > 0) {
     k_calibrate<<<(unsigned)((items + 255) / 256), 256, 0, stream>>>(
         h->item_row, h->item_val, items, d_y, h->first_row, h->first_owned, a.send);
