@@ -63,6 +63,7 @@ struct SpmvArgs {
   int32_t x_mode;          // x gather path: 0 L1+evict_last, 1 L1 no-allocate+evict_last
   int32_t jitter;          // hashed tile-range boundaries
   int32_t stream_only;     // profiling: run the TMA ring without gathers/math
+  int32_t early_gather;    // random gathers: issue tile k+1's gathers before tile k's depth loop
 };
 
 struct Handle {

@@ -124,9 +124,6 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
 
 }  // namespace
 
-// Gather look-ahead in tiles: short tiles carry few x registers per lane, so
-// two tiles of gathers can be in flight to cover random-access latency.
-__host__ __device__ constexpr int spmv_lookahead(int sigma) { return sigma > 0 ? 1 : 1; }
 // Warps per CTA: short tiles need fewer registers and less shared memory per
 // warp, and random gathers want as many warps in flight as fit.
 __host__ __device__ constexpr int spmv_threads(int sigma) { return sigma <= 32 ? 384 : 256; }
@@ -140,9 +137,9 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   using W = typename std::conditional<(SIG <= 17), uint32_t, uint64_t>::type;
   constexpr int B = 32 * SIG;
   constexpr int CH = SIG <= 32 ? SIG : (SIG + 1) / 2;  // x gathers in flight per lane
-  constexpr int LA = spmv_lookahead(SIG);              // tiles of gathers in flight
   constexpr int CAPC = B < kClosedSlots ? B : kClosedSlots;
   constexpr uint64_t FMASK = (1ull << SIG) - 1;
+  constexpr bool EARLY_OK = SIG <= 18;  // a second x array fits in registers
   constexpr uint32_t COL_OFF = B * 8, DESC_OFF = B * 12;
   constexpr uint32_t TILE_BYTES = B * 12 + 32 * sizeof(W);
 
@@ -197,9 +194,9 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   int64_t eov = 0;
   int s = 0;
   uint32_t phase = 0;
-  // x gathers run one tile ahead: while tile k is reduced, the first CH
-  // gathers of tile k+1 (whose col_idx already sit in the next ring stage)
-  // are in flight.
+  // x gathers run one tile ahead: while tile k is spliced and written back,
+  // the first CH gathers of tile k+1 (whose col_idx already sit in the next
+  // ring stage) are in flight.
   auto gather = [&](int st_idx, double(&xv)[CH]) {
     const int32_t* sc = reinterpret_cast<const int32_t*>(ring + (size_t)st_idx * a.stage_bytes + COL_OFF);
     if (a.x_mode == 1) {
@@ -219,13 +216,9 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       for (int u = 0; u < CH; ++u) xv[u] = ld_keep(a.x + sc[u * 32 + lane], pol_x);
     }
   };
-  double xa[CH], xb[CH];
+  double xa[CH];
   mbar_wait(bars, 0);
   gather(0, xa);
-  if (LA == 2 && kb + 1 < ke) {
-    mbar_wait(bars + 1, 0);
-    gather(1, xb);
-  }
 
   for (int64_t k = kb; k < ke; ++k) {
     const int slot = (int)((k - kb) & 31);
@@ -257,18 +250,12 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       phase = s == 0 ? phase ^ 1u : phase;
       continue;
     }
-    // gathers for tile k+LA go out before tile k is reduced
+    // random gathers (long misses): tile k+1's gathers also overlap tile k's
+    // depth loop, at the cost of a second register array and a copy
     double xn[CH];
-    if (k + LA < ke) {
-      if (LA == 1) {
-        if (!compute_only) mbar_wait(bars + sn, pn);
-        gather(sn, xn);
-      } else {
-        const int64_t ia = k - kb + LA;
-        const int sa = (int)(ia % S);
-        mbar_wait(bars + sa, (uint32_t)((ia / S) & 1));
-        gather(sa, xn);
-      }
+    if (EARLY_OK && a.early_gather && k + 1 < ke) {
+      if (!compute_only) mbar_wait(bars + sn, pn);
+      gather(sn, xn);
     }
     const unsigned char* st = ring + (size_t)s * a.stage_bytes;
     const double* sv = reinterpret_cast<const double*>(st);
@@ -324,17 +311,17 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     }
     __syncwarp();
     if (lane == 0 && k + S < ke && !compute_only) issue(k + S, s);  // refill this stage
+    // gathers for tile k+1 land in the registers the depth loop just drained;
+    // their latency overlaps this tile's splice, write-back and run merge
+    if (EARLY_OK && a.early_gather) {
+#pragma unroll
+      for (int u = 0; u < CH; ++u) xa[u] = xn[u];
+    } else if (k + 1 < ke) {
+      if (!compute_only) mbar_wait(bars + sn, pn);
+      gather(sn, xa);
+    }
     s = sn;
     phase = pn;
-#pragma unroll
-    for (int u = 0; u < CH; ++u) {
-      if (LA == 2) {
-        xa[u] = xb[u];
-        xb[u] = xn[u];
-      } else {
-        xa[u] = xn[u];
-      }
-    }
 
     // ---- splice across columns: tmp[i] = piece handed left by column i+1 ----
     const double give = seen ? red : sum;
@@ -553,13 +540,12 @@ int spmv_plan(Handle* h, int sms) {
   const bool random = h->lines_per_gather >= 8.0;
   const bool x_spills = x_bytes > 0.75 * l2;
   const int budget = !random ? 226 * 1024 : (x_spills ? 120 * 1024 : 150 * 1024);
-  h->x_mode = random ? 1 : 0;          // random: no L1 allocation for x
+  h->x_mode = random ? 1 : 4;  // random: no L1 allocation; local: plain ld.global.nc
   h->x_window = random && x_bytes > 32e6;  // random: keep x resident in L2
-  // stages: the tile being reduced + LA tiles whose gathers are in flight +
-  // one tile of TMA lead (S = LA + 2 preferred, LA + 1 minimum)
-  const int la = spmv_lookahead(sigma);
-  const int min_stages = la + 1;
-  int nw = spmv_threads(sigma) / 32, stages = random ? la + 2 : 4;
+  // stages: the tile being reduced + the next tile (its gathers go out as
+  // soon as the current depth loop ends) + TMA lead; 2 minimum
+  const int min_stages = 2;
+  int nw = spmv_threads(sigma) / 32, stages = random ? 3 : 4;
   auto need = [&](int w, int st) { return 512 + w * (closed_bytes + st * stage_bytes); };
   // local gathers: warps per SM matter most (keep them, give up depth first);
   // random gathers: keep the TMA lead (depth), give up warps
@@ -660,6 +646,8 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   const int x_mode = x_mode_env >= 0 ? x_mode_env : h->x_mode;
   const bool x_window = x_window_env >= 0 ? x_window_env != 0 : h->x_window;
   a.x_mode = x_mode;
+  a.early_gather = h->lines_per_gather >= 8.0 ? 1 : 0;
+  if (const char* e = std::getenv("CSR5G_EARLY")) a.early_gather = std::atoi(e) != 0;
   static const int jitter = [] {
     const char* e = std::getenv("CSR5G_JITTER");
     return e ? std::atoi(e) : 0;
