@@ -155,7 +155,15 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   double* closed = reinterpret_cast<double*>(smem + a.bar_bytes) + (size_t)wib * CAPC;
   unsigned char* ring = smem + a.bar_bytes + (size_t)NW * CAPC * 8 + (size_t)wib * S * a.stage_bytes;
   double* __restrict__ spill = a.spill + (size_t)w * B;
-  auto cslot = [&](int h) -> double* { return h < CAPC ? closed + h : spill + h; };
+  // explicit branches keep shared slots on STS/LDS (a selected pointer would
+  // turn every slot access into a generic load/store)
+  auto cput = [&](int h, double v) {
+    if (h < CAPC)
+      closed[h] = v;
+    else
+      spill[h] = v;
+  };
+  auto cget = [&](int h) -> double { return h < CAPC ? closed[h] : spill[h]; };
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_x = policy_evict_last();
   const W* __restrict__ desc = static_cast<const W*>(a.desc);
@@ -299,7 +307,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
             // column to the left (red, spmv.cpp:75-77)
             const bool f = (fr >> j) & 1ull;
             const bool green = f && seen;
-            if (green) *cslot(head) = sum;
+            if (green) cput(head, sum);
             head += green ? 1 : 0;
             red = (f && !seen) ? sum : red;
             seen = seen || f;
@@ -336,12 +344,12 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       const double o = __shfl_down_sync(kFull, acc, d);
       if (lane + d <= end) acc += o;
     }
-    if (seen) *cslot(yoff + cnt - 1) = sum + acc;  // the column's bottom piece
+    if (seen) cput(yoff + cnt - 1, sum + acc);  // the column's bottom piece
     __syncwarp();
 
     // ---- write-back of the tile's heads in order ----
-    const double c0 = *cslot(0);
-    const double cL = *cslot(H - 1);
+    const double c0 = cget(0);
+    const double cL = cget(H - 1);
     int64_t rL = 0;
     int64_t defer_lo = 0, defer_hi = 0;
     const int nch = (H + 31) >> 5;
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       if (h >= H) continue;
       const int64_t r = tile_row + (flagged ? (int64_t)e_here : (int64_t)h);
       if (h == H - 1) rL = r;
-      if (h != 0 && h != H - 1) y[r] = *cslot(h);
+      if (h != 0 && h != H - 1) y[r] = cget(h);
       if (flagged || h == H - 1) {  // empty rows up to the next head (or next tile)
         const int64_t nr = h + 1 < H ? tile_row + (int64_t)e_next : next_row;
         if (nr - r - 1 <= 8) {
