@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcsr5g.so")
+LIB_PATH = os.environ.get("CSR5G_LIB_OVERRIDE") or os.path.join(HERE, "libcsr5g.so")  # A/B experiments
 
 OK, EINVAL, ERUNTIME, ERANGE, ECUDA, ENOMEM = 0, 1, 2, 3, 4, 5
 MODE_DETERMINISTIC, MODE_ATOMIC = 0, 1

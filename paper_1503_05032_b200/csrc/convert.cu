@@ -551,7 +551,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   const int64_t items = 2 * (int64_t)h->nwarps + 1;
   TRY(dev_alloc(&h->item_row, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->item_val, (size_t)items, &alloc_ms, &bytes));
-  TRY(dev_alloc(&h->spill, (size_t)std::max(h->nwarps, 1) * B, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->spill, (size_t)std::max(h->nwarps, 1) * (B + 1), &alloc_ms, &bytes));
   trace.mark("plan");
 
   // ---- info ----

@@ -82,7 +82,7 @@ struct Handle {
   double* item_val = nullptr;
   csr5g_partial* send = nullptr;
   csr5g_partial* send_ext = nullptr;  // caller-provided record slot
-  double* spill = nullptr;            // nwarps * B doubles
+  double* spill = nullptr;            // nwarps * (B + 1) doubles
   int64_t next_row_after = 0, lead_rows = 0, tail_row_begin = 0, tail_pos = 0;
   int64_t first_row = 0, last_row = 0;
   bool first_owned = true, is_last = true, has_tail_item = false;

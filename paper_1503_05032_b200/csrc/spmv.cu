@@ -150,20 +150,23 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   const int w = blockIdx.x * NW + wib;
   const bool has_tiles = w < a.nwarps;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + wib * S;
-  // closed-segment slots: the first CAPC heads of a tile in shared memory, any
-  // further ones (tiles of very short rows) in a per-warp global spill area
+  // closed-segment slots (slot h + 1 = head h): in shared memory when a tile's
+  // H + 1 slots fit in CAPC, else (tiles of very short rows) all of them in a
+  // per-warp global spill area
   double* closed = reinterpret_cast<double*>(smem + a.bar_bytes) + (size_t)wib * CAPC;
   unsigned char* ring = smem + a.bar_bytes + (size_t)NW * CAPC * 8 + (size_t)wib * S * a.stage_bytes;
-  double* __restrict__ spill = a.spill + (size_t)w * B;
-  // explicit branches keep shared slots on STS/LDS (a selected pointer would
-  // turn every slot access into a generic load/store)
-  auto cput = [&](int h, double v) {
-    if (h < CAPC)
-      closed[h] = v;
+  double* __restrict__ spill = a.spill + (size_t)w * (B + 1);  // slots 0..B
+  // tile-uniform choice between the shared slots and the spill area; explicit
+  // branches keep the shared side on STS/LDS (a selected pointer would turn
+  // every slot access into a generic load/store)
+  bool fast = true;
+  auto cput = [&](int i, double v) {
+    if (fast)
+      closed[i] = v;
     else
-      spill[h] = v;
+      spill[i] = v;
   };
-  auto cget = [&](int h) -> double { return h < CAPC ? closed[h] : spill[h]; };
+  auto cget = [&](int i) -> double { return fast ? closed[i] : spill[i]; };
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_x = policy_evict_last();
   const W* __restrict__ desc = static_cast<const W*>(a.desc);
@@ -273,7 +276,6 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     const int yoff = (int)(wd >> (kSegBits + SIG));
     const int cnt = __popcll(fr);
     const int H = __shfl_sync(kFull, yoff + cnt, 31);
-    const uint64_t anyf = warp_or64(fr);
     // the first 64 empty_offset entries of a flagged tile, in flight during
     // the depth loop and consumed by the write-back
     int32_t eo_0 = 0, eo_1 = 0;
@@ -282,39 +284,49 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       if (lane + 32 < H) eo_1 = eo[lane + 32];
     }
 
-    // ---- depth loop: gathers first, then FMAs; closes go to closed[head] ----
-    double sum = 0.0, red = 0.0;
-    bool seen = false;
-    int head = yoff;
+    // ---- depth loop (spmv.cpp:61-95): gathers first, then FMAs ----
+    // Every close at a bit flag goes to a slot: lane i's k-th flag ends the
+    // segment of head yoff_i + k - 1 (k = 0: the piece continuing the column to
+    // the left, "red"), stored at slot yoff_i + k (slot h + 1 = head h).  A
+    // tile whose slots fit in shared memory (the common case) runs the
+    // unrolled loop; tiles of very short rows use the per-warp global spill
+    // area through a compact loop that re-reads x (L1 hits).
+    fast = H < CAPC;
+    double sum = 0.0;
+    if (fast) {
+      double* cp = closed + yoff;
 #pragma unroll
-    for (int j0 = 0; j0 < SIG; j0 += CH) {
-      double xv[CH];
-      if (j0 == 0) {
+      for (int j0 = 0; j0 < SIG; j0 += CH) {
+        double xv[CH];
+        if (j0 == 0) {
 #pragma unroll
-        for (int u = 0; u < CH; ++u) xv[u] = xa[u];
-      } else {
+          for (int u = 0; u < CH; ++u) xv[u] = xa[u];
+        } else {
 #pragma unroll
-        for (int u = 0; u < CH; ++u)
-          if (j0 + u < SIG) xv[u] = ld_keep(a.x + sc[(j0 + u) * 32 + lane], pol_x);
-      }
-#pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        const int j = j0 + u;
-        if (j < SIG) {
-          if ((anyf >> j) & 1ull) {  // warp-uniform: some lane closes a segment here
-            // branch-free inside: a close at depth j either seals a segment
-            // inside this column (green) or ends the piece continuing the
-            // column to the left (red, spmv.cpp:75-77)
-            const bool f = (fr >> j) & 1ull;
-            const bool green = f && seen;
-            if (green) cput(head, sum);
-            head += green ? 1 : 0;
-            red = (f && !seen) ? sum : red;
-            seen = seen || f;
-            sum = f ? 0.0 : sum;
-          }
-          sum = fma(sv[j * 32 + lane], xv[u], sum);
+          for (int u = 0; u < CH; ++u)
+            if (j0 + u < SIG) xv[u] = ld_keep(a.x + sc[(j0 + u) * 32 + lane], pol_x);
         }
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {
+          const int j = j0 + u;
+          if (j < SIG) {
+            if ((fr >> j) & 1ull) {  // predicated: store, advance, restart
+              *cp++ = sum;
+              sum = 0.0;
+            }
+            sum = fma(sv[j * 32 + lane], xv[u], sum);
+          }
+        }
+      }
+    } else {
+      double* sp = spill + yoff;
+#pragma unroll 1
+      for (int j = 0; j < SIG; ++j) {
+        if ((fr >> j) & 1ull) {
+          *sp++ = sum;
+          sum = 0.0;
+        }
+        sum = fma(sv[j * 32 + lane], __ldg(a.x + sc[j * 32 + lane]), sum);
       }
     }
     __syncwarp();
@@ -332,6 +344,8 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     phase = pn;
 
     // ---- splice across columns: tmp[i] = piece handed left by column i+1 ----
+    const bool seen = cnt > 0;
+    const double red = seen ? cget(yoff) : 0.0;  // this lane's own first close
     const double give = seen ? red : sum;
     double tmp = __shfl_down_sync(kFull, give, 1);
     if (lane == 31) tmp = 0.0;
@@ -344,12 +358,12 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       const double o = __shfl_down_sync(kFull, acc, d);
       if (lane + d <= end) acc += o;
     }
-    if (seen) cput(yoff + cnt - 1, sum + acc);  // the column's bottom piece
+    if (seen) cput(yoff + cnt, sum + acc);  // the column's bottom piece
     __syncwarp();
 
     // ---- write-back of the tile's heads in order ----
-    const double c0 = cget(0);
-    const double cL = cget(H - 1);
+    const double c0 = cget(1);
+    const double cL = cget(H);
     int64_t rL = 0;
     int64_t defer_lo = 0, defer_hi = 0;
     const int nch = (H + 31) >> 5;
@@ -369,7 +383,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       if (h >= H) continue;
       const int64_t r = tile_row + (flagged ? (int64_t)e_here : (int64_t)h);
       if (h == H - 1) rL = r;
-      if (h != 0 && h != H - 1) y[r] = cget(h);
+      if (h != 0 && h != H - 1) y[r] = cget(h + 1);
       if (flagged || h == H - 1) {  // empty rows up to the next head (or next tile)
         const int64_t nr = h + 1 < H ? tile_row + (int64_t)e_next : next_row;
         if (nr - r - 1 <= 8) {

@@ -119,6 +119,16 @@ def hard_shapes(orc):
     c2 = [j for k in range(3000) for j in range(3)]
     yield "alternating empties", orc.coo_to_csr(r2, c2, np.linspace(0.5, 1.5, len(r2)), 7000, 5)
     yield "random skew", orc.generate_synthetic(2, 5000, 3000, 40000, rng())
+    # regions of singleton rows (tiles with more heads than the shared-memory
+    # slots: spill path) between regions of long rows (shared-memory path), so
+    # both kinds of tile alternate inside one warp's tile range
+    r3, c3, row = [], [], 0
+    for blk in range(40):
+        for _ in range(700):
+            r3.append(row); c3.append((row * 7) % 900); row += 1
+        for _ in range(30):
+            r3.extend([row] * 45); c3.extend(range(blk, blk + 45)); row += 1
+    yield "spill/shared alternation", orc.coo_to_csr(r3, c3, np.linspace(0.5, 1.5, len(r3)), row, 900)
 
 
 @pytest.mark.parametrize("sigma", [1, 4, 5, 16, 17, 18, 27, 48])
