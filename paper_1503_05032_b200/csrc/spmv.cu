@@ -129,6 +129,7 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
 __host__ __device__ constexpr int spmv_threads(int sigma) { return sigma <= 32 ? 384 : 256; }
 // closed-segment slots per warp in shared memory (tiles rarely have more heads)
 constexpr int kClosedSlots = 128;
+constexpr int kEoSlots = 128;  // >= kClosedSlots - 1 heads of a shared-slot tile
 
 // Outside the anonymous namespace: the sigma instantiations are reached
 // through a function-pointer switch, and the runtime must register each one.
@@ -154,19 +155,13 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   // H + 1 slots fit in CAPC, else (tiles of very short rows) all of them in a
   // per-warp global spill area
   double* closed = reinterpret_cast<double*>(smem + a.bar_bytes) + (size_t)wib * CAPC;
-  unsigned char* ring = smem + a.bar_bytes + (size_t)NW * CAPC * 8 + (size_t)wib * S * a.stage_bytes;
+  // empty_offset entries of a flagged shared-slot tile, staged before the
+  // next tile's gathers go out so the write-back issues no global loads
+  int32_t* eos = reinterpret_cast<int32_t*>(smem + a.bar_bytes + (size_t)NW * CAPC * 8) +
+                 (size_t)wib * kEoSlots;
+  unsigned char* ring = smem + a.bar_bytes + (size_t)NW * (CAPC * 8 + kEoSlots * 4) +
+                        (size_t)wib * S * a.stage_bytes;
   double* __restrict__ spill = a.spill + (size_t)w * (B + 1);  // slots 0..B
-  // tile-uniform choice between the shared slots and the spill area; explicit
-  // branches keep the shared side on STS/LDS (a selected pointer would turn
-  // every slot access into a generic load/store)
-  bool fast = true;
-  auto cput = [&](int i, double v) {
-    if (fast)
-      closed[i] = v;
-    else
-      spill[i] = v;
-  };
-  auto cget = [&](int i) -> double { return fast ? closed[i] : spill[i]; };
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_x = policy_evict_last();
   const W* __restrict__ desc = static_cast<const W*>(a.desc);
@@ -276,12 +271,14 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     const int yoff = (int)(wd >> (kSegBits + SIG));
     const int cnt = __popcll(fr);
     const int H = __shfl_sync(kFull, yoff + cnt, 31);
-    // the first 64 empty_offset entries of a flagged tile, in flight during
-    // the depth loop and consumed by the write-back
-    int32_t eo_0 = 0, eo_1 = 0;
-    if (flagged) {
-      if (lane < H) eo_0 = eo[lane];
-      if (lane + 32 < H) eo_1 = eo[lane + 32];
+    const bool fast = H < CAPC;
+    // a flagged shared-slot tile's empty_offset entries (H < 128: at most 4
+    // per lane) are in flight during the depth loop
+    int32_t eov4[4] = {0, 0, 0, 0};
+    if (flagged && fast) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (lane + 32 * q < H) eov4[q] = eo[lane + 32 * q];
     }
 
     // ---- depth loop (spmv.cpp:61-95): gathers first, then FMAs ----
@@ -291,8 +288,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     // tile whose slots fit in shared memory (the common case) runs the
     // unrolled loop; tiles of very short rows use the per-warp global spill
     // area through a compact loop that re-reads x (L1 hits).
-    fast = H < CAPC;
-    double sum = 0.0;
+    double sum = 0.0, red = 0.0;
     if (fast) {
       double* cp = closed + yoff;
 #pragma unroll
@@ -323,11 +319,17 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
 #pragma unroll 1
       for (int j = 0; j < SIG; ++j) {
         if ((fr >> j) & 1ull) {
+          if (sp == spill + yoff) red = sum;
           *sp++ = sum;
           sum = 0.0;
         }
         sum = fma(sv[j * 32 + lane], __ldg(a.x + sc[j * 32 + lane]), sum);
       }
+    }
+    if (flagged && fast) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (lane + 32 * q < H) eos[lane + 32 * q] = eov4[q];
     }
     __syncwarp();
     if (lane == 0 && k + S < ke && !compute_only) issue(k + S, s);  // refill this stage
@@ -345,7 +347,10 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
 
     // ---- splice across columns: tmp[i] = piece handed left by column i+1 ----
     const bool seen = cnt > 0;
-    const double red = seen ? cget(yoff) : 0.0;  // this lane's own first close
+    // this lane's own first close: read back from shared memory (the spill
+    // loop keeps it in a register, so no global load here has to wait for
+    // the next tile's gathers)
+    if (fast && seen) red = closed[yoff];
     const double give = seen ? red : sum;
     double tmp = __shfl_down_sync(kFull, give, 1);
     if (lane == 31) tmp = 0.0;
@@ -358,44 +363,48 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       const double o = __shfl_down_sync(kFull, acc, d);
       if (lane + d <= end) acc += o;
     }
-    if (seen) cput(yoff + cnt, sum + acc);  // the column's bottom piece
+    if (seen) {  // the column's bottom piece
+      if (fast)
+        closed[yoff + cnt] = sum + acc;
+      else
+        spill[yoff + cnt] = sum + acc;
+    }
     __syncwarp();
 
     // ---- write-back of the tile's heads in order ----
-    const double c0 = cget(1);
-    const double cL = cget(H);
+    // Two copies of one loop: shared-slot tiles read slots and empty_offset
+    // from shared memory only, spill tiles from global memory.
+    double c0 = 0.0, cL = 0.0;
     int64_t rL = 0;
     int64_t defer_lo = 0, defer_hi = 0;
-    const int nch = (H + 31) >> 5;
+    auto write_back = [&](auto eo_at, auto slot_at) {
+      c0 = slot_at(1);
+      cL = slot_at(H);
+      const int nch = (H + 31) >> 5;
 #pragma unroll 1
-    for (int c = 0; c < nch; ++c) {  // warp-uniform trip count
-      const int h = lane + 32 * c;
-      // empty_offset of heads h and h+1: the first 64 come from registers
-      // loaded before the depth loop, later ones from memory
-      int32_t e_here = 0, e_next = 0;
-      if (flagged) {
-        const int32_t cur = c == 0 ? eo_0 : (c == 1 ? eo_1 : (h < H ? eo[h] : 0));
-        const int32_t nxt0 = c == 0 ? __shfl_sync(kFull, eo_1, 0) : 0;
-        const int32_t dn = __shfl_down_sync(kFull, cur, 1);
-        e_here = cur;
-        e_next = lane < 31 ? dn : (c == 0 ? nxt0 : (h + 1 < H ? eo[h + 1] : 0));
-      }
-      if (h >= H) continue;
-      const int64_t r = tile_row + (flagged ? (int64_t)e_here : (int64_t)h);
-      if (h == H - 1) rL = r;
-      if (h != 0 && h != H - 1) y[r] = cget(h + 1);
-      if (flagged || h == H - 1) {  // empty rows up to the next head (or next tile)
-        const int64_t nr = h + 1 < H ? tile_row + (int64_t)e_next : next_row;
-        if (nr - r - 1 <= 8) {
-          for (int64_t q = r + 1; q < nr; ++q) y[q] = 0.0;
-        } else if (defer_hi == defer_lo) {
-          defer_lo = r + 1;
-          defer_hi = nr;
-        } else {
-          for (int64_t q = r + 1; q < nr; ++q) y[q] = 0.0;
+      for (int c = 0; c < nch; ++c) {  // warp-uniform trip count
+        const int h = lane + 32 * c;
+        if (h >= H) break;
+        const int64_t r = tile_row + (flagged ? (int64_t)eo_at(h) : (int64_t)h);
+        if (h == H - 1) rL = r;
+        if (h != 0 && h != H - 1) y[r] = slot_at(h + 1);
+        if (flagged || h == H - 1) {  // empty rows up to the next head (or next tile)
+          const int64_t nr = h + 1 < H ? tile_row + (int64_t)eo_at(h + 1) : next_row;
+          if (nr - r - 1 <= 8) {
+            for (int64_t q = r + 1; q < nr; ++q) y[q] = 0.0;
+          } else if (defer_hi == defer_lo) {
+            defer_lo = r + 1;
+            defer_hi = nr;
+          } else {
+            for (int64_t q = r + 1; q < nr; ++q) y[q] = 0.0;
+          }
         }
       }
-    }
+    };
+    if (fast)
+      write_back([&](int i) { return eos[i]; }, [&](int i) { return closed[i]; });
+    else
+      write_back([&](int i) { return eo[i]; }, [&](int i) { return spill[i]; });
     rL = __shfl_sync(kFull, rL, (H - 1) & 31);
     uint32_t dm = __ballot_sync(kFull, defer_hi > defer_lo);
     while (dm) {  // long empty-row runs: zero cooperatively
@@ -568,7 +577,9 @@ int spmv_plan(Handle* h, int sms) {
   // soon as the current depth loop ends) + TMA lead; 2 minimum
   const int min_stages = 2;
   int nw = spmv_threads(sigma) / 32, stages = random ? 3 : 4;
-  auto need = [&](int w, int st) { return 512 + w * (closed_bytes + st * stage_bytes); };
+  auto need = [&](int w, int st) {
+    return 512 + w * (closed_bytes + kEoSlots * 4 + st * stage_bytes);
+  };
   // local gathers: warps per SM matter most (keep them, give up depth first);
   // random gathers: keep the TMA lead (depth), give up warps
   if (!random)
