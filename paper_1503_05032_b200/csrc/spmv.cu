@@ -41,6 +41,14 @@ __device__ __forceinline__ uint32_t saddr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+__device__ __forceinline__ void sts_if(int32_t* p, int32_t v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p st.shared.b32 [%0], %1;\n\t}" ::"r"(
+          saddr(p)),
+      "r"(v), "r"((int)pred)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(bar)) : "memory");
 }
@@ -326,11 +334,12 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
         sum = fma(sv[j * 32 + lane], __ldg(a.x + sc[j * 32 + lane]), sum);
       }
     }
-    if (flagged && fast) {
+    // predicated stores on every path: the loads above are consumed here, before
+    // the gathers go out, on flagged and unflagged tiles alike (a branch would
+    // leave a possibly-outstanding load whose scoreboard the gathers reuse)
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (lane + 32 * q < H) eos[lane + 32 * q] = eov4[q];
-    }
+    for (int q = 0; q < 4; ++q)
+      sts_if(eos + lane + 32 * q, eov4[q], flagged && fast && lane + 32 * q < H);
     __syncwarp();
     if (lane == 0 && k + S < ke && !compute_only) issue(k + S, s);  // refill this stage
     // gathers for tile k+1 land in the registers the depth loop just drained;
