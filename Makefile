@@ -10,7 +10,7 @@ SRCS     := $(wildcard $(PKG)/csrc/*.cu)
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 HDRS     := $(wildcard $(PKG)/csrc/*.cuh) include/csr5g.h
 
-.PHONY: all lib oracle shim clean
+.PHONY: all lib oracle shim probe clean
 all: lib oracle
 
 lib: $(PKG)/libcsr5g.so
@@ -32,6 +32,12 @@ build/shim_test: tests/cpp/shim_test.cpp include/csr5g.hpp include/csr5g.h $(PKG
 	@mkdir -p build
 	$(CXX_SYS) -std=c++20 -O2 -Wall -Iinclude $< -L$(PKG) -lcsr5g \
 	  -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
+
+# measurement tool (random-gather ceiling), not part of the product
+probe: build/gather_probe
+build/gather_probe: tools/gather_probe.cu
+	@mkdir -p build
+	$(NVCC) -O3 -std=c++17 $(ARCH) $< -o $@
 
 clean:
 	rm -rf build $(PKG)/libcsr5g.so

@@ -566,26 +566,34 @@ int spmv_plan(Handle* h, int sms) {
   //  * local gathers (stencils): up to 226 KB -- the largest ring and warp
   //    count; x gathers mostly hit L1/L2 with few misses in flight;
   //  * random gathers: whatever shared memory is not carved out stays L1,
-  //    which is where outstanding gather misses land.  Measured on R-MAT s24
-  //    (x 134 MB > L2): 115 KB -> 2.26 ms, 183 KB -> 3.02 ms, 206 KB -> 5.76 ms.
-  //    When x fits in L2 (misses are short), more warps win instead.
+  //    which is where outstanding gather misses land.  About 100 KB of ring
+  //    with 2 stages measured best on both R-MAT s24 (x 134 MB > L2; 2 stages
+  //    x 4/6/7/9/10 warps = 64/85/99/127/141 KB -> 2.10/1.74/1.67/1.76/2.02
+  //    ms) and mixed s23 (x 67 MB < L2; 6/9/11/12 warps = 57/85/103/113 KB ->
+  //    0.67/0.56/0.52/0.53 ms).  tools/gather_probe.cu: uniform random
+  //    8-byte gathers top out near 275 G/s (x in L2) and 115 G/s (x 134 MB)
+  //    with <= 50% carveout, and fall to 65 / 44 G/s at a 100% carveout.
   const int sigma = (int)h->info.sigma;
   const int wbytes = h->wide ? 8 : 4;
   const int64_t tile_bytes = h->B * 12 + 32 * wbytes;
   const int stage_bytes = (int)((tile_bytes + 127) / 128 * 128);
   const int closed_bytes = (int)(std::min<int64_t>(h->B, kClosedSlots) * 8);
-  int l2 = 0;
-  CSR5G_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device));
-  const double x_bytes = 8.0 * (double)h->info.n;
   const bool random = h->lines_per_gather >= 8.0;
-  const bool x_spills = x_bytes > 0.75 * l2;
-  const int budget = !random ? 226 * 1024 : (x_spills ? 120 * 1024 : 150 * 1024);
+  int budget = !random ? 226 * 1024 : 104 * 1024;
+  if (const char* e = std::getenv("CSR5G_BUDGET_KB")) budget = std::atoi(e) * 1024;  // experiments
   h->x_mode = random ? 1 : 4;  // random: no L1 allocation; local: plain ld.global.nc
-  h->x_window = random && x_bytes > 32e6;  // random: keep x resident in L2
+  // No L2 persisting window on x by default: with the 2-stage random plan it
+  // gains < 1% (R-MAT s24 1.658 vs 1.669 ms) while its persisting lines outlive
+  // the launch and slowed the next unrelated SpMV by 13% (st27 0.504 vs 0.446
+  // ms).  CSR5G_XWINDOW=1 turns it on for experiments.
+  h->x_window = false;
   // stages: the tile being reduced + the next tile (its gathers go out as
   // soon as the current depth loop ends) + TMA lead; 2 minimum
   const int min_stages = 2;
-  int nw = spmv_threads(sigma) / 32, stages = random ? 3 : 4;
+  // random gathers: two stages -- the shared memory a third would take is
+  // worth more as L1 for outstanding gather misses (measured: R-MAT s24 at
+  // 150 KB, 7 warps: 2 stages 1.67 ms, 3 stages 2.11 ms)
+  int nw = spmv_threads(sigma) / 32, stages = random ? 2 : 4;
   auto need = [&](int w, int st) {
     return 512 + w * (closed_bytes + kEoSlots * 4 + st * stage_bytes);
   };
