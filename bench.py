@@ -7,14 +7,19 @@
 One step = one CSR5 SpMV y = A x over the whole matrix (one pass of the hot
 path).  At N=1 the workload is BASELINE config 2, the 3D 27-point stencil
 200^3 (213.8M nnz, sigma = 27 by the reference rule, 64-bit descriptors).
-Under torchrun (N>1) the same matrix is tile-range sharded over the ranks with
-x replicated (strong scaling); a step includes the boundary-row exchange.
+Under torchrun (N>1) the matrix is tile-range sharded over the ranks with x
+replicated; a step includes the boundary-row exchange (NCCL).  Default
+--scaling weak: the global matrix is N times the 1-GPU one (the stencil N
+times deeper along z, graphs log2 N scales larger: R-MAT s24 -> s27 at N=8,
+BASELINE config 5), so per-GPU work is fixed; --scaling strong shards the
+1-GPU matrix itself.
 
 `value` is GFLOP/s = 2*nnz / t with A and x resident in HBM; t is the max over
 ranks of CUDA-event time on the launching stream.  The matrix (2.76 GB) is far
 larger than the 126 MB L2, so no L2 flush is done between steps; x (64 MB) is
 reused across steps as it is within one SpMV.  `e2e` is the same metric through
-the host-buffer call: pinned x H2D + SpMV + y D2H per step.  The roofline
+the host-buffer call (csr5.spmv_host_batch): per step pinned x H2D + SpMV + y
+D2H, pipelined across steps on separate copy engines.  The roofline
 figure is for the dominant tile kernel alone (events around it), with the
 algorithmic bytes of SURVEY 8(d).
 """
@@ -120,7 +125,7 @@ def host_matrix(workload: dict):
 
     from oracle.oracle import Csr, Oracle, stencil
     if workload["gen"] == "stencil":
-        return stencil(Oracle(), workload["kind"], workload["a"])
+        return stencil(Oracle(), workload["kind"], workload["a"], workload.get("layers"))
     from paper_1503_05032_b200.synthetic import make_matrix
     d = make_matrix(workload, "cuda")
     a = Csr(d.m, d.n, d.row_ptr.cpu().numpy(), d.col_idx.cpu().numpy().astype(np.int64),
@@ -131,7 +136,8 @@ def host_matrix(workload: dict):
 
 def workload_n(workload: dict) -> int:
     if workload["gen"] == "stencil":
-        return workload["a"] ** (3 if workload["kind"] == 1 else 2)
+        return workload["a"] ** (2 if workload["kind"] == 1 else 1) * workload.get("layers",
+                                                                                 workload["a"])
     return 1 << (workload["scale"] if workload["gen"] == "rmat" else workload["log2_m"])
 
 
@@ -177,6 +183,27 @@ def reference_cpu(workload: dict, x, budget_s: float, omega=4, sigma=16, steps=N
                 csr_scalar_ms=scalar, omega=omega, sigma=sigma, y=y)
 
 
+def est_nnz(wl: dict) -> int:
+    from oracle.oracle import stencil_box_size
+    if wl["gen"] == "stencil":
+        return stencil_box_size(wl["kind"], wl["a"], wl.get("layers", wl["a"]))[1]
+    if wl["gen"] == "rmat":
+        return wl["edge_factor"] << wl["scale"]
+    return int((1 << wl["log2_m"]) * (1 - wl["p_empty"]) * (wl["min_len"] + wl["max_len"]) / 2
+               + wl["n_long"] * wl["long_len"])
+
+
+def mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return None
+
+
 def cpu_info():
     model = "unknown"
     try:
@@ -197,18 +224,30 @@ def run_reference(args, workload_name, workload):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_1503_05032_b200.synthetic import bench_x
+    from paper_1503_05032_b200.synthetic import bench_x, scaled_workload
+    note = "1-GPU workload"
+    if world > 1 and args.scaling == "weak":
+        # the same global matrix as our arm, when the host can hold the
+        # reference's copies of it (~40 B per nonzero: int64 CSR + Csr5Matrix)
+        wl_g = scaled_workload(workload, world)
+        need = 40 * est_nnz(wl_g)
+        avail = mem_available()
+        if avail is None or need < 0.6 * avail:
+            workload, note = wl_g, f"global matrix of the {world}-GPU weak-scaling run"
+        else:
+            note = (f"1-GPU workload: the {world}x matrix needs ~{need / 1e9:.0f} GB of host RAM, "
+                    f"{avail / 1e9:.0f} GB available")
     r = reference_cpu(workload, bench_x(workload_n(workload)), 0.0, steps=args.steps,
                       warmup=args.warmup)
     ms = r["mean_ms"]
     gf = 2.0 * r["nnz"] / (ms * 1e6)
     model, ncpu = cpu_info()
-    sample = (f"full {workload_name} matrix, reference csr5::spmv_csr5 omega={r['omega']} "
-              f"sigma={r['sigma']} deterministic, one call per step")
+    sample = (f"full {workload_name} matrix ({note}, nnz={r['nnz']}), reference csr5::spmv_csr5 "
+              f"omega={r['omega']} sigma={r['sigma']} deterministic, one call per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": gf, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name, "desc": workload["desc"], "nnz": r["nnz"],
                    "m": r["m"], "omega": r["omega"], "sigma": r["sigma"], "mode": "deterministic"},
         "cpu_baseline": {"value": gf, "unit": UNIT, "cores": r["threads"], "kind": "reference",
@@ -230,20 +269,38 @@ def run_ours(args, workload_name, workload):
     from paper_1503_05032_b200 import csr5, mg
     from paper_1503_05032_b200.synthetic import bench_x
     rank, world, local = dist_env()
+    if os.environ.get("CSR5G_SHARE_GPU") == "1":  # functional multi-rank check on one GPU
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL over NVLink; CSR5G_DIST_BACKEND=gloo lets several ranks share one
+        # GPU for a functional check of the sharded flow (not a timing)
+        backend = os.environ.get("CSR5G_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
-    from paper_1503_05032_b200.synthetic import make_matrix
-    a = make_matrix(workload, dev)
+    from paper_1503_05032_b200.synthetic import WorkloadMatrix, make_matrix, scaled_workload
+    if world == 1:
+        a = make_matrix(workload, dev)
+        m, n, nnz = a.m, a.n, a.nnz
+    else:
+        # weak: the global matrix is `world` times the 1-GPU one; strong: the
+        # 1-GPU matrix itself.  Either way each rank generates the global
+        # row_ptr and only its own slice of entries where the generator allows.
+        if args.scaling == "weak":
+            workload = scaled_workload(workload, world)
+        W = WorkloadMatrix(workload, dev)
+        m, n, nnz = W.m, W.n, W.nnz
     torch.cuda.synchronize()
-    x_host = bench_x(a.n)
+    x_host = bench_x(n)
     x = torch.as_tensor(x_host).to(dev)
-    y = torch.empty(a.m, dtype=torch.float64, device=dev)
-    sigma = csr5.select_sigma(a.nnz / a.m)
+    y = torch.empty(m, dtype=torch.float64, device=dev)
+    sigma = csr5.select_sigma(nnz / m)
 
     # -- conversion (device-resident CSR -> usable CSR5), timed twice --------
     if world == 1:
@@ -256,26 +313,42 @@ def run_ours(args, workload_name, workload):
         info = a5.info
         run = lambda: csr5.spmv_csr5(a5, x, y)  # noqa: E731
     else:
-        lo, hi = mg.Csr5Sharded.slices_for(a.nnz, sigma, rank, world)
+        lo, hi = mg.Csr5Sharded.slices_for(nnz, sigma, rank, world)
+        col_s, val_s = W.entries(lo, hi)
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sh = mg.Csr5Sharded(a.row_ptr, a.col_idx[lo:], a.val[lo:], a.m, a.n, a.nnz, sigma, rank,
-                            world)
+        sh = mg.Csr5Sharded(W.row_ptr, col_s, val_s, m, n, nnz, sigma, rank, world)
+        torch.cuda.synchronize()
         conv_ms = (time.perf_counter() - t0) * 1e3
+        del col_s, val_s
         a5 = sh.a5
-        info = a5.info
+        info = a5.info if a5 is not None else None
         run = lambda: sh.spmv(x, y)  # noqa: E731
 
     # -- correctness guard before timing (bench.cpp:130-141 analogue) --------
+    # y over the rows this rank writes, against cuSPARSE (torch sparse CSR)
     run()
     torch.cuda.synchronize()
-    A = torch.sparse_csr_tensor(a.row_ptr, a.col_idx.long(), a.val, (a.m, a.n))
-    y_chk = (A @ x.unsqueeze(1)).squeeze(1)
-    own = (info.own_row_begin, info.own_row_end)
-    err = ((y[own[0]:own[1]] - y_chk[own[0]:own[1]]).abs() /
-           y_chk[own[0]:own[1]].abs().clamp(min=1.0)).max().item()
+    if world == 1:
+        own = (0, m)
+        rp_own, col_own, val_own = a.row_ptr, a.col_idx, a.val
+    else:
+        own = sh.own
+        rp_own = W.row_ptr[own[0]:own[1] + 1]
+        e0, e1 = (int(rp_own[0]), int(rp_own[-1])) if own[1] > own[0] else (0, 0)
+        col_own, val_own = W.entries(e0, e1)
+        rp_own = rp_own - e0
+    err = 0.0
+    if own[1] > own[0]:
+        A = torch.sparse_csr_tensor(rp_own, col_own.long(), val_own, (own[1] - own[0], n))
+        y_chk = (A @ x.unsqueeze(1)).squeeze(1)
+        err = ((y[own[0]:own[1]] - y_chk).abs() / y_chk.abs().clamp(min=1.0)).max().item()
+        del A, y_chk
+    del rp_own, col_own, val_own
+    if world > 1:
+        W.drop()
     if not err <= 1e-12:
         raise SystemExit(f"correctness guard: max relative error {err} > 1e-12")
-    del A, y_chk
 
     def barrier():
         if dist is not None:
@@ -284,14 +357,15 @@ def run_ours(args, workload_name, workload):
     def max_over_ranks(v: float) -> float:
         if dist is None:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64,
+                         device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
     # A working set that fits in L2 (126 MB) would be re-read from L2 by
     # back-to-back steps: flush it between steps (outside the events) then.
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush = info.spmv_bytes < 4 * l2_bytes
+    flush = info is not None and info.spmv_bytes < 4 * l2_bytes
     scrub = torch.empty(2 * l2_bytes // 8 + 1, dtype=torch.float64, device=dev) if flush else None
 
     for _ in range(args.warmup):
@@ -311,7 +385,7 @@ def run_ours(args, workload_name, workload):
         if world == 1:
             csr5.spmv_csr5_evt(a5, x, y, tk[k][0], tk[k][1])
         else:
-            run()
+            sh.spmv(x, y, events=tk[k])
         steps_ev[k][1].record()
     torch.cuda.synchronize()
     barrier()
@@ -319,29 +393,51 @@ def run_ours(args, workload_name, workload):
     clk = clocks.stop()
     total_ms = max_over_ranks(sum(b.elapsed_ms(e) for b, e in steps_ev))
     ms = total_ms / args.steps
-    tile_ms = (sum(b.elapsed_ms(e) for b, e in tk) / args.steps) if world == 1 else None
+    tile_ms = (sum(b.elapsed_ms(e) for b, e in tk) / args.steps) if a5 is not None else None
 
     # -- end to end through the host-buffer call ------------------------------
-    xh = torch.as_tensor(x_host).pin_memory()
-    yh = torch.empty(a.m, dtype=torch.float64).pin_memory()
+    # Every step moves its own x in from pinned host memory and its y out.
+    # N=1: csr5.spmv_host_batch (csr5g_spmv_host_batch), which pipelines step
+    # k+1's x H2D and step k's y D2H around SpMV k on separate copy engines.
+    # The serial form (H2D, SpMV, D2H back to back on one stream) is reported
+    # beside it.  N>1: the serial form through the sharded driver.
+    ring = min(args.steps, 4)
+    xh = [torch.as_tensor(x_host).pin_memory() for _ in range(ring)]
+    yh = [torch.empty(m, dtype=torch.float64).pin_memory() for _ in range(ring)]
 
-    def e2e_step():
-        x.copy_(xh, non_blocking=True)
+    def e2e_serial(k):
+        x.copy_(xh[k % ring], non_blocking=True)
         run()
-        yh.copy_(y, non_blocking=True)
-    for _ in range(args.warmup):
-        e2e_step()
-    e0, e1 = csr5.Event(), csr5.Event()
-    torch.cuda.synchronize()
-    barrier()
-    e0.record()
-    for _ in range(args.steps):
-        e2e_step()
-    e1.record()
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(e0.elapsed_ms(e1)) / args.steps
+        yh[k % ring].copy_(y, non_blocking=True)
 
-    flops = 2.0 * a.nnz
+    def e2e_timed(fn):
+        e0, e1 = csr5.Event(), csr5.Event()
+        torch.cuda.synchronize()
+        barrier()
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_ms(e1)) / args.steps
+
+    for k in range(args.warmup):
+        e2e_serial(k)
+    e2e_serial_ms = e2e_timed(lambda: [e2e_serial(k) for k in range(args.steps)])
+    e2e_path = "serial: pinned x H2D + spmv + y D2H per step, one stream, CUDA events"
+    e2e_ms = e2e_serial_ms
+    if world == 1:
+        xs = [xh[k % ring] for k in range(args.steps)]
+        ys = [yh[k % ring] for k in range(args.steps)]
+        csr5.spmv_host_batch(a5, xs[:args.warmup], ys[:args.warmup])
+        e2e_ms = e2e_timed(lambda: csr5.spmv_host_batch(a5, xs, ys))
+        e2e_path = ("csr5.spmv_host_batch (csr5g_spmv_host_batch): per step pinned x H2D + SpMV + "
+                    "y D2H, x_{k+1} H2D and y_k D2H overlapping SpMV k; CUDA events on the "
+                    "caller stream")
+        err_h = float(np.max(np.abs(yh[(args.steps - 1) % ring].numpy() - y.cpu().numpy())))
+        if err_h != 0.0:
+            raise SystemExit(f"host-batch path differs from the device path by {err_h}")
+
+    flops = 2.0 * nnz
     value = flops / (ms * 1e6)
     peak, peak_src = peaks()
     line = None
@@ -378,9 +474,9 @@ def run_ours(args, workload_name, workload):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name, "desc": workload["desc"], "m": a.m, "n": a.n,
-                       "nnz": a.nnz, "omega": 32, "sigma": sigma, "p": info.p,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name, "desc": workload["desc"], "m": m, "n": n,
+                       "nnz": nnz, "omega": 32, "sigma": sigma, "p": info.p,
                        "desc_word_bits": info.word_bits, "mode": "deterministic",
                        "spmv_plan": {"lines_per_gather": round(info.lines_per_gather, 2),
                                      "warps_per_cta": info.warps_per_cta, "stages": info.stages,
@@ -399,9 +495,10 @@ def run_ours(args, workload_name, workload):
                            "spmv_equiv_excl_alloc": (conv_ms - info.alloc_ms) / ms},
             "cpu_baseline": cpu,
             "e2e": {"value": flops / (e2e_ms * 1e6), "unit": UNIT,
-                    "h2d_bytes_per_step": 8 * a.n, "d2h_bytes_per_step": 8 * a.m,
-                    "ms_per_step": e2e_ms,
-                    "path": "pinned x H2D + csr5.spmv_csr5 + y D2H, CUDA events"},
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * m,
+                    "ms_per_step": e2e_ms, "path": e2e_path,
+                    "serial_value": flops / (e2e_serial_ms * 1e6),
+                    "serial_ms_per_step": e2e_serial_ms},
             "gpu_launches": args.steps * (2 if world == 1 else 3),
             "clocks": clk,
             "correctness_max_rel_err": err,
@@ -424,6 +521,9 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="st27_200")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N>1: weak = the global matrix is N times the 1-GPU workload (stencils "
+                         "N times deeper, graphs log2 N scales larger); strong = the same matrix")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -151,6 +151,17 @@ CSR5G_API int csr5g_build_host(int device, int64_t m, int64_t n, int64_t nnz,
                                const double *h_val, const csr5g_params *params,
                                csr5g_matrix *out);
 CSR5G_API int csr5g_spmv_host(csr5g_matrix h, const double *h_x, double *h_y, int32_t mode);
+
+/* Batch of independent SpMVs on host vectors (spmv.hpp:58-61 called `count`
+ * times): y_k = A x_k for h_xs[k] (n doubles) / h_ys[k] (m doubles).  The
+ * copies run as a pipeline over two device buffer pairs on the handle's own
+ * streams -- x_{k+1} H2D and y_k D2H overlap SpMV k -- so pinned host buffers
+ * give one PCIe transfer time per step instead of the sum.  Stream-ordered:
+ * starts after work queued on `stream`, and `stream` continues after the last
+ * y copy; the host buffers must stay valid until then. */
+CSR5G_API int csr5g_spmv_host_batch(csr5g_matrix h, const double *const *h_xs,
+                                    double *const *h_ys, int64_t count, int32_t mode,
+                                    void *stream);
 CSR5G_API int csr5g_to_csr_host(csr5g_matrix h, int64_t *h_col_idx, double *h_val);
 
 /* Implicit destruction of Csr5Matrix (value type) -> explicit release. */
@@ -169,6 +180,16 @@ CSR5G_API int csr5g_event_destroy(void *ev);
 CSR5G_API int csr5g_stencil_size(int32_t kind, int64_t a, int64_t *m, int64_t *nnz);
 CSR5G_API int csr5g_stencil_fill(int32_t kind, int64_t a, int64_t *d_row_ptr, int32_t *d_col_idx,
                        double *d_val, void *stream);
+/* Box variant for weak scaling: the outermost axis (y in 2D, z in 3D) has
+ * `layers` points instead of a (layers = a is the stencil above).  Writes the
+ * full row_ptr (m+1) but only the entries at global positions [pos_begin,
+ * pos_end) into d_col_idx / d_val (a shard's slice: pos_begin = 0, pos_end =
+ * nnz for the whole matrix). */
+CSR5G_API int csr5g_stencil_box_size(int32_t kind, int64_t a, int64_t layers, int64_t *m,
+                                     int64_t *nnz);
+CSR5G_API int csr5g_stencil_box_fill(int32_t kind, int64_t a, int64_t layers, int64_t pos_begin,
+                                     int64_t pos_end, int64_t *d_row_ptr, int32_t *d_col_idx,
+                                     double *d_val, void *stream);
 
 /* Irregular synthetic matrices on the device (BASELINE configs 3-5).  Two
  * phases: *_create generates and sizes the matrix (m, nnz) and keeps it in a

@@ -514,15 +514,24 @@ def have_ref() -> bool:
     return os.path.exists(LIB_REF)
 
 
-def stencil(orc: "Oracle", kind: int, a: int) -> Csr:
-    """Host twin of csr5g_stencil_fill (testgen.c orc_stencil)."""
+def stencil_box_size(kind: int, a: int, layers: int) -> tuple[int, int]:
+    """(m, nnz) of the a x .. x layers stencil (mirrors csr5g_stencil_box_size)."""
+    def ax(e):
+        return 1 if e == 1 else 3 * e - 2
+    if kind == 0:
+        return a * layers, a * layers + 2 * (a - 1) * layers + 2 * (layers - 1) * a
+    return a * a * layers, ax(a) * ax(a) * ax(layers)
+
+
+def stencil(orc: "Oracle", kind: int, a: int, layers: int | None = None) -> Csr:
+    """Host twin of csr5g_stencil_box_fill (testgen.c orc_stencil_box)."""
     import ctypes as C
-    m = a * a if kind == 0 else a * a * a
-    nnz = (1 if a == 1 else 5 * a * a - 4 * a) if kind == 0 else (1 if a == 1 else (3 * a - 2) ** 3)
+    layers = a if layers is None else layers
+    m, nnz = stencil_box_size(kind, a, layers)
     rp = np.empty(m + 1, np.int64)
     ci = np.empty(nnz, np.int64)
     va = np.empty(nnz, np.float64)
-    fn = orc.L.orc_stencil
-    fn.argtypes = [C.c_int, C.c_int64, _i64p, _i64p, _f64p]
-    fn(kind, a, _p(rp, _i64p), _p(ci, _i64p), _p(va, _f64p))
+    fn = orc.L.orc_stencil_box
+    fn.argtypes = [C.c_int, C.c_int64, C.c_int64, _i64p, _i64p, _f64p]
+    fn(kind, a, layers, _p(rp, _i64p), _p(ci, _i64p), _p(va, _f64p))
     return Csr(m, m, rp, ci, va)

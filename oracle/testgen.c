@@ -270,18 +270,20 @@ int orc_generate_synthetic(int kind, int64_t m, int64_t n, int64_t nnz_target, u
   return rc;
 }
 
-/* Host twin of csr5g_stencil_fill (paper_1503_05032_b200/csrc/synth.cu) for the
- * reference arm of bench.py: kind 0 = 2D 5-point (a x a), kind 1 = 3D
- * 27-point (a^3).  Caller buffers: row_ptr[m+1], col_idx[nnz], val[nnz]. */
-void orc_stencil(int kind, int64_t a, int64_t *row_ptr, int64_t *col_idx, double *val) {
-  const int64_t m = kind == 0 ? a * a : a * a * a;
+/* Host twin of csr5g_stencil_box_fill (paper_1503_05032_b200/csrc/synth.cu)
+ * for the reference arm of bench.py: kind 0 = 2D 5-point (a x layers), kind 1
+ * = 3D 27-point (a x a x layers); layers = a is the square / cube.  Caller
+ * buffers: row_ptr[m+1], col_idx[nnz], val[nnz]. */
+void orc_stencil_box(int kind, int64_t a, int64_t layers, int64_t *row_ptr, int64_t *col_idx,
+                     double *val) {
+  const int64_t m = kind == 0 ? a * layers : a * a * layers;
   int64_t q = 0;
   row_ptr[0] = 0;
   for (int64_t r = 0; r < m; ++r) {
     if (kind == 0) {
       const int64_t iy = r / a, ix = r - iy * a;
       const int64_t cand[5] = {r - a, r - 1, r, r + 1, r + a};
-      const int ok[5] = {iy > 0, ix > 0, 1, ix < a - 1, iy < a - 1};
+      const int ok[5] = {iy > 0, ix > 0, 1, ix < a - 1, iy < layers - 1};
       for (int k = 0; k < 5; ++k)
         if (ok[k]) {
           col_idx[q] = cand[k];
@@ -291,7 +293,7 @@ void orc_stencil(int kind, int64_t a, int64_t *row_ptr, int64_t *col_idx, double
     } else {
       const int64_t z = r / (a * a), rem = r - z * a * a, y = rem / a, x = rem - y * a;
       for (int dz = -1; dz <= 1; ++dz) {
-        if (z + dz < 0 || z + dz >= a) continue;
+        if (z + dz < 0 || z + dz >= layers) continue;
         for (int dy = -1; dy <= 1; ++dy) {
           if (y + dy < 0 || y + dy >= a) continue;
           for (int dx = -1; dx <= 1; ++dx) {
@@ -305,4 +307,8 @@ void orc_stencil(int kind, int64_t a, int64_t *row_ptr, int64_t *col_idx, double
     }
     row_ptr[r + 1] = q;
   }
+}
+
+void orc_stencil(int kind, int64_t a, int64_t *row_ptr, int64_t *col_idx, double *val) {
+  orc_stencil_box(kind, a, a, row_ptr, col_idx, val);
 }

@@ -75,6 +75,7 @@ SIGNATURES = {
     "csr5g_build_host": (C.c_int, [C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, C.POINTER(Params),
                                    C.POINTER(_vp)]),
     "csr5g_spmv_host": (C.c_int, [_vp, _vp, _vp, _i32]),
+    "csr5g_spmv_host_batch": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
     "csr5g_to_csr_host": (C.c_int, [_vp, _vp, _vp]),
     "csr5g_event_create": (C.c_int, [C.POINTER(_vp)]),
     "csr5g_event_record": (C.c_int, [_vp, _vp]),
@@ -82,6 +83,8 @@ SIGNATURES = {
     "csr5g_event_destroy": (C.c_int, [_vp]),
     "csr5g_stencil_size": (C.c_int, [_i32, _i64, C.POINTER(_i64), C.POINTER(_i64)]),
     "csr5g_stencil_fill": (C.c_int, [_i32, _i64, _vp, _vp, _vp, _vp]),
+    "csr5g_stencil_box_size": (C.c_int, [_i32, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64)]),
+    "csr5g_stencil_box_fill": (C.c_int, [_i32, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
     "csr5g_rmat_create": (C.c_int, [_i32, _i32, C.c_uint64, _i32, _vp, C.POINTER(_vp),
                                     C.POINTER(_i64), C.POINTER(_i64)]),
     "csr5g_mixed_create": (C.c_int, [_i32, C.c_double, _i32, _i64, _i32, _i32, C.c_uint64, _vp,

@@ -202,9 +202,46 @@ def spmv_csr5(a5: Csr5Matrix, x: torch.Tensor, y: torch.Tensor | None = None,
 
 
 def spmv_host(a5: Csr5Matrix, x: np.ndarray, mode="deterministic") -> np.ndarray:
-    """Host-vector overload (spmv.hpp:60): stages x to the device and y back."""
-    xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64)).to(f"cuda:{a5.device}")
-    return spmv_csr5(a5, xd, mode=mode).cpu().numpy()
+    """Host-vector overload (spmv.hpp:60) through csr5g_spmv_host: x H2D, SpMV,
+    y D2H on the handle's pipeline; returns a new host y."""
+    if mode not in _MODES:
+        raise ValueError(f"spmv: unknown mode {mode!r}")
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.ndim != 1 or x.size != a5.n:
+        raise ValueError(f"spmv: x has length {x.size}, expected {a5.n}")
+    y = np.empty(a5.m, dtype=np.float64)
+    with torch.cuda.device(a5.device):
+        check(lib().csr5g_spmv_host(a5.handle, x.ctypes.data, y.ctypes.data, _MODES[mode]))
+    return y
+
+
+def _host_ptr(v, length: int, what: str) -> int:
+    if isinstance(v, torch.Tensor):
+        if v.is_cuda or v.dtype != torch.float64 or not v.is_contiguous() or v.numel() != length:
+            raise ValueError(f"spmv: {what} must be a contiguous host float64 tensor of length "
+                             f"{length}")
+        return v.data_ptr()
+    if (not isinstance(v, np.ndarray) or v.dtype != np.float64 or not v.flags.c_contiguous
+            or v.size != length):
+        raise ValueError(f"spmv: {what} must be a contiguous float64 array of length {length}")
+    return v.ctypes.data
+
+
+def spmv_host_batch(a5: Csr5Matrix, xs, ys, mode="deterministic", stream=None) -> None:
+    """y_k = A x_k for host vectors xs[k] -> ys[k] (numpy arrays or CPU tensors,
+    pinned for overlap): one H2D + SpMV + D2H per vector, pipelined so that
+    x_{k+1}'s copy in and y_k's copy out overlap SpMV k (csr5g_spmv_host_batch).
+    Stream-ordered on `stream`: synchronise it before reading ys."""
+    if len(xs) != len(ys):
+        raise ValueError(f"spmv: {len(xs)} x vectors but {len(ys)} y vectors")
+    if mode not in _MODES:
+        raise ValueError(f"spmv: unknown mode {mode!r}")
+    k = len(xs)
+    px = (C.c_void_p * max(k, 1))(*[_host_ptr(v, a5.n, "x") for v in xs])
+    py = (C.c_void_p * max(k, 1))(*[_host_ptr(v, a5.m, "y") for v in ys])
+    with torch.cuda.device(a5.device):
+        check(lib().csr5g_spmv_host_batch(a5.handle, px, py, k, _MODES[mode],
+                                          _stream_ptr(stream)))
 
 
 def csr5_to_csr(a5: Csr5Matrix, row_ptr: torch.Tensor, stream=None) -> CsrMatrix:
@@ -261,6 +298,28 @@ def stencil(kind: int, a: int, device="cuda", stream=None) -> CsrMatrix:
     check(lib().csr5g_stencil_fill(kind, a, rp.data_ptr(), ci.data_ptr(), va.data_ptr(),
                                    _stream_ptr(stream)))
     return CsrMatrix(m.value, m.value, rp, ci, va)
+
+
+def stencil_box_size(kind: int, a: int, layers: int) -> tuple[int, int]:
+    """(m, nnz) of the stencil on an a x .. x layers box (csr5g_stencil_box_size)."""
+    m, nnz = C.c_int64(), C.c_int64()
+    check(lib().csr5g_stencil_box_size(kind, a, layers, C.byref(m), C.byref(nnz)))
+    return m.value, nnz.value
+
+
+def stencil_box(kind: int, a: int, layers: int, pos_begin: int = 0, pos_end: int | None = None,
+                device="cuda", stream=None):
+    """Stencil on a box whose outermost axis has `layers` points: the full
+    row_ptr and the entries at global positions [pos_begin, pos_end) (a shard's
+    slice).  Returns (m, nnz, row_ptr, col_slice, val_slice)."""
+    m, nnz = stencil_box_size(kind, a, layers)
+    hi = nnz if pos_end is None else pos_end
+    rp = torch.empty(m + 1, dtype=torch.int64, device=device)
+    ci = torch.empty(max(hi - pos_begin, 0), dtype=torch.int32, device=device)
+    va = torch.empty(max(hi - pos_begin, 0), dtype=torch.float64, device=device)
+    check(lib().csr5g_stencil_box_fill(kind, a, layers, pos_begin, hi, rp.data_ptr(),
+                                       ci.data_ptr(), va.data_ptr(), _stream_ptr(stream)))
+    return m, nnz, rp, ci, va
 
 
 def _from_generator(gen: C.c_void_p, m: int, nnz: int, device, stream) -> CsrMatrix:
@@ -329,5 +388,5 @@ def spmv_csr5_evt(a5: Csr5Matrix, x: torch.Tensor, y: torch.Tensor, ev0: Event, 
 
 
 __all__ = ["TuningParams", "CsrMatrix", "Csr5Matrix", "csr_to_csr5", "csr_to_csr5_shard",
-           "spmv_csr5", "spmv_host", "csr5_to_csr", "dump_format", "select_sigma", "layout",
-           "stencil", "Event", "spmv_csr5_evt", "Partial"]
+           "spmv_csr5", "spmv_host", "spmv_host_batch", "csr5_to_csr", "dump_format", "select_sigma", "layout",
+           "stencil", "stencil_box", "stencil_box_size", "Event", "spmv_csr5_evt", "Partial"]

@@ -234,29 +234,37 @@ int csr5g_build_host(int device, int64_t m, int64_t n, int64_t nnz, const int64_
   return done(csr5g_build(device, m, n, nnz, d_rp, d_ci, d_va, params, nullptr, out));
 }
 
+static int check_mode(int32_t mode) {
+  if (mode != CSR5G_MODE_DETERMINISTIC && mode != CSR5G_MODE_ATOMIC)
+    return fail(CSR5G_EINVAL, "csr5g: unknown spmv mode " + std::to_string(mode));
+  return CSR5G_OK;
+}
+
 int csr5g_spmv_host(csr5g_matrix h, const double* h_x, double* h_y, int32_t mode) {
   if (!h) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
   const csr5g_info& in = h->h->info;
-  CSR5G_CUDA(cudaSetDevice(h->h->device));
-  double *dx = nullptr, *dy = nullptr;
-  auto done = [&](int rc) {
-    cudaFree(dx);
-    cudaFree(dy);
-    return rc;
-  };
-  cudaError_t e;
-  if ((e = cudaMalloc(&dx, sizeof(double) * std::max<int64_t>(in.n, 1))) != cudaSuccess ||
-      (e = cudaMalloc(&dy, sizeof(double) * std::max<int64_t>(in.m, 1))) != cudaSuccess)
-    return done(cuda_fail(e, "cudaMalloc(x/y)"));
-  if (in.n > 0 &&
-      (e = cudaMemcpy(dx, h_x, sizeof(double) * in.n, cudaMemcpyHostToDevice)) != cudaSuccess)
-    return done(cuda_fail(e, "cudaMemcpy(x)"));
-  int rc = csr5g_spmv(h, dx, dy, mode, nullptr);
-  if (rc) return done(rc);
-  if (in.m > 0 &&
-      (e = cudaMemcpy(h_y, dy, sizeof(double) * in.m, cudaMemcpyDeviceToHost)) != cudaSuccess)
-    return done(cuda_fail(e, "cudaMemcpy(y)"));
-  return done(CSR5G_OK);
+  if (in.m > 0 && !h_y) return fail(CSR5G_EINVAL, "spmv: y is NULL");
+  if (in.n > 0 && !h_x) return fail(CSR5G_EINVAL, "spmv: x is NULL");
+  if (int rc = check_mode(mode)) return rc;
+  int rc = spmv_host_batch(h->h, &h_x, &h_y, 1, mode, nullptr);
+  if (rc) return rc;
+  CSR5G_CUDA(cudaStreamSynchronize(nullptr));
+  return CSR5G_OK;
+}
+
+int csr5g_spmv_host_batch(csr5g_matrix h, const double* const* h_xs, double* const* h_ys,
+                          int64_t count, int32_t mode, void* stream) {
+  if (!h) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
+  if (count < 0) return fail(CSR5G_EINVAL, "csr5g: negative batch count");
+  if (count == 0) return CSR5G_OK;
+  if (!h_xs || !h_ys) return fail(CSR5G_EINVAL, "csr5g: NULL vector list");
+  const csr5g_info& in = h->h->info;
+  for (int64_t k = 0; k < count; ++k) {
+    if (in.m > 0 && !h_ys[k]) return fail(CSR5G_EINVAL, "spmv: y is NULL");
+    if (in.n > 0 && !h_xs[k]) return fail(CSR5G_EINVAL, "spmv: x is NULL");
+  }
+  if (int rc = check_mode(mode)) return rc;
+  return spmv_host_batch(h->h, h_xs, h_ys, count, mode, static_cast<cudaStream_t>(stream));
 }
 
 int csr5g_to_csr_host(csr5g_matrix h, int64_t* h_col_idx, double* h_val) {

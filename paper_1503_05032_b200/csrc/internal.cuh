@@ -66,6 +66,8 @@ struct SpmvArgs {
   int32_t early_gather;    // random gathers: issue tile k+1's gathers before tile k's depth loop
 };
 
+struct Pipeline;  // pipeline.cu: host-vector copy/compute pipeline
+
 struct Handle {
   int device = 0;
   csr5g_info info{};
@@ -91,6 +93,7 @@ struct Handle {
   int x_mode = 0;                 // gather path chosen by the plan
   bool x_window = false;          // L2 persisting window on x
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
+  Pipeline* pipe = nullptr;  // created by the first host-vector SpMV
 };
 
 // ---- errors --------------------------------------------------------------
@@ -116,6 +119,9 @@ int launch_fixup(Handle* h, const csr5g_partial* d_all, int world, int rank, dou
                  cudaStream_t stream);
 int launch_to_csr(Handle* h, int32_t* d_col, double* d_val, cudaStream_t stream);
 int spmv_plan(Handle* h, int sms);
+int spmv_host_batch(Handle* h, const double* const* xs, double* const* ys, int64_t count,
+                    int mode, cudaStream_t stream);
+void free_pipeline(Pipeline* p);
 
 // ---- device helpers ----------------------------------------------------------
 __device__ __forceinline__ uint64_t policy_evict_first() {

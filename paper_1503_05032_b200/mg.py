@@ -67,6 +67,30 @@ def owned_ranges(infos) -> list[tuple[int, int]]:
     return [(int(i.own_row_begin), int(i.own_row_end)) for i in infos]
 
 
+def _staged(dist, group=None) -> bool:
+    """gloo process groups (CPU tests, or several ranks sharing one GPU for a
+    functional check) stage CUDA tensors through host memory."""
+    return dist.get_backend(group) == "gloo"
+
+
+def all_gather_flat(dist, out, inp, group=None):
+    """out[world * k] <- every rank's inp[k]: NCCL all_gather_into_tensor, or a
+    host-staged list all_gather on gloo."""
+    if not _staged(dist, group) or not inp.is_cuda:
+        if _staged(dist, group):
+            parts = list(out.view(-1, inp.numel()).unbind(0))
+            dist.all_gather(parts, inp, group=group)
+        else:
+            dist.all_gather_into_tensor(out, inp, group=group)
+        return out
+    import torch
+    h = inp.cpu()
+    parts = [torch.empty_like(h) for _ in range(out.numel() // inp.numel())]
+    dist.all_gather(parts, h, group=group)
+    out.copy_(torch.cat(parts).to(out.device))
+    return out
+
+
 def exchange_records(dist, send, world: int, group=None):
     """All-gather every rank's 16-byte boundary record (int64 row, f64 value
     bits) -> [world, 2] int64 on send's device.  Backend-agnostic (NCCL on the
@@ -107,24 +131,28 @@ class Csr5Sharded:
         if self.active:
             check(lib().csr5g_set_send_buffer(self.a5.handle, C.c_void_p(self.send.data_ptr())))
         own = torch.tensor([self.own[0], self.own[1]], dtype=torch.int64, device=dev)
-        allown = [torch.zeros_like(own) for _ in range(world)]
-        dist.all_gather(allown, own, group=group)
-        self.ranges = [(int(t[0]), int(t[1])) for t in allown]
+        allown = torch.zeros(2 * world, dtype=torch.int64, device=dev)
+        all_gather_flat(dist, allown, own, group)
+        t = allown.cpu().tolist()
+        self.ranges = [(t[2 * g], t[2 * g + 1]) for g in range(world)]
 
     @staticmethod
     def slices_for(nnz: int, sigma: int, rank: int, world: int):
         v = shard_view(nnz, sigma, rank, world)
         return (0, 0) if v is None else (v.pos_begin, v.pos_end)
 
-    def spmv(self, x, y):
-        """y[own rows] = (A x)[own rows]; other rows of y are scratch."""
-        from .csr5 import spmv_csr5
+    def spmv(self, x, y, events=None):
+        """y[own rows] = (A x)[own rows]; other rows of y are scratch.  `events`
+        (csr5.Event pair) brackets this rank's tile kernel."""
+        from .csr5 import spmv_csr5, spmv_csr5_evt
         torch = self.torch
-        if self.active:
+        if self.active and events is not None:
+            spmv_csr5_evt(self.a5, x, y, events[0], events[1])
+        elif self.active:
             spmv_csr5(self.a5, x, y)
         else:
             self.send.copy_(torch.tensor([-1, 0], dtype=torch.int64, device=self.send.device))
-        self.dist.all_gather_into_tensor(self.table, self.send, group=self.group)
+        all_gather_flat(self.dist, self.table, self.send, self.group)
         if self.active:
             check(lib().csr5g_fixup(self.a5.handle, C.c_void_p(self.table.data_ptr()),
                                     self.world_eff, self.rank, C.c_void_p(y.data_ptr()),
@@ -141,18 +169,16 @@ class Csr5Sharded:
 def gather_owned(dist, y, x, ranges, rank, group=None):
     """x[lo:hi] <- rank g's y[lo:hi] for every g (host logic shared with the
     gloo tests)."""
+    staged = _staged(dist, group) and x.is_cuda
     for g, (lo, hi) in enumerate(ranges):
         if hi <= lo:
             continue
-        buf = y[lo:hi] if g == rank else x[lo:hi]
         if g == rank:
-            x[lo:hi].copy_(buf)
-            dist.broadcast(x[lo:hi], src=g, group=group)
-        else:
-            t = x[lo:hi].contiguous()
-            dist.broadcast(t, src=g, group=group)
-            if t.data_ptr() != x[lo:hi].data_ptr():
-                x[lo:hi].copy_(t)
+            x[lo:hi].copy_(y[lo:hi])
+        t = x[lo:hi].cpu() if staged else x[lo:hi].contiguous()
+        dist.broadcast(t, src=g, group=group)
+        if g != rank and (staged or t.data_ptr() != x[lo:hi].data_ptr()):
+            x[lo:hi].copy_(t)
 
 
 # ---------------------------------------------------------------------------

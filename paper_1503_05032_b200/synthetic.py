@@ -83,6 +83,67 @@ WORKLOADS = {
 def make_matrix(wl: dict, device="cuda"):
     """The workload's CSR, generated on the device by libcsr5g."""
     from . import csr5
+    if wl["gen"] == "stencil" and wl.get("layers", wl["a"]) != wl["a"]:
+        m, nnz, rp, ci, va = csr5.stencil_box(wl["kind"], wl["a"], wl["layers"], device=device)
+        return csr5.CsrMatrix(m, m, rp, ci, va)
+    return _make_matrix(wl, device)
+
+
+def scaled_workload(wl: dict, world: int) -> dict:
+    """Weak scaling: the global problem on `world` GPUs is `world` times the
+    1-GPU problem -- stencils grow along the outermost axis (layers = a*world),
+    graphs by log2(world) in scale (R-MAT s24 at 8 GPUs is s27, BASELINE
+    config 5)."""
+    w = dict(wl)
+    if world == 1:
+        return w
+    if wl["gen"] == "stencil":
+        w["layers"] = wl["a"] * world
+    else:
+        if world & (world - 1):
+            raise ValueError("weak scaling of a graph workload needs a power-of-two GPU count")
+        k = world.bit_length() - 1
+        w["scale" if wl["gen"] == "rmat" else "log2_m"] += k
+    w["desc"] = f"{wl['desc']}; x{world} for weak scaling"
+    return w
+
+
+class WorkloadMatrix:
+    """A workload's global CSR for a multi-GPU rank: the full row_ptr on the
+    device and `entries(lo, hi)` giving (col_idx, val) at global positions
+    [lo, hi).  Stencils generate only what is asked for; graphs are generated
+    whole (their dedup is global) and sliced."""
+
+    def __init__(self, wl: dict, device="cuda"):
+        from . import csr5
+        self.wl, self.device = wl, device
+        if wl["gen"] == "stencil":
+            self.layers = wl.get("layers", wl["a"])
+            self.m, self.nnz = csr5.stencil_box_size(wl["kind"], wl["a"], self.layers)
+            _, _, self.row_ptr, _, _ = csr5.stencil_box(wl["kind"], wl["a"], self.layers, 0, 0,
+                                                        device=device)
+            self.full = None
+        else:
+            self.full = _make_matrix(wl, device)
+            self.m, self.nnz, self.row_ptr = self.full.m, self.full.nnz, self.full.row_ptr
+        self.n = self.m
+
+    def entries(self, lo: int, hi: int):
+        from . import csr5
+        if self.full is not None:
+            return self.full.col_idx[lo:hi], self.full.val[lo:hi]
+        _, _, _, ci, va = csr5.stencil_box(self.wl["kind"], self.wl["a"], self.layers, lo, hi,
+                                           device=self.device)
+        return ci, va
+
+    def drop(self):
+        """Release the whole-matrix arrays of a generated graph."""
+        self.full = None
+
+
+def _make_matrix(wl: dict, device="cuda"):
+    """The workload's CSR, generated on the device by libcsr5g."""
+    from . import csr5
     if wl["gen"] == "stencil":
         return csr5.stencil(wl["kind"], wl["a"], device=device)
     if wl["gen"] == "rmat":

@@ -227,3 +227,34 @@ def test_shards_concatenate_and_fix_up(g, orc):
                 assert np.array_equal(np.concatenate([e[f] for e in ex]), getattr(full, f)), f
             tp = np.concatenate([e["tile_ptr"][:-1] for e in ex[:-1]] + [ex[-1]["tile_ptr"]])
             assert np.array_equal(tp, full.tile_ptr)
+
+
+def test_host_vector_paths(g, orc):
+    """csr5g_spmv_host and the pipelined csr5g_spmv_host_batch (pinned and
+    pageable host vectors, batches longer than the two buffer pairs, a second
+    batch reusing the handle's pipeline) give the device path's y."""
+    rng = orc.rng(11)
+    a = orc.generate_synthetic(2, 4000, 3000, 90000, 9)
+    sigma = orc.select_sigma(a.nnz / a.m)
+    a5 = gpu_build(g, a, sigma)
+    xs = [rng.random_x(a.n) for _ in range(5)]
+    ys_dev = [gpu_y(g, a5, x) for x in xs]
+    for x, yd in zip(xs, ys_dev):
+        assert_y_close(yd, orc.spmv(a, x, 32, sigma), a, x, "device path")
+        assert np.array_equal(g.spmv_host(a5, x), yd)  # deterministic mode: bit-stable
+    for pinned in (True, False):
+        for count in (1, 2, 5):
+            hx = [torch.as_tensor(x) for x in xs[:count]]
+            hy = [torch.full((a.m,), float("nan"), dtype=torch.float64) for _ in range(count)]
+            if pinned:
+                hx = [t.pin_memory() for t in hx]
+                hy = [t.pin_memory() for t in hy]
+            g.spmv_host_batch(a5, hx, hy)
+            torch.cuda.current_stream().synchronize()
+            for k in range(count):
+                assert np.array_equal(hy[k].numpy(), ys_dev[k]), (pinned, count, k)
+    with pytest.raises(ValueError, match="2 x vectors but 1 y"):
+        g.spmv_host_batch(a5, xs[:2], [np.empty(a.m)])
+    with pytest.raises(ValueError, match="length"):
+        g.spmv_host_batch(a5, [np.empty(a.n + 1)], [np.empty(a.m)])
+    a5.release()
