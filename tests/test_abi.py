@@ -55,3 +55,30 @@ def test_no_cpu_fallback_without_gpu():
     rc = L.csr5g_build(0, 0, 0, 0, None, None, None, C.byref(p), None, C.byref(h))
     assert rc == _lib.ECUDA
     assert "CUDA" in L.csr5g_last_error().decode() or "device" in L.csr5g_last_error().decode()
+
+
+def test_stencil_box_sizes_and_weak_scaling():
+    """csr5g_stencil_box_size (host-only) against the oracle's formula and the
+    host generator; the weak-scaling workload rule of bench.py."""
+    import ctypes as C
+
+    from oracle.oracle import Oracle, stencil, stencil_box_size
+    from paper_1503_05032_b200 import _lib
+    from paper_1503_05032_b200.synthetic import WORKLOADS, scaled_workload
+    L = _lib.lib()
+    orc = Oracle()
+    for kind in (0, 1):
+        for a in (1, 2, 3, 7):
+            for layers in (1, 2, a, 3 * a):
+                m, nnz = C.c_int64(), C.c_int64()
+                assert L.csr5g_stencil_box_size(kind, a, layers, C.byref(m), C.byref(nnz)) == 0
+                assert (m.value, nnz.value) == stencil_box_size(kind, a, layers)
+                if m.value <= 2000:
+                    h = stencil(orc, kind, a, layers)
+                    assert (h.m, h.row_ptr[-1]) == (m.value, nnz.value)
+    w = scaled_workload(WORKLOADS["st27_200"], 8)
+    assert (w["a"], w["layers"]) == (200, 1600)
+    assert scaled_workload(WORKLOADS["rmat24"], 8)["scale"] == 27  # BASELINE config 5
+    assert scaled_workload(WORKLOADS["mixed23"], 4)["log2_m"] == 25
+    with pytest.raises(ValueError, match="power-of-two"):
+        scaled_workload(WORKLOADS["rmat24"], 3)

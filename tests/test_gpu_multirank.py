@@ -1,0 +1,42 @@
+"""The sharded bench flow end to end with several ranks on the one GPU the
+test box has: torchrun, process group over gloo (NCCL refuses two ranks on one
+device), weak and strong scaling.  Each rank runs bench.py's correctness guard
+(its owned rows of y against cuSPARSE, boundary fix-ups included) before any
+timing; the timings of ranks sharing a GPU mean nothing and are not checked.
+No kernel waits on another rank: the exchange is host-mediated."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def _port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,workload,scaling", [(2, "lap5_1000", "weak"),
+                                                (3, "lap5_1000", "strong"),
+                                                (4, "lap5_1000", "weak")])
+def test_bench_sharded_on_one_gpu(n, workload, scaling):
+    env = dict(os.environ, CSR5G_DIST_BACKEND="gloo", CSR5G_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py",
+           "--gpus", str(n), "--steps", "3", "--warmup", "3", "--workload", workload,
+           "--scaling", scaling]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 prints one line
+    d = lines[0]
+    assert d["n_gpus"] == n and d["scaling"] == scaling
+    assert d["correctness_max_rel_err"] <= 1e-12
+    m1 = 1000 * 1000
+    assert d["config"]["m"] == (m1 * n if scaling == "weak" else m1)
