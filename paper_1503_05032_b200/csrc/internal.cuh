@@ -64,6 +64,8 @@ struct SpmvArgs {
   int32_t jitter;          // hashed tile-range boundaries
   int32_t stream_only;     // profiling: run the TMA ring without gathers/math
   int32_t early_gather;    // random gathers: issue tile k+1's gathers before tile k's depth loop
+  float x_frac;            // share of x lines given evict_last (the rest evict_first)
+  int32_t y_hint;          // y stores: 1 = L2 evict_first, no L1 allocation
 };
 
 struct Pipeline;  // pipeline.cu: host-vector copy/compute pipeline
@@ -133,6 +135,18 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
+}
+// evict_last for a fraction of the lines (chosen by address), evict_first for
+// the rest: a working set larger than L2 keeps a resident part instead of
+// thrashing all of it
+__device__ __forceinline__ uint64_t policy_evict_last_frac(float f) {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(p) : "f"(f));
+  return p;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
+               : "memory");
 }
 // Streaming read-once loads: no L1 allocation, evict-first in L2.
 __device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {

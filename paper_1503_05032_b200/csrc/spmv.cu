@@ -134,7 +134,9 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
 
 // Warps per CTA: short tiles need fewer registers and less shared memory per
 // warp, and random gathers want as many warps in flight as fit.
-__host__ __device__ constexpr int spmv_threads(int sigma) { return sigma <= 32 ? 384 : 256; }
+__host__ __device__ constexpr int spmv_threads(int sigma) {
+  return sigma <= 5 ? 768 : sigma <= 13 ? 512 : sigma <= 32 ? 384 : 256;
+}
 // closed-segment slots per warp in shared memory (tiles rarely have more heads)
 constexpr int kClosedSlots = 128;
 constexpr int kEoSlots = 128;  // >= kClosedSlots - 1 heads of a shared-slot tile
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
                         (size_t)wib * S * a.stage_bytes;
   double* __restrict__ spill = a.spill + (size_t)w * (B + 1);  // slots 0..B
   const uint64_t pol_s = policy_evict_first();
-  const uint64_t pol_x = policy_evict_last();
+  const uint64_t pol_x = a.x_frac >= 1.0f ? policy_evict_last() : policy_evict_last_frac(a.x_frac);
   const W* __restrict__ desc = static_cast<const W*>(a.desc);
 
   int64_t kb = 0, ke = 0;
@@ -201,6 +203,13 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   if (!has_tiles) return;
 
   double* __restrict__ y = a.y;
+  const bool yh = a.y_hint != 0;
+  auto put_y = [&](int64_t r, double v) {
+    if (yh)
+      st_hint(y + r, v, pol_s);
+    else
+      y[r] = v;
+  };
   int64_t pend_row = -1;
   double pend_val = 0.0;
   bool pend_first = true;
@@ -396,16 +405,16 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
         if (h >= H) break;
         const int64_t r = tile_row + (flagged ? (int64_t)eo_at(h) : (int64_t)h);
         if (h == H - 1) rL = r;
-        if (h != 0 && h != H - 1) y[r] = slot_at(h + 1);
+        if (h != 0 && h != H - 1) put_y(r, slot_at(h + 1));
         if (flagged || h == H - 1) {  // empty rows up to the next head (or next tile)
           const int64_t nr = h + 1 < H ? tile_row + (int64_t)eo_at(h + 1) : next_row;
           if (nr - r - 1 <= 8) {
-            for (int64_t q = r + 1; q < nr; ++q) y[q] = 0.0;
+            for (int64_t q = r + 1; q < nr; ++q) put_y(q, 0.0);
           } else if (defer_hi == defer_lo) {
             defer_lo = r + 1;
             defer_hi = nr;
           } else {
-            for (int64_t q = r + 1; q < nr; ++q) y[q] = 0.0;
+            for (int64_t q = r + 1; q < nr; ++q) put_y(q, 0.0);
           }
         }
       }
@@ -421,7 +430,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       dm &= dm - 1;
       const int64_t lo = __shfl_sync(kFull, defer_lo, src);
       const int64_t hi = __shfl_sync(kFull, defer_hi, src);
-      for (int64_t q = lo + lane; q < hi; q += 32) y[q] = 0.0;
+      for (int64_t q = lo + lane; q < hi; q += 32) put_y(q, 0.0);
     }
     __syncwarp();  // closed[] is rewritten by the next tile
 
@@ -431,7 +440,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
         if (pend_first)
           put_item(a, 2 * (int64_t)w, pend_row, pend_val);
         else
-          y[pend_row] = pend_val;
+          put_y(pend_row, pend_val);
       }
     };
     if (k == kb) {
@@ -594,8 +603,10 @@ int spmv_plan(Handle* h, int sms) {
   // worth more as L1 for outstanding gather misses (measured: R-MAT s24 at
   // 150 KB, 7 warps: 2 stages 1.67 ms, 3 stages 2.11 ms)
   int nw = spmv_threads(sigma) / 32, stages = random ? 2 : 4;
+  // one mbarrier per warp and stage at the start, 128-byte aligned
+  auto bars = [](int w, int st) { return (w * st * 8 + 127) / 128 * 128; };
   auto need = [&](int w, int st) {
-    return 512 + w * (closed_bytes + kEoSlots * 4 + st * stage_bytes);
+    return bars(w, st) + w * (closed_bytes + kEoSlots * 4 + st * stage_bytes);
   };
   // local gathers: warps per SM matter most (keep them, give up depth first);
   // random gathers: keep the TMA lead (depth), give up warps
@@ -611,7 +622,7 @@ int spmv_plan(Handle* h, int sms) {
   h->warps_per_block = nw;
   h->stages = stages;
   h->stage_bytes = stage_bytes;
-  h->bar_bytes = 512;  // nw * stages * 8 <= 16 * 4 * 8
+  h->bar_bytes = bars(nw, stages);
   h->smem_bytes = need(nw, stages);
   CSR5G_CUDA(cudaFuncSetAttribute(spmv_fn((int)h->info.sigma),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
@@ -697,6 +708,16 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   const bool x_window = x_window_env >= 0 ? x_window_env != 0 : h->x_window;
   a.x_mode = x_mode;
   a.early_gather = h->lines_per_gather >= 8.0 ? 1 : 0;
+  static const float x_frac_env = [] {
+    const char* e = std::getenv("CSR5G_XFRAC");
+    return e ? (float)std::atof(e) : -1.0f;
+  }();
+  static const int y_hint_env = [] {
+    const char* e = std::getenv("CSR5G_YHINT");
+    return e ? std::atoi(e) : -1;
+  }();
+  a.x_frac = x_frac_env > 0.0f ? std::min(1.0f, x_frac_env) : 1.0f;
+  a.y_hint = y_hint_env >= 0 ? y_hint_env : 0;
   if (const char* e = std::getenv("CSR5G_EARLY")) a.early_gather = std::atoi(e) != 0;
   static const int jitter = [] {
     const char* e = std::getenv("CSR5G_JITTER");
