@@ -164,6 +164,19 @@ CSR5G_API int csr5g_spmv_host_batch(csr5g_matrix h, const double *const *h_xs,
                                     void *stream);
 CSR5G_API int csr5g_to_csr_host(csr5g_matrix h, int64_t *h_col_idx, double *h_val);
 
+/* The plain-CSR kernels the reference times CSR5 against (spmv.cpp:139-209),
+ * on the device: CSR5G_CSR_SCALAR = spmv_csr_scalar (one thread per row, row
+ * order -- also the summation order of dense_spmv_oracle, csr.cpp:85-98),
+ * CSR5G_CSR_SEGSUM = spmv_csr_segsum (products, then a segmented sum per row).
+ * They feed run_benchmark's iteration scenario (bench.cpp:86-90, t_csr).  The
+ * caller's device CSR (int64 row_ptr, int32 col_idx); y fully overwritten;
+ * stream-ordered. */
+#define CSR5G_CSR_SCALAR 0
+#define CSR5G_CSR_SEGSUM 1
+CSR5G_API int csr5g_csr_spmv(int device, int32_t kernel, int64_t m, int64_t n, int64_t nnz,
+                             const int64_t *d_row_ptr, const int32_t *d_col_idx,
+                             const double *d_val, const double *d_x, double *d_y, void *stream);
+
 /* Implicit destruction of Csr5Matrix (value type) -> explicit release. */
 CSR5G_API int csr5g_release(csr5g_matrix h);
 

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <exception>
 #include <new>
+#include <sstream>
 #include <span>
 #include <string>
 #include <vector>
@@ -244,5 +245,60 @@ void ref_csr_get(void* av, int64_t* row_ptr, int64_t* col_idx, double* val) {
   std::memcpy(val, a->val.data(), a->val.size() * sizeof(double));
 }
 void ref_csr_free(void* a) { delete static_cast<csr5::CsrMatrix*>(a); }
+
+// bench.cpp:55-72 parse_kernel_list: kinds (0 csr-scalar, 1 csr-segsum,
+// 2 csr5) into out[cap]; returns the count, or -(status) on an exception.
+int ref_parse_kernels(const char* text, int* out, int cap) {
+  try {
+    const auto v = csr5::parse_kernel_list(text);
+    int k = 0;
+    for (auto kind : v)
+      if (k < cap) out[k++] = static_cast<int>(kind);
+    return static_cast<int>(v.size());
+  } catch (const std::exception& e) {
+    return -fail(e);
+  }
+}
+
+// bench.cpp:86-90 iteration_speedup.
+int ref_iteration_speedup(double t_csr, double t_pre, double t_new, int64_t n, double* out) {
+  try {
+    *out = csr5::iteration_speedup(t_csr, t_pre, t_new, n);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// bench.cpp:177-186 emit_csv over a report assembled from plain arrays
+// (kernel names separated by '\n'); the CSV text goes to out[cap].
+int64_t ref_emit_csv(const char* matrix, int64_t m, int64_t n, int64_t nnz, int threads,
+                     int nk, const char* kernel_names, const double* best, const double* avg,
+                     const double* gflops, const double* conv, const double* s50,
+                     const double* s500, char* out, int64_t cap) {
+  csr5::BenchReport r;
+  r.matrix = matrix;
+  r.m = m;
+  r.n = n;
+  r.nnz = nnz;
+  r.threads = threads;
+  std::stringstream names(kernel_names);
+  for (int i = 0; i < nk; ++i) {
+    csr5::KernelResult k;
+    std::getline(names, k.kernel, '\n');
+    k.best_ms = best[i];
+    k.avg_ms = avg[i];
+    k.gflops = gflops[i];
+    k.conv_ms = conv[i];
+    k.speedup_n50 = s50[i];
+    k.speedup_n500 = s500[i];
+    r.kernels.push_back(k);
+  }
+  std::ostringstream os;
+  csr5::emit_csv(r, os);
+  const std::string t = os.str();
+  if ((int64_t)t.size() + 1 <= cap) std::memcpy(out, t.c_str(), t.size() + 1);
+  return (int64_t)t.size();
+}
 
 }  // extern "C"

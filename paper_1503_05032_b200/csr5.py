@@ -244,6 +244,29 @@ def spmv_host_batch(a5: Csr5Matrix, xs, ys, mode="deterministic", stream=None) -
                                           _stream_ptr(stream)))
 
 
+_CSR_KERNELS = {"csr-scalar": 0, "csr-segsum": 1}
+
+
+def spmv_csr(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor | None = None,
+             kernel: str = "csr-scalar", stream=None) -> torch.Tensor:
+    """spmv.cpp:139-209 spmv_csr_scalar / spmv_csr_segsum on the device
+    (csr5g_csr_spmv): the plain-CSR baselines of run_benchmark."""
+    if kernel not in _CSR_KERNELS:
+        raise ValueError(f"unknown kernel '{kernel}' (expected csr-scalar or csr-segsum)")
+    if x.dim() != 1 or x.numel() != a.n:
+        raise ValueError(f"spmv: x has length {x.numel()}, expected {a.n}")
+    if y is None:
+        y = torch.empty(a.m, dtype=torch.float64, device=x.device)
+    elif y.numel() != a.m:
+        raise ValueError(f"spmv: y has length {y.numel()}, expected {a.m}")
+    dev = a.row_ptr.device.index or 0
+    with torch.cuda.device(dev):
+        check(lib().csr5g_csr_spmv(dev, _CSR_KERNELS[kernel], a.m, a.n, a.nnz,
+                                   a.row_ptr.data_ptr(), a.col_idx.data_ptr(), a.val.data_ptr(),
+                                   x.data_ptr(), y.data_ptr(), _stream_ptr(stream)))
+    return y
+
+
 def csr5_to_csr(a5: Csr5Matrix, row_ptr: torch.Tensor, stream=None) -> CsrMatrix:
     """format.cpp:254-265: undo the tile transposition (row_ptr is unchanged by
     the format, so the caller's copy is reused)."""
@@ -388,5 +411,5 @@ def spmv_csr5_evt(a5: Csr5Matrix, x: torch.Tensor, y: torch.Tensor, ev0: Event, 
 
 
 __all__ = ["TuningParams", "CsrMatrix", "Csr5Matrix", "csr_to_csr5", "csr_to_csr5_shard",
-           "spmv_csr5", "spmv_host", "spmv_host_batch", "csr5_to_csr", "dump_format", "select_sigma", "layout",
+           "spmv_csr5", "spmv_csr", "spmv_host", "spmv_host_batch", "csr5_to_csr", "dump_format", "select_sigma", "layout",
            "stencil", "stencil_box", "stencil_box_size", "Event", "spmv_csr5_evt", "Partial"]

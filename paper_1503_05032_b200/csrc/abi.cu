@@ -267,6 +267,21 @@ int csr5g_spmv_host_batch(csr5g_matrix h, const double* const* h_xs, double* con
   return spmv_host_batch(h->h, h_xs, h_ys, count, mode, static_cast<cudaStream_t>(stream));
 }
 
+int csr5g_csr_spmv(int device, int32_t kernel, int64_t m, int64_t n, int64_t nnz,
+                   const int64_t* d_row_ptr, const int32_t* d_col_idx, const double* d_val,
+                   const double* d_x, double* d_y, void* stream) {
+  if (kernel != CSR5G_CSR_SCALAR && kernel != CSR5G_CSR_SEGSUM)
+    return fail(CSR5G_EINVAL, "csr5g: unknown CSR kernel " + std::to_string(kernel));
+  if (m < 0 || n < 0 || nnz < 0) return fail(CSR5G_EINVAL, "csr: negative dimension");
+  if (m > 0 && (!d_row_ptr || !d_y)) return fail(CSR5G_EINVAL, "spmv: row_ptr or y is NULL");
+  if (nnz > 0 && (!d_col_idx || !d_val || !d_x))
+    return fail(CSR5G_EINVAL, "spmv: col_idx, val or x is NULL");
+  if (m >= (int64_t(1) << 31))
+    return fail(CSR5G_ERANGE, "csr5g: m >= 2^31 rows is unsupported");
+  return csr_spmv(device, kernel, m, n, nnz, d_row_ptr, d_col_idx, d_val, d_x, d_y,
+                  static_cast<cudaStream_t>(stream));
+}
+
 int csr5g_to_csr_host(csr5g_matrix h, int64_t* h_col_idx, double* h_val) {
   if (!h) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
   const int64_t nz = h->h->info.nnz_held;

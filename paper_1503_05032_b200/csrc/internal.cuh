@@ -124,6 +124,9 @@ int spmv_plan(Handle* h, int sms);
 int spmv_host_batch(Handle* h, const double* const* xs, double* const* ys, int64_t count,
                     int mode, cudaStream_t stream);
 void free_pipeline(Pipeline* p);
+int csr_spmv(int device, int kernel, int64_t m, int64_t n, int64_t nnz, const int64_t* rp,
+             const int32_t* col, const double* val, const double* x, double* y,
+             cudaStream_t stream);
 
 // ---- device helpers ----------------------------------------------------------
 __device__ __forceinline__ uint64_t policy_evict_first() {
