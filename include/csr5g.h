@@ -177,6 +177,30 @@ CSR5G_API int csr5g_csr_spmv(int device, int32_t kernel, int64_t m, int64_t n, i
                              const int64_t *d_row_ptr, const int32_t *d_col_idx,
                              const double *d_val, const double *d_x, double *d_y, void *stream);
 
+/* Matrix files (SURVEY 8f "ingest").  matrix_market.cpp:38-96
+ * read_matrix_market: parses an ASCII coordinate file (real / integer /
+ * pattern, general / symmetric) into a host COO object -- 0-based indices,
+ * pattern values 1.0, symmetric entries mirrored (diagonal once) -- with the
+ * reference's std::runtime_error texts (CSR5G_ERUNTIME).  csr5g_coo_get copies
+ * its `count` entries out (any pointer may be NULL). */
+typedef struct csr5g_coo_s *csr5g_coo;
+CSR5G_API int csr5g_mm_read(const char *path, csr5g_coo *out, int64_t *m, int64_t *n,
+                            int64_t *count);
+CSR5G_API int csr5g_coo_get(csr5g_coo c, int64_t *h_rows, int64_t *h_cols, double *h_vals);
+CSR5G_API int csr5g_coo_release(csr5g_coo c);
+
+/* csr.cpp:35-72 coo_to_csr on the device: device COO (int64 rows / cols, f64
+ * values, `count` entries, any order, duplicates allowed) -> canonical CSR:
+ * sorted by (row, col), duplicates summed in input order (bit-identical to the
+ * reference's sums).  Outputs: d_row_ptr[m+1], d_col_idx / d_val with room
+ * for `count` entries; *nnz = the unique entries written.  An out-of-range
+ * entry fails with the reference's std::invalid_argument text (first such
+ * entry).  Synchronises `stream`. */
+CSR5G_API int csr5g_coo_to_csr(int device, int64_t m, int64_t n, int64_t count,
+                               const int64_t *d_rows, const int64_t *d_cols, const double *d_vals,
+                               int64_t *d_row_ptr, int32_t *d_col_idx, double *d_val,
+                               int64_t *nnz, void *stream);
+
 /* Implicit destruction of Csr5Matrix (value type) -> explicit release. */
 CSR5G_API int csr5g_release(csr5g_matrix h);
 

@@ -19,6 +19,7 @@
 #include "csr5/bench.hpp"
 #include "csr5/csr.hpp"
 #include "csr5/format.hpp"
+#include "csr5/matrix_market.hpp"
 #include "csr5/spmv.hpp"
 #include "csr5/synthetic.hpp"
 #include "csr5/tuning.hpp"
@@ -299,6 +300,44 @@ int64_t ref_emit_csv(const char* matrix, int64_t m, int64_t n, int64_t nnz, int 
   const std::string t = os.str();
   if ((int64_t)t.size() + 1 <= cap) std::memcpy(out, t.c_str(), t.size() + 1);
   return (int64_t)t.size();
+}
+
+// matrix_market.cpp:38-96 read_matrix_market: entries into a handle.
+int ref_mm_read(const char* path, int64_t* m, int64_t* n, int64_t* count, void** out) {
+  try {
+    auto* d = new csr5::MatrixMarketData(csr5::read_matrix_market(std::string(path)));
+    *m = d->m;
+    *n = d->n;
+    *count = (int64_t)d->entries.size();
+    *out = d;
+    return 0;
+  } catch (const std::exception& e) {
+    *out = nullptr;
+    return fail(e);
+  }
+}
+void ref_mm_get(void* h, int64_t* rows, int64_t* cols, double* vals) {
+  const auto* d = static_cast<csr5::MatrixMarketData*>(h);
+  for (size_t k = 0; k < d->entries.size(); ++k) {
+    rows[k] = d->entries[k].row;
+    cols[k] = d->entries[k].col;
+    vals[k] = d->entries[k].value;
+  }
+}
+void ref_mm_free(void* h) { delete static_cast<csr5::MatrixMarketData*>(h); }
+
+// csr.cpp:35-72 coo_to_csr -> a CsrMatrix handle (ref_csr_nnz / ref_csr_get).
+int ref_coo_to_csr(int64_t m, int64_t n, int64_t count, const int64_t* rows, const int64_t* cols,
+                   const double* vals, void** out) {
+  try {
+    std::vector<csr5::CooEntry> e((size_t)count);
+    for (int64_t k = 0; k < count; ++k) e[(size_t)k] = {rows[k], cols[k], vals[k]};
+    *out = new csr5::CsrMatrix(csr5::coo_to_csr(std::move(e), m, n));
+    return 0;
+  } catch (const std::exception& ex) {
+    *out = nullptr;
+    return fail(ex);
+  }
 }
 
 }  // extern "C"

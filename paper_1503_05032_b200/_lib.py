@@ -77,6 +77,12 @@ SIGNATURES = {
     "csr5g_spmv_host": (C.c_int, [_vp, _vp, _vp, _i32]),
     "csr5g_spmv_host_batch": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
     "csr5g_to_csr_host": (C.c_int, [_vp, _vp, _vp]),
+    "csr5g_mm_read": (C.c_int, [C.c_char_p, C.POINTER(_vp), C.POINTER(_i64), C.POINTER(_i64),
+                                C.POINTER(_i64)]),
+    "csr5g_coo_get": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "csr5g_coo_release": (C.c_int, [_vp]),
+    "csr5g_coo_to_csr": (C.c_int, [C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                   C.POINTER(_i64), _vp]),
     "csr5g_csr_spmv": (C.c_int, [C.c_int, _i32, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "csr5g_event_create": (C.c_int, [C.POINTER(_vp)]),
     "csr5g_event_record": (C.c_int, [_vp, _vp]),

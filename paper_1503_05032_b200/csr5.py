@@ -21,6 +21,7 @@ libcsr5g.so.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -267,6 +268,52 @@ def spmv_csr(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor | None = None,
     return y
 
 
+def read_matrix_market(path: str):
+    """matrix_market.cpp:38-96 (csr5g_mm_read): (m, n, rows, cols, vals) as
+    host numpy arrays, 0-based, symmetric files expanded.  Parse errors raise
+    RuntimeError with the reference's text."""
+    h, m, n, cnt = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int64()
+    check(lib().csr5g_mm_read(os.fsencode(path), C.byref(h), C.byref(m), C.byref(n),
+                              C.byref(cnt)))
+    try:
+        rows = np.empty(cnt.value, np.int64)
+        cols = np.empty(cnt.value, np.int64)
+        vals = np.empty(cnt.value, np.float64)
+        check(lib().csr5g_coo_get(h, rows.ctypes.data, cols.ctypes.data, vals.ctypes.data))
+    finally:
+        lib().csr5g_coo_release(h)
+    return m.value, n.value, rows, cols, vals
+
+
+def coo_to_csr(rows, cols, vals, m: int, n: int, device="cuda", stream=None) -> CsrMatrix:
+    """csr.cpp:35-72 on the device (csr5g_coo_to_csr): sort by (row, col), sum
+    duplicates in input order.  Out-of-range entries raise ValueError with the
+    reference's std::invalid_argument text."""
+    r = torch.as_tensor(rows, dtype=torch.int64).to(device).contiguous()
+    c = torch.as_tensor(cols, dtype=torch.int64).to(device).contiguous()
+    v = torch.as_tensor(vals, dtype=torch.float64).to(device).contiguous()
+    k = r.numel()
+    if c.numel() != k or v.numel() != k:
+        raise ValueError("coo_to_csr: rows, cols and vals differ in length")
+    rp = torch.empty(m + 1, dtype=torch.int64, device=device)
+    ci = torch.empty(max(k, 1), dtype=torch.int32, device=device)
+    va = torch.empty(max(k, 1), dtype=torch.float64, device=device)
+    nnz = C.c_int64()
+    dev = rp.device.index or 0
+    with torch.cuda.device(dev):
+        check(lib().csr5g_coo_to_csr(dev, m, n, k, r.data_ptr(), c.data_ptr(), v.data_ptr(),
+                                     rp.data_ptr(), ci.data_ptr(), va.data_ptr(), C.byref(nnz),
+                                     _stream_ptr(stream)))
+    return CsrMatrix(m, n, rp, ci[:nnz.value].clone(), va[:nnz.value].clone())
+
+
+def load_matrix_market(path: str, device="cuda") -> CsrMatrix:
+    """matrix_market.cpp:98-101 load_matrix_market: read, then coo_to_csr on
+    the device."""
+    m, n, rows, cols, vals = read_matrix_market(path)
+    return coo_to_csr(rows, cols, vals, m, n, device=device)
+
+
 def csr5_to_csr(a5: Csr5Matrix, row_ptr: torch.Tensor, stream=None) -> CsrMatrix:
     """format.cpp:254-265: undo the tile transposition (row_ptr is unchanged by
     the format, so the caller's copy is reused)."""
@@ -411,5 +458,5 @@ def spmv_csr5_evt(a5: Csr5Matrix, x: torch.Tensor, y: torch.Tensor, ev0: Event, 
 
 
 __all__ = ["TuningParams", "CsrMatrix", "Csr5Matrix", "csr_to_csr5", "csr_to_csr5_shard",
-           "spmv_csr5", "spmv_csr", "spmv_host", "spmv_host_batch", "csr5_to_csr", "dump_format", "select_sigma", "layout",
+           "spmv_csr5", "spmv_csr", "read_matrix_market", "coo_to_csr", "load_matrix_market", "spmv_host", "spmv_host_batch", "csr5_to_csr", "dump_format", "select_sigma", "layout",
            "stencil", "stencil_box", "stencil_box_size", "Event", "spmv_csr5_evt", "Partial"]
