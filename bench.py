@@ -479,6 +479,30 @@ def run_ours(args, workload_name, workload):
                          "speedup_n50": iteration_speedup(t_csr["csr-scalar"], conv_ms, ms, 50),
                          "speedup_n500": iteration_speedup(t_csr["csr-scalar"], conv_ms, ms, 500),
                          "baseline": "GPU csr-scalar (one thread per row), spmv.cpp:139-154"}
+        # ingest: device COO -> CSR (csr.cpp:35-72) of this matrix's entries in
+        # a random order (sort + duplicate merge + row_ptr)
+        try:
+            g = torch.Generator(device=dev).manual_seed(1)
+            perm = torch.randperm(nnz, device=dev, generator=g)
+            rows = torch.repeat_interleave(torch.arange(m, device=dev),
+                                           a.row_ptr[1:] - a.row_ptr[:-1])[perm]
+            cols = a.col_idx.long()[perm]
+            vals = a.val[perm]
+            del perm
+            csr5.coo_to_csr(rows, cols, vals, m, n, device=dev)  # warm the pool
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            c2 = csr5.coo_to_csr(rows, cols, vals, m, n, device=dev)
+            torch.cuda.synchronize()
+            ingest_ms = (time.perf_counter() - t0) * 1e3
+            same = bool(torch.equal(c2.row_ptr, a.row_ptr) and torch.equal(c2.col_idx, a.col_idx)
+                        and torch.equal(c2.val, a.val))
+            iteration["ingest"] = {"coo_to_csr_ms": ingest_ms, "entries": nnz,
+                                   "order": "random permutation", "equals_generator_csr": same}
+            del rows, cols, vals, c2
+        except (MemoryError, RuntimeError, TypeError) as e:
+            if iteration is not None:
+                iteration["ingest"] = {"error": str(e)[:200]}
         run()  # leave y = the CSR5 result for the CPU comparison below
         torch.cuda.synchronize()
 

@@ -201,6 +201,14 @@ CSR5G_API int csr5g_coo_to_csr(int device, int64_t m, int64_t n, int64_t count,
                                int64_t *d_row_ptr, int32_t *d_col_idx, double *d_val,
                                int64_t *nnz, void *stream);
 
+/* Host-staged form of csr5g_coo_to_csr (the reference's host coo_to_csr
+ * signature, csr.hpp): host COO in, host CSR out with int64 col_idx; the
+ * output buffers hold m+1 / count entries. */
+CSR5G_API int csr5g_coo_to_csr_host(int device, int64_t m, int64_t n, int64_t count,
+                                    const int64_t *h_rows, const int64_t *h_cols,
+                                    const double *h_vals, int64_t *h_row_ptr,
+                                    int64_t *h_col_idx, double *h_val, int64_t *nnz);
+
 /* Implicit destruction of Csr5Matrix (value type) -> explicit release. */
 CSR5G_API int csr5g_release(csr5g_matrix h);
 
@@ -209,6 +217,8 @@ CSR5G_API int csr5g_event_create(void **ev);
 CSR5G_API int csr5g_event_record(void *ev, void *stream);
 CSR5G_API int csr5g_event_elapsed_ms(void *ev_begin, void *ev_end, float *ms);
 CSR5G_API int csr5g_event_destroy(void *ev);
+/* cudaStreamSynchronize for callers without a CUDA runtime (NULL = legacy). */
+CSR5G_API int csr5g_stream_synchronize(void *stream);
 
 /* Synthetic inputs on the device (bench / tests): counter-based, so the
  * same call gives the same matrix on any GPU.  kind: 0 = 2D 5-point Laplacian

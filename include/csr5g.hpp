@@ -13,6 +13,10 @@
 // csr5_to_csr             format.hpp:186      csr5_to_csr
 // dump_format             format.hpp:190      dump_format
 // select_sigma            tuning.hpp:29       select_sigma
+// CooEntry, coo_to_csr    csr.hpp             CooEntry, coo_to_csr (sorted + summed on the GPU)
+// read_matrix_market,     matrix_market.hpp   read_matrix_market, load_matrix_market
+//   load_matrix_market
+// (host-vector batch)                         spmv_csr5_batch (pipelined H2D/SpMV/D2H)
 //
 // Errors are rethrown as the reference's exception types with the library's
 // message: CSR5G_EINVAL -> std::invalid_argument, CSR5G_ERANGE ->
@@ -229,6 +233,81 @@ inline void dump_format(const Csr5Matrix& a5, std::ostream& out) {
     }
     out << '\n';
   }
+}
+
+// y_k = A x_k for a batch of host vectors (csr5g_spmv_host_batch): x_{k+1}
+// H2D and y_k D2H overlap SpMV k; synchronises before returning.  Pinned
+// (cudaHostAlloc'd) vectors overlap fully; pageable ones still work.
+inline void spmv_csr5_batch(const Csr5Matrix& a5, const std::vector<const double*>& xs,
+                            const std::vector<double*>& ys,
+                            SpmvMode mode = SpmvMode::deterministic) {
+  if (xs.size() != ys.size())
+    throw std::invalid_argument("spmv: " + std::to_string(xs.size()) + " x vectors but " +
+                                std::to_string(ys.size()) + " y vectors");
+  check(csr5g_spmv_host_batch(a5.handle(), xs.data(), ys.data(), (int64_t)xs.size(),
+                              static_cast<int32_t>(mode), nullptr));
+  check(csr5g_stream_synchronize(nullptr));
+}
+
+struct CooEntry {
+  index_t row;
+  index_t col;
+  double value;
+};
+
+struct MatrixMarketData {
+  std::vector<CooEntry> entries;
+  index_t m = 0;
+  index_t n = 0;
+};
+
+// csr.cpp:35-72: sorted by (row, col), duplicates summed in input order (on
+// `device`); out-of-range entries throw std::invalid_argument.
+inline CsrMatrix coo_to_csr(const std::vector<CooEntry>& entries, index_t m, index_t n,
+                            int device = 0) {
+  std::vector<index_t> r(entries.size()), c(entries.size());
+  std::vector<double> v(entries.size());
+  for (std::size_t k = 0; k < entries.size(); ++k) {
+    r[k] = entries[k].row;
+    c[k] = entries[k].col;
+    v[k] = entries[k].value;
+  }
+  CsrMatrix a;
+  a.m = m;
+  a.n = n;
+  a.row_ptr.resize(static_cast<std::size_t>(m < 0 ? 0 : m) + 1);
+  a.col_idx.resize(entries.size());
+  a.val.resize(entries.size());
+  index_t nnz = 0;
+  check(csr5g_coo_to_csr_host(device, m, n, (int64_t)entries.size(), r.data(), c.data(),
+                              v.data(), a.row_ptr.data(), a.col_idx.data(), a.val.data(), &nnz));
+  a.col_idx.resize((std::size_t)nnz);
+  a.val.resize((std::size_t)nnz);
+  return a;
+}
+
+// matrix_market.cpp:38-96; parse errors throw std::runtime_error with the
+// reference's text.
+inline MatrixMarketData read_matrix_market(const std::string& path) {
+  csr5g_coo h = nullptr;
+  int64_t m = 0, n = 0, k = 0;
+  check(csr5g_mm_read(path.c_str(), &h, &m, &n, &k));
+  std::vector<index_t> r((std::size_t)k), c((std::size_t)k);
+  std::vector<double> v((std::size_t)k);
+  const int rc = csr5g_coo_get(h, r.data(), c.data(), v.data());
+  csr5g_coo_release(h);
+  check(rc);
+  MatrixMarketData d;
+  d.m = m;
+  d.n = n;
+  d.entries.resize((std::size_t)k);
+  for (std::size_t q = 0; q < (std::size_t)k; ++q) d.entries[q] = {r[q], c[q], v[q]};
+  return d;
+}
+
+inline CsrMatrix load_matrix_market(const std::string& path, int device = 0) {
+  const MatrixMarketData d = read_matrix_market(path);
+  return coo_to_csr(d.entries, d.m, d.n, device);
 }
 
 }  // namespace csr5g

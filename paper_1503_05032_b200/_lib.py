@@ -83,11 +83,14 @@ SIGNATURES = {
     "csr5g_coo_release": (C.c_int, [_vp]),
     "csr5g_coo_to_csr": (C.c_int, [C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                    C.POINTER(_i64), _vp]),
+    "csr5g_coo_to_csr_host": (C.c_int, [C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                        C.POINTER(_i64)]),
     "csr5g_csr_spmv": (C.c_int, [C.c_int, _i32, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "csr5g_event_create": (C.c_int, [C.POINTER(_vp)]),
     "csr5g_event_record": (C.c_int, [_vp, _vp]),
     "csr5g_event_elapsed_ms": (C.c_int, [_vp, _vp, C.POINTER(C.c_float)]),
     "csr5g_event_destroy": (C.c_int, [_vp]),
+    "csr5g_stream_synchronize": (C.c_int, [_vp]),
     "csr5g_stencil_size": (C.c_int, [_i32, _i64, C.POINTER(_i64), C.POINTER(_i64)]),
     "csr5g_stencil_fill": (C.c_int, [_i32, _i64, _vp, _vp, _vp, _vp]),
     "csr5g_stencil_box_size": (C.c_int, [_i32, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64)]),

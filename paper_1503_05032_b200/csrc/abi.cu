@@ -340,4 +340,9 @@ int csr5g_event_destroy(void* ev) {
   return CSR5G_OK;
 }
 
+int csr5g_stream_synchronize(void* stream) {
+  CSR5G_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return CSR5G_OK;
+}
+
 }  // extern "C"

@@ -304,4 +304,41 @@ int csr5g_coo_to_csr(int device, int64_t m, int64_t n, int64_t count, const int6
   return rc;
 }
 
+int csr5g_coo_to_csr_host(int device, int64_t m, int64_t n, int64_t count, const int64_t* h_rows,
+                          const int64_t* h_cols, const double* h_vals, int64_t* h_row_ptr,
+                          int64_t* h_col_idx, double* h_val, int64_t* nnz) {
+  if (!nnz || !h_row_ptr || (count > 0 && (!h_rows || !h_cols || !h_vals || !h_col_idx || !h_val)))
+    return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  *nnz = 0;
+  if (m < 0 || n < 0 || count < 0) return fail(CSR5G_EINVAL, "csr: negative dimension");
+  CSR5G_CUDA(cudaSetDevice(device));
+  const size_t k = (size_t)std::max<int64_t>(count, 1);
+  int64_t *dr = nullptr, *dc = nullptr, *drp = nullptr;
+  double *dv = nullptr, *dov = nullptr;
+  int32_t* doc = nullptr;
+  auto done = [&](int rc) {
+    for (void* p : {(void*)dr, (void*)dc, (void*)drp, (void*)dv, (void*)dov, (void*)doc})
+      if (p) cudaFree(p);
+    return rc;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&dr, 8 * k)) || (e = cudaMalloc(&dc, 8 * k)) || (e = cudaMalloc(&dv, 8 * k)) ||
+      (e = cudaMalloc(&drp, 8 * (size_t)(m + 1))) || (e = cudaMalloc(&doc, 4 * k)) ||
+      (e = cudaMalloc(&dov, 8 * k)))
+    return done(cuda_fail(e, "cudaMalloc(coo)"));
+  if (count > 0 && ((e = cudaMemcpy(dr, h_rows, 8 * count, cudaMemcpyHostToDevice)) ||
+                    (e = cudaMemcpy(dc, h_cols, 8 * count, cudaMemcpyHostToDevice)) ||
+                    (e = cudaMemcpy(dv, h_vals, 8 * count, cudaMemcpyHostToDevice))))
+    return done(cuda_fail(e, "cudaMemcpy(coo)"));
+  int rc = csr5g_coo_to_csr(device, m, n, count, dr, dc, dv, drp, doc, dov, nnz, nullptr);
+  if (rc) return done(rc);
+  std::vector<int32_t> cols((size_t)*nnz);
+  if ((e = cudaMemcpy(h_row_ptr, drp, 8 * (size_t)(m + 1), cudaMemcpyDeviceToHost)) ||
+      (*nnz && ((e = cudaMemcpy(cols.data(), doc, 4 * (size_t)*nnz, cudaMemcpyDeviceToHost)) ||
+                (e = cudaMemcpy(h_val, dov, 8 * (size_t)*nnz, cudaMemcpyDeviceToHost)))))
+    return done(cuda_fail(e, "cudaMemcpy(csr)"));
+  for (size_t q = 0; q < cols.size(); ++q) h_col_idx[q] = cols[q];
+  return done(CSR5G_OK);
+}
+
 }  // extern "C"

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <fstream>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -124,6 +125,52 @@ int main() {
       (void)spmv_csr5(a5, DenseVector(29, 1.0));
     } catch (const std::invalid_argument& e) {
       threw = std::string(e.what()) == "spmv: x has length 29, expected 30";
+    }
+    CHECK(threw);
+  }
+  // batch of host vectors through the pipelined entry point
+  {
+    const CsrMatrix a = random_csr(99, 900, 800, 0.02);
+    Csr5Matrix a5 = csr_to_csr5(a);
+    std::vector<DenseVector> xs(5, DenseVector((std::size_t)a.n)), ys(5);
+    std::vector<const double*> px;
+    std::vector<double*> py;
+    for (std::size_t k = 0; k < xs.size(); ++k) {
+      for (std::size_t i = 0; i < xs[k].size(); ++i) xs[k][i] = 0.25 + 0.01 * (double)((i + k) % 89);
+      ys[k].assign((std::size_t)a.m, -1.0);
+      px.push_back(xs[k].data());
+      py.push_back(ys[k].data());
+    }
+    spmv_csr5_batch(a5, px, py);
+    for (std::size_t k = 0; k < xs.size(); ++k) CHECK(ys[k] == spmv_csr5(a5, xs[k]));
+  }
+  // Matrix Market -> coo_to_csr on the device -> CSR5
+  {
+    const char* path = "build/shim_test.mtx";
+    {
+      std::ofstream f(path);
+      f << "%%MatrixMarket matrix coordinate real symmetric\n% c\n4 4 5\n1 1 2.0\n2 1 -1\n"
+           "3 3 4.5\n4 2 1e-3\n2 1 0.5\n";
+    }
+    const CsrMatrix a = load_matrix_market(path);
+    CHECK(a.m == 4 && a.n == 4 && a.nnz() == 6);
+    CHECK((a.row_ptr == std::vector<index_t>{0, 2, 4, 5, 6}));
+    CHECK((a.col_idx == std::vector<index_t>{0, 1, 0, 3, 2, 1}));
+    CHECK((a.val == std::vector<double>{2.0, -0.5, -0.5, 1e-3, 4.5, 1e-3}));
+    const DenseVector x{1.0, 2.0, 3.0, 4.0};
+    CHECK(max_rel(spmv_csr5(csr_to_csr5(a), x), oracle(a, x)) <= 1e-12);
+    bool threw = false;
+    try {
+      (void)coo_to_csr({{0, 0, 1.0}, {2, 5, 1.0}}, 3, 3);
+    } catch (const std::invalid_argument& e) {
+      threw = std::string(e.what()) == "coo entry 1 out of bounds: (2, 5) for a 3x3 matrix";
+    }
+    CHECK(threw);
+    threw = false;
+    try {
+      (void)read_matrix_market("build/does_not_exist.mtx");
+    } catch (const std::runtime_error& e) {
+      threw = std::string(e.what()) == "matrix market: cannot open 'build/does_not_exist.mtx'";
     }
     CHECK(threw);
   }
