@@ -503,6 +503,22 @@ def run_ours(args, workload_name, workload):
         except (MemoryError, RuntimeError, TypeError) as e:
             if iteration is not None:
                 iteration["ingest"] = {"error": str(e)[:200]}
+        # gather ceiling: the same nnz x-gathers alone (torch.index_select over
+        # this matrix's col_idx, a library kernel) -- what the x traffic costs
+        # without the matrix stream and the reduction
+        try:
+            idx = a.col_idx.long()
+            xs = x.index_select(0, idx)
+            b, e = csr5.Event(), csr5.Event()
+            b.record()
+            for _ in range(5):
+                torch.index_select(x, 0, idx, out=xs)
+            e.record()
+            torch.cuda.synchronize()
+            iteration["gather_only_ms"] = b.elapsed_ms(e) / 5
+            del idx, xs
+        except (MemoryError, RuntimeError, TypeError):
+            pass
         run()  # leave y = the CSR5 result for the CPU comparison below
         torch.cuda.synchronize()
 
@@ -516,6 +532,8 @@ def run_ours(args, workload_name, workload):
         if tile_ms:
             achieved = bytes_alg / (tile_ms * 1e-3) / 1e9
             traffic = ncu_traffic(workload_name)
+            if iteration and iteration.get("gather_only_ms"):
+                iteration["gather_only_over_kernel"] = iteration["gather_only_ms"] / tile_ms
             roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic,
                     "kernel": "k_spmv (tile kernel)", "kernel_ms": tile_ms,
