@@ -130,6 +130,82 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
   return ((uint64_t)hi << 32) | lo;
 }
 
+__device__ __forceinline__ void write_run(int64_t row, double v, double* y, int64_t first_row,
+                                          int first_owned, csr5g_partial* send) {
+  if (!first_owned && row == first_row) {
+    send->row = row;
+    send->value = v;
+  } else {
+    y[row] = v;
+  }
+}
+
+// One full warp merges items [base, base + 32): segmented warp reduction over
+// the non-decreasing keys; a run that continues past the window is finished
+// by the warp holding its start, walking forward.  Items written by other
+// CTAs of the same launch are read through L2 (ld.cg).
+__device__ void calibrate_window(const int64_t* __restrict__ item_row,
+                                 const double* __restrict__ item_val, int64_t N, int64_t base,
+                                 double* __restrict__ y, int64_t first_row, int first_owned,
+                                 csr5g_partial* send) {
+  const int lane = threadIdx.x & 31;
+  if (base == 0 && lane == 0) {
+    send->row = -1;
+    send->value = 0.0;
+  }
+  __syncwarp();
+  const int64_t i = base + lane;
+  const bool valid = i < N;
+  const int64_t key = valid ? __ldcg(item_row + i) : (LLONG_MAX - lane);
+  int64_t prev = __shfl_up_sync(kFull, key, 1);
+  if (lane == 0) prev = base > 0 ? __ldcg(item_row + base - 1) : LLONG_MIN;
+  const bool start = valid && key != prev;
+  const uint32_t sm = __ballot_sync(kFull, start);
+  const uint32_t vm = __ballot_sync(kFull, valid);
+  const uint64_t above = (uint64_t)sm >> (lane + 1);
+  const int end = above ? lane + __ffsll((long long)above) - 1 : 31 - __clz(vm);
+  double v = valid ? __ldcg(item_val + i) : 0.0;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double o = __shfl_down_sync(kFull, v, d);
+    if (lane + d <= end) v += o;
+  }
+  const int ls = sm ? 31 - __clz(sm) : -1;
+  bool cont = false;
+  int64_t rk = 0;
+  if (ls >= 0) {
+    rk = __shfl_sync(kFull, key, ls);
+    cont = (base + 32 < N) && __ldcg(item_row + base + 32) == rk;
+  }
+  if (start && !(cont && lane == ls)) write_run(key, v, y, first_row, first_owned, send);
+  if (cont) {
+    double total = __shfl_sync(kFull, v, ls);
+    for (int64_t pos = base + 32;; pos += 32) {
+      const int64_t q = pos + lane;
+      const bool mt = q < N && __ldcg(item_row + q) == rk;
+      const uint32_t mm = __ballot_sync(kFull, mt);
+      double s = mt ? __ldcg(item_val + q) : 0.0;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(kFull, s, d);
+      total += s;
+      if (mm != kFull) break;
+    }
+    if (lane == 0) write_run(rk, total, y, first_row, first_owned, send);
+  }
+}
+
+__global__ void k_calibrate(const int64_t* __restrict__ item_row,
+                            const double* __restrict__ item_val, int64_t N, double* __restrict__ y,
+                            int64_t first_row, int first_owned, csr5g_partial* send) {
+  // launched as a programmatic dependent of k_spmv: its launch overlaps the
+  // SpMV; the items are read only once that grid has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane;
+  if (base >= N) return;
+  calibrate_window(item_row, item_val, N, base, y, first_row, first_owned, send);
+}
+
 }  // namespace
 
 // Warps per CTA: short tiles need fewer registers and less shared memory per
@@ -154,6 +230,9 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   constexpr uint32_t COL_OFF = B * 8, DESC_OFF = B * 12;
   constexpr uint32_t TILE_BYTES = B * 12 + 32 * sizeof(W);
 
+  // the calibration grid may launch now; it waits (griddepcontrol.wait) for
+  // this grid to complete before reading the items
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int NW = blockDim.x >> 5;
@@ -200,340 +279,279 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   __syncwarp();
 
   rows_part(a);
-  if (!has_tiles) return;
-
-  double* __restrict__ y = a.y;
-  const bool yh = a.y_hint != 0;
-  auto put_y = [&](int64_t r, double v) {
-    if (yh)
-      st_hint(y + r, v, pol_s);
-    else
-      y[r] = v;
-  };
-  int64_t pend_row = -1;
-  double pend_val = 0.0;
-  bool pend_first = true;
-  uint32_t tpv = 0, tpv_next = 0;
-  int64_t eov = 0;
-  int s = 0;
-  uint32_t phase = 0;
-  // x gathers run one tile ahead: while tile k is spliced and written back,
-  // the first CH gathers of tile k+1 (whose col_idx already sit in the next
-  // ring stage) are in flight.
-  auto gather = [&](int st_idx, double(&xv)[CH]) {
-    const int32_t* sc = reinterpret_cast<const int32_t*>(ring + (size_t)st_idx * a.stage_bytes + COL_OFF);
-    if (a.x_mode == 1) {
-#pragma unroll
-      for (int u = 0; u < CH; ++u) xv[u] = ld_keep_na(a.x + sc[u * 32 + lane], pol_x);
-    } else if (a.x_mode == 2) {
-#pragma unroll
-      for (int u = 0; u < CH; ++u) xv[u] = ld_x_lsu(a.x + sc[u * 32 + lane], pol_x);
-    } else if (a.x_mode == 3) {
-#pragma unroll
-      for (int u = 0; u < CH; ++u) xv[u] = ld_x_cg(a.x + sc[u * 32 + lane]);
-    } else if (a.x_mode == 4) {
-#pragma unroll
-      for (int u = 0; u < CH; ++u) xv[u] = ld_x_plain(a.x + sc[u * 32 + lane]);
-    } else {
-#pragma unroll
-      for (int u = 0; u < CH; ++u) xv[u] = ld_keep(a.x + sc[u * 32 + lane], pol_x);
-    }
-  };
-  double xa[CH];
-  mbar_wait(bars, 0);
-  gather(0, xa);
-
-  for (int64_t k = kb; k < ke; ++k) {
-    const int slot = (int)((k - kb) & 31);
-    if (slot == 0) {  // per-tile scalars, 32 tiles per batch
-      const int64_t last = a.tile_ptr_len - 1;
-      tpv = a.tile_ptr[k + lane < last ? k + lane : last];
-      tpv_next = a.tile_ptr[k + 32 < last ? k + 32 : last];
-      eov = a.eo_ptr[k + lane < a.pcs ? k + lane : a.pcs];
-    }
-    const uint32_t tp = __shfl_sync(kFull, tpv, slot);
-    const uint32_t tpn_s = __shfl_sync(kFull, tpv, (slot + 1) & 31);
-    const uint32_t tpn = slot == 31 ? tpv_next : tpn_s;
-    const int64_t eo_base = __shfl_sync(kFull, eov, slot);
-    const int64_t tile_row = tp & 0x7fffffffu;
-    const bool flagged = (tp >> 31) != 0;
-    const int64_t next_row = (k + 1 == a.pcs) ? a.next_row_after : (int64_t)(tpn & 0x7fffffffu);
-    const int32_t* __restrict__ eo = a.eo + eo_base;
-
-    // profiling knob 2: compute only -- every tile re-reads the resident
-    // stage 0, no TMA traffic after the prologue (y is garbage)
-    const bool compute_only = a.stream_only == 2;
-    const int sn = compute_only ? 0 : (s + 1 == S ? 0 : s + 1);
-    const uint32_t pn = compute_only ? 0u : (s + 1 == S ? phase ^ 1u : phase);
-    if (a.stream_only == 1) {  // profiling knob 1: the TMA ring alone (y is garbage)
-      mbar_wait(bars + s, phase);
-      __syncwarp();
-      if (lane == 0 && k + S < ke) issue(k + S, s);
-      s = s + 1 == S ? 0 : s + 1;
-      phase = s == 0 ? phase ^ 1u : phase;
-      continue;
-    }
-    // random gathers (long misses): tile k+1's gathers also overlap tile k's
-    // depth loop, at the cost of a second register array and a copy
-    double xn[CH];
-    if (EARLY_OK && a.early_gather && k + 1 < ke) {
-      if (!compute_only) mbar_wait(bars + sn, pn);
-      gather(sn, xn);
-    }
-    const unsigned char* st = ring + (size_t)s * a.stage_bytes;
-    const double* sv = reinterpret_cast<const double*>(st);
-    const int32_t* sc = reinterpret_cast<const int32_t*>(st + COL_OFF);
-    const uint64_t wd = (uint64_t)reinterpret_cast<const W*>(st + DESC_OFF)[lane];
-    const uint64_t fr = __brevll(wd & FMASK) >> (64 - SIG);  // bit j = depth j
-    const int yoff = (int)(wd >> (kSegBits + SIG));
-    const int cnt = __popcll(fr);
-    const int H = __shfl_sync(kFull, yoff + cnt, 31);
-    const bool fast = H < CAPC;
-    // a flagged shared-slot tile's empty_offset entries (H < 128: at most 4
-    // per lane) are in flight during the depth loop
-    int32_t eov4[4] = {0, 0, 0, 0};
-    if (flagged && fast) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (lane + 32 * q < H) eov4[q] = eo[lane + 32 * q];
-    }
-
-    // ---- depth loop (spmv.cpp:61-95): gathers first, then FMAs ----
-    // Every close at a bit flag goes to a slot: lane i's k-th flag ends the
-    // segment of head yoff_i + k - 1 (k = 0: the piece continuing the column to
-    // the left, "red"), stored at slot yoff_i + k (slot h + 1 = head h).  A
-    // tile whose slots fit in shared memory (the common case) runs the
-    // unrolled loop; tiles of very short rows use the per-warp global spill
-    // area through a compact loop that re-reads x (L1 hits).
-    double sum = 0.0, red = 0.0;
-    if (fast) {
-      double* cp = closed + yoff;
-#pragma unroll
-      for (int j0 = 0; j0 < SIG; j0 += CH) {
-        double xv[CH];
-        if (j0 == 0) {
-#pragma unroll
-          for (int u = 0; u < CH; ++u) xv[u] = xa[u];
-        } else {
-#pragma unroll
-          for (int u = 0; u < CH; ++u)
-            if (j0 + u < SIG) xv[u] = ld_keep(a.x + sc[(j0 + u) * 32 + lane], pol_x);
-        }
-#pragma unroll
-        for (int u = 0; u < CH; ++u) {
-          const int j = j0 + u;
-          if (j < SIG) {
-            if ((fr >> j) & 1ull) {  // predicated: store, advance, restart
-              *cp++ = sum;
-              sum = 0.0;
-            }
-            sum = fma(sv[j * 32 + lane], xv[u], sum);
-          }
-        }
-      }
-    } else {
-      double* sp = spill + yoff;
-#pragma unroll 1
-      for (int j = 0; j < SIG; ++j) {
-        if ((fr >> j) & 1ull) {
-          if (sp == spill + yoff) red = sum;
-          *sp++ = sum;
-          sum = 0.0;
-        }
-        sum = fma(sv[j * 32 + lane], __ldg(a.x + sc[j * 32 + lane]), sum);
-      }
-    }
-    // predicated stores on every path: the loads above are consumed here, before
-    // the gathers go out, on flagged and unflagged tiles alike (a branch would
-    // leave a possibly-outstanding load whose scoreboard the gathers reuse)
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      sts_if(eos + lane + 32 * q, eov4[q], flagged && fast && lane + 32 * q < H);
-    __syncwarp();
-    if (lane == 0 && k + S < ke && !compute_only) issue(k + S, s);  // refill this stage
-    // gathers for tile k+1 land in the registers the depth loop just drained;
-    // their latency overlaps this tile's splice, write-back and run merge
-    if (EARLY_OK && a.early_gather) {
-#pragma unroll
-      for (int u = 0; u < CH; ++u) xa[u] = xn[u];
-    } else if (k + 1 < ke) {
-      if (!compute_only) mbar_wait(bars + sn, pn);
-      gather(sn, xa);
-    }
-    s = sn;
-    phase = pn;
-
-    // ---- splice across columns: tmp[i] = piece handed left by column i+1 ----
-    const bool seen = cnt > 0;
-    // this lane's own first close: read back from shared memory (the spill
-    // loop keeps it in a register, so no global load here has to wait for
-    // the next tile's gathers)
-    if (fast && seen) red = closed[yoff];
-    const double give = seen ? red : sum;
-    double tmp = __shfl_down_sync(kFull, give, 1);
-    if (lane == 31) tmp = 0.0;
-    const uint32_t hb = __ballot_sync(kFull, seen);
-    const uint64_t above = (uint64_t)hb >> (lane + 1);
-    const int end = above ? lane + __ffsll((long long)above) - 1 : 31;
-    double acc = tmp;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const double o = __shfl_down_sync(kFull, acc, d);
-      if (lane + d <= end) acc += o;
-    }
-    if (seen) {  // the column's bottom piece
-      if (fast)
-        closed[yoff + cnt] = sum + acc;
+  if (has_tiles) {
+    double* __restrict__ y = a.y;
+    const bool yh = a.y_hint != 0;
+    auto put_y = [&](int64_t r, double v) {
+      if (yh)
+        st_hint(y + r, v, pol_s);
       else
-        spill[yoff + cnt] = sum + acc;
-    }
-    __syncwarp();
+        y[r] = v;
+    };
+    int64_t pend_row = -1;
+    double pend_val = 0.0;
+    bool pend_first = true;
+    uint32_t tpv = 0, tpv_next = 0;
+    int64_t eov = 0;
+    int s = 0;
+    uint32_t phase = 0;
+    // x gathers run one tile ahead: while tile k is spliced and written back,
+    // the first CH gathers of tile k+1 (whose col_idx already sit in the next
+    // ring stage) are in flight.
+    auto gather = [&](int st_idx, double(&xv)[CH]) {
+      const int32_t* sc = reinterpret_cast<const int32_t*>(ring + (size_t)st_idx * a.stage_bytes + COL_OFF);
+      if (a.x_mode == 1) {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) xv[u] = ld_keep_na(a.x + sc[u * 32 + lane], pol_x);
+      } else if (a.x_mode == 2) {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) xv[u] = ld_x_lsu(a.x + sc[u * 32 + lane], pol_x);
+      } else if (a.x_mode == 3) {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) xv[u] = ld_x_cg(a.x + sc[u * 32 + lane]);
+      } else if (a.x_mode == 4) {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) xv[u] = ld_x_plain(a.x + sc[u * 32 + lane]);
+      } else {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) xv[u] = ld_keep(a.x + sc[u * 32 + lane], pol_x);
+      }
+    };
+    double xa[CH];
+    mbar_wait(bars, 0);
+    gather(0, xa);
 
-    // ---- write-back of the tile's heads in order ----
-    // Two copies of one loop: shared-slot tiles read slots and empty_offset
-    // from shared memory only, spill tiles from global memory.
-    double c0 = 0.0, cL = 0.0;
-    int64_t rL = 0;
-    int64_t defer_lo = 0, defer_hi = 0;
-    auto write_back = [&](auto eo_at, auto slot_at) {
-      c0 = slot_at(1);
-      cL = slot_at(H);
-      const int nch = (H + 31) >> 5;
-#pragma unroll 1
-      for (int c = 0; c < nch; ++c) {  // warp-uniform trip count
-        const int h = lane + 32 * c;
-        if (h >= H) break;
-        const int64_t r = tile_row + (flagged ? (int64_t)eo_at(h) : (int64_t)h);
-        if (h == H - 1) rL = r;
-        if (h != 0 && h != H - 1) put_y(r, slot_at(h + 1));
-        if (flagged || h == H - 1) {  // empty rows up to the next head (or next tile)
-          const int64_t nr = h + 1 < H ? tile_row + (int64_t)eo_at(h + 1) : next_row;
-          if (nr - r - 1 <= 8) {
-            for (int64_t q = r + 1; q < nr; ++q) put_y(q, 0.0);
-          } else if (defer_hi == defer_lo) {
-            defer_lo = r + 1;
-            defer_hi = nr;
+    for (int64_t k = kb; k < ke; ++k) {
+      const int slot = (int)((k - kb) & 31);
+      if (slot == 0) {  // per-tile scalars, 32 tiles per batch
+        const int64_t last = a.tile_ptr_len - 1;
+        tpv = a.tile_ptr[k + lane < last ? k + lane : last];
+        tpv_next = a.tile_ptr[k + 32 < last ? k + 32 : last];
+        eov = a.eo_ptr[k + lane < a.pcs ? k + lane : a.pcs];
+      }
+      const uint32_t tp = __shfl_sync(kFull, tpv, slot);
+      const uint32_t tpn_s = __shfl_sync(kFull, tpv, (slot + 1) & 31);
+      const uint32_t tpn = slot == 31 ? tpv_next : tpn_s;
+      const int64_t eo_base = __shfl_sync(kFull, eov, slot);
+      const int64_t tile_row = tp & 0x7fffffffu;
+      const bool flagged = (tp >> 31) != 0;
+      const int64_t next_row = (k + 1 == a.pcs) ? a.next_row_after : (int64_t)(tpn & 0x7fffffffu);
+      const int32_t* __restrict__ eo = a.eo + eo_base;
+
+      // profiling knob 2: compute only -- every tile re-reads the resident
+      // stage 0, no TMA traffic after the prologue (y is garbage)
+      const bool compute_only = a.stream_only == 2;
+      const int sn = compute_only ? 0 : (s + 1 == S ? 0 : s + 1);
+      const uint32_t pn = compute_only ? 0u : (s + 1 == S ? phase ^ 1u : phase);
+      if (a.stream_only == 1) {  // profiling knob 1: the TMA ring alone (y is garbage)
+        mbar_wait(bars + s, phase);
+        __syncwarp();
+        if (lane == 0 && k + S < ke) issue(k + S, s);
+        s = s + 1 == S ? 0 : s + 1;
+        phase = s == 0 ? phase ^ 1u : phase;
+        continue;
+      }
+      // random gathers (long misses): tile k+1's gathers also overlap tile k's
+      // depth loop, at the cost of a second register array and a copy
+      double xn[CH];
+      if (EARLY_OK && a.early_gather && k + 1 < ke) {
+        if (!compute_only) mbar_wait(bars + sn, pn);
+        gather(sn, xn);
+      }
+      const unsigned char* st = ring + (size_t)s * a.stage_bytes;
+      const double* sv = reinterpret_cast<const double*>(st);
+      const int32_t* sc = reinterpret_cast<const int32_t*>(st + COL_OFF);
+      const uint64_t wd = (uint64_t)reinterpret_cast<const W*>(st + DESC_OFF)[lane];
+      const uint64_t fr = __brevll(wd & FMASK) >> (64 - SIG);  // bit j = depth j
+      const int yoff = (int)(wd >> (kSegBits + SIG));
+      const int cnt = __popcll(fr);
+      const int H = __shfl_sync(kFull, yoff + cnt, 31);
+      const bool fast = H < CAPC;
+      // a flagged shared-slot tile's empty_offset entries (H < 128: at most 4
+      // per lane) are in flight during the depth loop
+      int32_t eov4[4] = {0, 0, 0, 0};
+      if (flagged && fast) {
+  #pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (lane + 32 * q < H) eov4[q] = eo[lane + 32 * q];
+      }
+
+      // ---- depth loop (spmv.cpp:61-95): gathers first, then FMAs ----
+      // Every close at a bit flag goes to a slot: lane i's k-th flag ends the
+      // segment of head yoff_i + k - 1 (k = 0: the piece continuing the column to
+      // the left, "red"), stored at slot yoff_i + k (slot h + 1 = head h).  A
+      // tile whose slots fit in shared memory (the common case) runs the
+      // unrolled loop; tiles of very short rows use the per-warp global spill
+      // area through a compact loop that re-reads x (L1 hits).
+      double sum = 0.0, red = 0.0;
+      if (fast) {
+        double* cp = closed + yoff;
+  #pragma unroll
+        for (int j0 = 0; j0 < SIG; j0 += CH) {
+          double xv[CH];
+          if (j0 == 0) {
+  #pragma unroll
+            for (int u = 0; u < CH; ++u) xv[u] = xa[u];
           } else {
-            for (int64_t q = r + 1; q < nr; ++q) put_y(q, 0.0);
+  #pragma unroll
+            for (int u = 0; u < CH; ++u)
+              if (j0 + u < SIG) xv[u] = ld_keep(a.x + sc[(j0 + u) * 32 + lane], pol_x);
+          }
+  #pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            const int j = j0 + u;
+            if (j < SIG) {
+              if ((fr >> j) & 1ull) {  // predicated: store, advance, restart
+                *cp++ = sum;
+                sum = 0.0;
+              }
+              sum = fma(sv[j * 32 + lane], xv[u], sum);
+            }
           }
         }
+      } else {
+        double* sp = spill + yoff;
+  #pragma unroll 1
+        for (int j = 0; j < SIG; ++j) {
+          if ((fr >> j) & 1ull) {
+            if (sp == spill + yoff) red = sum;
+            *sp++ = sum;
+            sum = 0.0;
+          }
+          sum = fma(sv[j * 32 + lane], __ldg(a.x + sc[j * 32 + lane]), sum);
+        }
       }
-    };
-    if (fast)
-      write_back([&](int i) { return eos[i]; }, [&](int i) { return closed[i]; });
-    else
-      write_back([&](int i) { return eo[i]; }, [&](int i) { return spill[i]; });
-    rL = __shfl_sync(kFull, rL, (H - 1) & 31);
-    uint32_t dm = __ballot_sync(kFull, defer_hi > defer_lo);
-    while (dm) {  // long empty-row runs: zero cooperatively
-      const int src = __ffs(dm) - 1;
-      dm &= dm - 1;
-      const int64_t lo = __shfl_sync(kFull, defer_lo, src);
-      const int64_t hi = __shfl_sync(kFull, defer_hi, src);
-      for (int64_t q = lo + lane; q < hi; q += 32) put_y(q, 0.0);
-    }
-    __syncwarp();  // closed[] is rewritten by the next tile
+      // predicated stores on every path: the loads above are consumed here, before
+      // the gathers go out, on flagged and unflagged tiles alike (a branch would
+      // leave a possibly-outstanding load whose scoreboard the gathers reuse)
+  #pragma unroll
+      for (int q = 0; q < 4; ++q)
+        sts_if(eos + lane + 32 * q, eov4[q], flagged && fast && lane + 32 * q < H);
+      __syncwarp();
+      if (lane == 0 && k + S < ke && !compute_only) issue(k + S, s);  // refill this stage
+      // gathers for tile k+1 land in the registers the depth loop just drained;
+      // their latency overlaps this tile's splice, write-back and run merge
+      if (EARLY_OK && a.early_gather) {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) xa[u] = xn[u];
+      } else if (k + 1 < ke) {
+        if (!compute_only) mbar_wait(bars + sn, pn);
+        gather(sn, xa);
+      }
+      s = sn;
+      phase = pn;
 
-    // ---- row runs across the warp's consecutive tiles ----
-    auto flush = [&]() {
-      if (lane == 0) {
-        if (pend_first)
-          put_item(a, 2 * (int64_t)w, pend_row, pend_val);
-        else
-          put_y(pend_row, pend_val);
+      // ---- splice across columns: tmp[i] = piece handed left by column i+1 ----
+      const bool seen = cnt > 0;
+      // this lane's own first close: read back from shared memory (the spill
+      // loop keeps it in a register, so no global load here has to wait for
+      // the next tile's gathers)
+      if (fast && seen) red = closed[yoff];
+      const double give = seen ? red : sum;
+      double tmp = __shfl_down_sync(kFull, give, 1);
+      if (lane == 31) tmp = 0.0;
+      const uint32_t hb = __ballot_sync(kFull, seen);
+      const uint64_t above = (uint64_t)hb >> (lane + 1);
+      const int end = above ? lane + __ffsll((long long)above) - 1 : 31;
+      double acc = tmp;
+  #pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double o = __shfl_down_sync(kFull, acc, d);
+        if (lane + d <= end) acc += o;
       }
-    };
-    if (k == kb) {
-      pend_row = tile_row;
-      pend_val = c0;
-      pend_first = true;
-    } else if (tile_row == pend_row) {
-      pend_val += c0;
-    } else {
-      flush();
-      pend_row = tile_row;
-      pend_val = c0;
-      pend_first = false;
+      if (seen) {  // the column's bottom piece
+        if (fast)
+          closed[yoff + cnt] = sum + acc;
+        else
+          spill[yoff + cnt] = sum + acc;
+      }
+      __syncwarp();
+
+      // ---- write-back of the tile's heads in order ----
+      // Two copies of one loop: shared-slot tiles read slots and empty_offset
+      // from shared memory only, spill tiles from global memory.
+      double c0 = 0.0, cL = 0.0;
+      int64_t rL = 0;
+      int64_t defer_lo = 0, defer_hi = 0;
+      auto write_back = [&](auto eo_at, auto slot_at) {
+        c0 = slot_at(1);
+        cL = slot_at(H);
+        const int nch = (H + 31) >> 5;
+  #pragma unroll 1
+        for (int c = 0; c < nch; ++c) {  // warp-uniform trip count
+          const int h = lane + 32 * c;
+          if (h >= H) break;
+          const int64_t r = tile_row + (flagged ? (int64_t)eo_at(h) : (int64_t)h);
+          if (h == H - 1) rL = r;
+          if (h != 0 && h != H - 1) put_y(r, slot_at(h + 1));
+          if (flagged || h == H - 1) {  // empty rows up to the next head (or next tile)
+            const int64_t nr = h + 1 < H ? tile_row + (int64_t)eo_at(h + 1) : next_row;
+            if (nr - r - 1 <= 8) {
+              for (int64_t q = r + 1; q < nr; ++q) put_y(q, 0.0);
+            } else if (defer_hi == defer_lo) {
+              defer_lo = r + 1;
+              defer_hi = nr;
+            } else {
+              for (int64_t q = r + 1; q < nr; ++q) put_y(q, 0.0);
+            }
+          }
+        }
+      };
+      if (fast)
+        write_back([&](int i) { return eos[i]; }, [&](int i) { return closed[i]; });
+      else
+        write_back([&](int i) { return eo[i]; }, [&](int i) { return spill[i]; });
+      rL = __shfl_sync(kFull, rL, (H - 1) & 31);
+      uint32_t dm = __ballot_sync(kFull, defer_hi > defer_lo);
+      while (dm) {  // long empty-row runs: zero cooperatively
+        const int src = __ffs(dm) - 1;
+        dm &= dm - 1;
+        const int64_t lo = __shfl_sync(kFull, defer_lo, src);
+        const int64_t hi = __shfl_sync(kFull, defer_hi, src);
+        for (int64_t q = lo + lane; q < hi; q += 32) put_y(q, 0.0);
+      }
+      __syncwarp();  // closed[] is rewritten by the next tile
+
+      // ---- row runs across the warp's consecutive tiles ----
+      auto flush = [&]() {
+        if (lane == 0) {
+          if (pend_first)
+            put_item(a, 2 * (int64_t)w, pend_row, pend_val);
+          else
+            put_y(pend_row, pend_val);
+        }
+      };
+      if (k == kb) {
+        pend_row = tile_row;
+        pend_val = c0;
+        pend_first = true;
+      } else if (tile_row == pend_row) {
+        pend_val += c0;
+      } else {
+        flush();
+        pend_row = tile_row;
+        pend_val = c0;
+        pend_first = false;
+      }
+      if (H >= 2) {
+        flush();
+        pend_row = rL;
+        pend_val = cL;
+        pend_first = false;
+      }
     }
-    if (H >= 2) {
-      flush();
-      pend_row = rL;
-      pend_val = cL;
-      pend_first = false;
-    }
-  }
-  if (lane == 0) {
-    if (pend_first) {
-      put_item(a, 2 * (int64_t)w, pend_row, pend_val);
-      put_item(a, 2 * (int64_t)w + 1, pend_row, 0.0);
-    } else {
-      put_item(a, 2 * (int64_t)w + 1, pend_row, pend_val);
+    if (lane == 0) {
+      if (pend_first) {
+        put_item(a, 2 * (int64_t)w, pend_row, pend_val);
+        put_item(a, 2 * (int64_t)w + 1, pend_row, 0.0);
+      } else {
+        put_item(a, 2 * (int64_t)w + 1, pend_row, pend_val);
+      }
     }
   }
 }
 
 namespace {
-
-__device__ __forceinline__ void write_run(int64_t row, double v, double* y, int64_t first_row,
-                                          int first_owned, csr5g_partial* send) {
-  if (!first_owned && row == first_row) {
-    send->row = row;
-    send->value = v;
-  } else {
-    y[row] = v;
-  }
-}
-
-__global__ void k_calibrate(const int64_t* __restrict__ item_row,
-                            const double* __restrict__ item_val, int64_t N, double* __restrict__ y,
-                            int64_t first_row, int first_owned, csr5g_partial* send) {
-  const int lane = threadIdx.x & 31;
-  const int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane;
-  if (base >= N) return;
-  if (base == 0 && lane == 0) {
-    send->row = -1;
-    send->value = 0.0;
-  }
-  __syncwarp();
-  const int64_t i = base + lane;
-  const bool valid = i < N;
-  const int64_t key = valid ? item_row[i] : (LLONG_MAX - lane);
-  int64_t prev = __shfl_up_sync(kFull, key, 1);
-  if (lane == 0) prev = base > 0 ? item_row[base - 1] : LLONG_MIN;
-  const bool start = valid && key != prev;
-  const uint32_t sm = __ballot_sync(kFull, start);
-  const uint32_t vm = __ballot_sync(kFull, valid);
-  const uint64_t above = (uint64_t)sm >> (lane + 1);
-  const int end = above ? lane + __ffsll((long long)above) - 1 : 31 - __clz(vm);
-  double v = valid ? item_val[i] : 0.0;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const double o = __shfl_down_sync(kFull, v, d);
-    if (lane + d <= end) v += o;
-  }
-  const int ls = sm ? 31 - __clz(sm) : -1;
-  bool cont = false;
-  int64_t rk = 0;
-  if (ls >= 0) {
-    rk = __shfl_sync(kFull, key, ls);
-    cont = (base + 32 < N) && item_row[base + 32] == rk;
-  }
-  if (start && !(cont && lane == ls)) write_run(key, v, y, first_row, first_owned, send);
-  if (cont) {
-    double total = __shfl_sync(kFull, v, ls);
-    for (int64_t pos = base + 32;; pos += 32) {
-      const int64_t q = pos + lane;
-      const bool mt = q < N && item_row[q] == rk;
-      const uint32_t mm = __ballot_sync(kFull, mt);
-      double s = mt ? item_val[q] : 0.0;
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(kFull, s, d);
-      total += s;
-      if (mm != kFull) break;
-    }
-    if (lane == 0) write_run(rk, total, y, first_row, first_owned, send);
-  }
-}
 
 __global__ void k_fixup(const csr5g_partial* __restrict__ all, int world, int rank, int64_t row,
                         double* __restrict__ y) {
@@ -729,6 +747,11 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     return e ? std::atoi(e) : 0;
   }();
   a.stream_only = stream_only;
+  const int64_t items = 2 * (int64_t)h->nwarps + (h->has_tail_item ? 1 : 0);
+  static const bool pdl_on = [] {  // CSR5G_PDL=0: plain stream order (A/B)
+    const char* e = std::getenv("CSR5G_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
   if (ev0) CSR5G_CUDA(cudaEventRecord(ev0, stream));
   if (grid > 0) {
     cudaLaunchConfig_t cfg{};
@@ -761,12 +784,20 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     CSR5G_CUDA(cudaLaunchKernelEx(&cfg, spmv_fn(a.sigma), a));
   }
   if (ev1) CSR5G_CUDA(cudaEventRecord(ev1, stream));
-  const int64_t items = 2 * (int64_t)h->nwarps + (h->has_tail_item ? 1 : 0);
   if (stream_only) return CSR5G_OK;  // no items were produced
   if (!atomic && items > 0) {
-    k_calibrate<<<(unsigned)((items + 255) / 256), 256, 0, stream>>>(
-        h->item_row, h->item_val, items, d_y, h->first_row, h->first_owned, a.send);
-    CSR5G_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)((items + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl;
+    cfg.numAttrs = pdl_on ? 1 : 0;
+    CSR5G_CUDA(cudaLaunchKernelEx(&cfg, k_calibrate, (const int64_t*)h->item_row,
+                                  (const double*)h->item_val, items, d_y, h->first_row,
+                                  (int)h->first_owned, a.send));
   } else if (!atomic) {
     const csr5g_partial none{-1, 0.0};
     CSR5G_CUDA(cudaMemcpyAsync(a.send, &none, sizeof none, cudaMemcpyHostToDevice, stream));
