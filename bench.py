@@ -378,13 +378,30 @@ def run_ours(args, workload_name, workload):
     torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
-    # the steps: the public call alone between the events
+    # the steps: the public call alone between the events (iterative mode:
+    # plus y -> x, the all-gather of the owned ranges at N>1)
+    if args.iterative:
+        if m != n:
+            raise SystemExit("--iterative needs a square matrix")
+        x_keep = x.clone()
+
+        def step():
+            run()
+            if world == 1:
+                x.copy_(y)
+            else:
+                sh.gather_y_into_x(y, x)
+    else:
+        step = run
     for k in range(args.steps):
         if scrub is not None:
             scrub.zero_()
         steps_ev[k][0].record()
-        run()
+        step()
         steps_ev[k][1].record()
+    if args.iterative:
+        x.copy_(x_keep)
+        del x_keep
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -577,6 +594,8 @@ def run_ours(args, workload_name, workload):
             "config": {"workload": workload_name, "desc": workload["desc"], "m": m, "n": n,
                        "nnz": nnz, "omega": 32, "sigma": sigma, "p": info.p,
                        "desc_word_bits": info.word_bits, "mode": "deterministic",
+                       "step": ("iterative: SpMV + y->x all-gather" if args.iterative else
+                                "SpMV (+ boundary exchange at N>1)"),
                        "spmv_plan": {"lines_per_gather": round(info.lines_per_gather, 2),
                                      "warps_per_cta": info.warps_per_cta, "stages": info.stages,
                                      "smem_bytes": info.smem_bytes, "x_mode": info.x_mode,
@@ -621,6 +640,9 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="st27_200")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--iterative", action="store_true",
+                    help="y -> x mode (square A): each step is SpMV plus the all-gather of y "
+                         "into every rank's x (x <- y at N=1)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="N>1: weak = the global matrix is N times the 1-GPU workload (stencils "
                          "N times deeper, graphs log2 N scales larger); strong = the same matrix")

@@ -12,7 +12,8 @@ holding its first nonzero.  Each shard has at most one partial to send (its
 first row, when it does not own it); the driver all-gathers the 16-byte
 records and every owner adds the partials of later shards in shard order
 (csr5g_fixup) -- deterministic.  In the iterative mode (y -> x, square A) the
-owned row ranges of y are all-gathered into every rank's x.
+owned row ranges of y are all-gathered (one NCCL all-gather, ranges padded to
+the longest) into every rank's x.
 
 The reference has no distributed backend; this is new ("Multi-GPU
 driver").  Host logic is covered by world_size-2 gloo tests on CPU
@@ -160,25 +161,32 @@ class Csr5Sharded:
         return y
 
     def gather_y_into_x(self, y, x):
-        """Iterative mode: every rank's x <- the owned ranges of y (uneven
-        ranges: one broadcast per root, coalesced by NCCL's group semantics)."""
+        """Iterative mode (square A): every rank's x <- the owned ranges of y,
+        one all-gather (gather_owned)."""
         gather_owned(self.dist, y, x, self.ranges, self.rank, self.group)
         return x
 
 
 def gather_owned(dist, y, x, ranges, rank, group=None):
-    """x[lo:hi] <- rank g's y[lo:hi] for every g (host logic shared with the
-    gloo tests)."""
-    staged = _staged(dist, group) and x.is_cuda
+    """x[lo:hi] <- rank g's y[lo:hi] for every g: one all-gather of the owned
+    ranges (NCCL over NVLink; host-staged on gloo).  Ranges are uneven, so each
+    rank sends its range padded to the longest and the received blocks are
+    copied into place.  Host logic shared with the gloo tests."""
+    import torch
+    lens = [max(0, hi - lo) for lo, hi in ranges]
+    width = max(lens) if lens else 0
+    if width == 0:
+        return x
+    send = torch.zeros(width, dtype=y.dtype, device=y.device)
+    lo, hi = ranges[rank]
+    if hi > lo:
+        send[:hi - lo].copy_(y[lo:hi])
+    recv = torch.empty(width * len(ranges), dtype=y.dtype, device=y.device)
+    all_gather_flat(dist, recv, send, group)
     for g, (lo, hi) in enumerate(ranges):
-        if hi <= lo:
-            continue
-        if g == rank:
-            x[lo:hi].copy_(y[lo:hi])
-        t = x[lo:hi].cpu() if staged else x[lo:hi].contiguous()
-        dist.broadcast(t, src=g, group=group)
-        if g != rank and (staged or t.data_ptr() != x[lo:hi].data_ptr()):
-            x[lo:hi].copy_(t)
+        if hi > lo:
+            x[lo:hi].copy_(recv[g * width:g * width + hi - lo])
+    return x
 
 
 # ---------------------------------------------------------------------------

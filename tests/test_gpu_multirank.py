@@ -22,15 +22,16 @@ def _port() -> int:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,workload,scaling", [(2, "lap5_1000", "weak"),
-                                                (3, "lap5_1000", "strong"),
-                                                (4, "lap5_1000", "weak")])
-def test_bench_sharded_on_one_gpu(n, workload, scaling):
+@pytest.mark.parametrize("n,workload,scaling,iterative", [(2, "lap5_1000", "weak", False),
+                                                          (3, "lap5_1000", "strong", False),
+                                                          (4, "lap5_1000", "weak", False),
+                                                          (3, "lap5_1000", "weak", True)])
+def test_bench_sharded_on_one_gpu(n, workload, scaling, iterative):
     env = dict(os.environ, CSR5G_DIST_BACKEND="gloo", CSR5G_SHARE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py",
            "--gpus", str(n), "--steps", "3", "--warmup", "3", "--workload", workload,
-           "--scaling", scaling]
+           "--scaling", scaling] + (["--iterative"] if iterative else [])
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
