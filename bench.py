@@ -384,12 +384,14 @@ def run_ours(args, workload_name, workload):
         if m != n:
             raise SystemExit("--iterative needs a square matrix")
         x_keep = x.clone()
+        bufs = [x, y]
 
         def step():
-            run()
-            if world == 1:
-                x.copy_(y)
+            if world == 1:  # ping-pong: y of this step is x of the next
+                csr5.spmv_csr5(a5, bufs[0], bufs[1])
+                bufs.reverse()
             else:
+                run()
                 sh.gather_y_into_x(y, x)
     else:
         step = run
@@ -642,7 +644,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--iterative", action="store_true",
                     help="y -> x mode (square A): each step is SpMV plus the all-gather of y "
-                         "into every rank's x (x <- y at N=1)")
+                         "into every rank's x (N=1: x and y swap roles every step)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="N>1: weak = the global matrix is N times the 1-GPU workload (stencils "
                          "N times deeper, graphs log2 N scales larger); strong = the same matrix")
