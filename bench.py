@@ -16,7 +16,7 @@ BASELINE config 5), so per-GPU work is fixed; --scaling strong shards the
 
 `value` is GFLOP/s = 2*nnz / t with A and x resident in HBM; t is the max over
 ranks of CUDA-event time on the launching stream.  L2 is flushed between timed
-calls (2x L2 written outside the events).  `e2e` is the same metric through
+calls (2x L2 read outside the events).  `e2e` is the same metric through
 the host-buffer call (csr5.spmv_host_batch): per step pinned x H2D + SpMV + y
 D2H, pipelined across steps on separate copy engines.  The roofline
 figure is for the dominant tile kernel alone (events around it), with the
@@ -361,8 +361,9 @@ def run_ours(args, workload_name, workload):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
-    # L2 flushed between timed calls (a 2x-L2 write outside the events), so no
-    # step starts with x or the matrix left in L2 by the previous one
+    # L2 flushed between timed calls (a 2x-L2 read outside the events), so no
+    # step starts with x or the matrix left in L2 by the previous one; a read
+    # leaves clean lines, so the next call pays no write-back for the flush
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     scrub = torch.empty(2 * l2_bytes // 8 + 1, dtype=torch.float64, device=dev)
 
@@ -395,7 +396,7 @@ def run_ours(args, workload_name, workload):
         step = run
     for k in range(args.steps):
         if scrub is not None:
-            scrub.zero_()
+            scrub.sum()  # read-only flush: evicts without leaving dirty lines
         steps_ev[k][0].record()
         step()
         steps_ev[k][1].record()
@@ -409,7 +410,7 @@ def run_ours(args, workload_name, workload):
     # recorded around the tile kernel on its stream
     for k in range(args.steps):
         if scrub is not None:
-            scrub.zero_()
+            scrub.sum()  # read-only flush: evicts without leaving dirty lines
         if world == 1:
             csr5.spmv_csr5_evt(a5, x, y, tk[k][0], tk[k][1])
         elif a5 is not None:
@@ -605,7 +606,7 @@ def run_ours(args, workload_name, workload):
                                      "x_l2_window": info.x_window},
                        "parallelism": f"tile-range shards x{world}, x replicated",
                        "l2": (f"L2 flushed between timed calls ({2 * l2_bytes / 1e6:.0f} MB "
-                              f"written outside the events); working set "
+                              f"read outside the events); working set "
                               f"{info.spmv_bytes / 1e6:.0f} MB per SpMV"),
                        "x": "mt19937_64(1), 0.5 + (rng()>>11)*2^-53 (bench.cpp:103-105)"},
             "gbs_effective": info.spmv_bytes * world / (ms * 1e-3) / 1e9 if world == 1 else None,
