@@ -152,6 +152,93 @@ __global__ void __launch_bounds__(128) k_desc_transpose(
   for (int j = 0; j < sigma; ++j) col_out[tb + j * 32 + lane] = ib[j * 33 + lane];
 }
 
+// Same output as k_desc_transpose, fed by TMA: persistent warps walk tiles
+// gw, gw + W, ...; lane 0 bulk-copies a tile's val (B*8 bytes) and col_idx (B*4)
+// into a 2-stage linear ring one tile ahead, so the global reads are deep
+// asynchronous streams instead of latency-bound register loads.  The lanes then
+// move the tile through a padded buffer (conflict-free both ways) and write
+// the transposed rows coalesced.  Needs 16-byte aligned inputs (the launcher
+// falls back to k_desc_transpose otherwise).
+template <typename W>
+__global__ void __launch_bounds__(512) k_desc_transpose_tma(
+    const uint32_t* __restrict__ head_bits, const uint32_t* __restrict__ tile_ptr,
+    const int32_t* __restrict__ col_in, const double* __restrict__ val_in,
+    int32_t* __restrict__ col_out, double* __restrict__ val_out, W* __restrict__ desc,
+    int64_t* __restrict__ eo_cnt, int64_t pcs, int sigma, int stage_bytes) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int B = 32 * sigma;
+  const int64_t nwt = (int64_t)gridDim.x * NW;
+  const int64_t gw = (int64_t)blockIdx.x * NW + wib;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm) + 2 * wib;
+  const size_t pad_bytes = ((size_t)sigma * 33 * 8 + 127) / 128 * 128;
+  unsigned char* base = sm + 256 + (size_t)wib * (2 * (size_t)stage_bytes + pad_bytes);
+  double* buf = reinterpret_cast<double*>(base + 2 * (size_t)stage_bytes);
+  const uint64_t pol = policy_evict_first();
+  auto issue = [&](int64_t k, int st) {  // lane 0
+    unsigned char* dst = base + (size_t)st * stage_bytes;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect(bars + st, (uint32_t)B * 12u);
+    bulk_load(dst, val_in + k * B, (uint32_t)B * 8u, bars + st, pol);
+    bulk_load(dst + (size_t)B * 8, col_in + k * B, (uint32_t)B * 4u, bars + st, pol);
+  };
+  if (lane == 0) {
+    mbar_init(bars);
+    mbar_init(bars + 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (gw < pcs) issue(gw, 0);
+    if (gw + nwt < pcs) issue(gw + nwt, 1);
+  }
+  __syncwarp();
+  const float inv = 1.0f / (float)sigma;
+  int st = 0;
+  uint32_t phase = 0;
+  for (int64_t k = gw; k < pcs; k += nwt) {
+    // ---- descriptor (format.cpp:102-121 + descriptor.cpp:38-62) ----
+    const uint64_t bits = column_bits(head_bits, k, B, sigma, lane);
+    const int cnt = __popcll(bits);
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const int yoff = incl - cnt;
+    const int H = __shfl_sync(kFull, incl, 31);
+    const uint32_t hb = __ballot_sync(kFull, cnt > 0);
+    const uint64_t above = (uint64_t)hb >> (lane + 1);
+    const int seg = cnt ? (above ? __ffsll((long long)above) - 1 : 31 - lane) : 0;
+    const uint64_t flags = __brevll(bits) >> (64 - sigma);
+    desc[k * 32 + lane] =
+        (W)(((uint64_t)yoff << (kSegBits + sigma)) | ((uint64_t)seg << sigma) | flags);
+    if (lane == 0) eo_cnt[k] = (tile_ptr[k] >> 31) ? H : 0;
+
+    // ---- transpose: logical i*sigma+j -> physical j*32+i (format.hpp:76-88) ----
+    mbar_wait(bars + st, phase);
+    const double* sv = reinterpret_cast<const double*>(base + (size_t)st * stage_bytes);
+    const int32_t* sc = reinterpret_cast<const int32_t*>(sv + B);
+    const int64_t tb = k * B;
+    for (int e = lane; e < B; e += 32) {
+      const int i = __float2int_rz(((float)e + 0.5f) * inv);
+      buf[(e - i * sigma) * 33 + i] = sv[e];
+    }
+    __syncwarp();
+    for (int j = 0; j < sigma; ++j) val_out[tb + j * 32 + lane] = buf[j * 33 + lane];
+    __syncwarp();
+    int32_t* ib = reinterpret_cast<int32_t*>(buf);
+    for (int e = lane; e < B; e += 32) {
+      const int i = __float2int_rz(((float)e + 0.5f) * inv);
+      ib[(e - i * sigma) * 33 + i] = sc[e];
+    }
+    __syncwarp();  // the stage has been read: refill it two tiles ahead
+    if (lane == 0 && k + 2 * nwt < pcs) issue(k + 2 * nwt, st);
+    for (int j = 0; j < sigma; ++j) col_out[tb + j * 32 + lane] = ib[j * 33 + lane];
+    __syncwarp();
+    st ^= 1;
+    phase ^= (st == 0);
+  }
+}
+
 // empty_offset entries of flagged tiles (format.cpp:123-136): for every head
 // in column-major order, row_of_nonzero(g) - tile_row.
 __global__ void k_eo(const uint32_t* __restrict__ head_bits, const uint32_t* __restrict__ tile_ptr,
@@ -452,20 +539,48 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   }
   trace.mark("tile_ptr");
   if (pcs > 0) {
-    const size_t smem = (size_t)4 * sigma * 33 * sizeof(double);
-    const unsigned grid = (unsigned)((pcs + 3) / 4);
-    if (h->wide) {
-      TRYC(cudaFuncSetAttribute(k_desc_transpose<uint64_t>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_desc_transpose<uint64_t><<<grid, 128, smem, stream>>>(
-          head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint64_t*)h->desc, eo_cnt,
-          pcs, (int)sigma);
+    // TMA-fed kernel when the input tiles are 16-byte aligned (B*8 and B*4 are
+    // multiples of 16 for every sigma); the register-load kernel otherwise
+    const bool aligned = ((uintptr_t)d_col_idx & 15) == 0 && ((uintptr_t)d_val & 15) == 0;
+    if (aligned) {
+      const int stage_bytes = (int)(((size_t)B * 12 + 127) / 128 * 128);
+      const size_t pad_bytes = ((size_t)sigma * 33 * 8 + 127) / 128 * 128;
+      const size_t per_warp = 2 * (size_t)stage_bytes + pad_bytes;
+      const int nw = (int)std::max<size_t>(1, std::min<size_t>(16, (220 * 1024 - 256) / per_warp));
+      const size_t smem = 256 + nw * per_warp;
+      const int64_t warps_needed = pcs;
+      int sms = 0;
+      TRYC(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      const unsigned grid = (unsigned)std::min<int64_t>((warps_needed + nw - 1) / nw, sms);
+      if (h->wide) {
+        TRYC(cudaFuncSetAttribute(k_desc_transpose_tma<uint64_t>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_desc_transpose_tma<uint64_t><<<grid, 32 * nw, smem, stream>>>(
+            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint64_t*)h->desc, eo_cnt,
+            pcs, (int)sigma, stage_bytes);
+      } else {
+        TRYC(cudaFuncSetAttribute(k_desc_transpose_tma<uint32_t>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_desc_transpose_tma<uint32_t><<<grid, 32 * nw, smem, stream>>>(
+            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint32_t*)h->desc, eo_cnt,
+            pcs, (int)sigma, stage_bytes);
+      }
     } else {
-      TRYC(cudaFuncSetAttribute(k_desc_transpose<uint32_t>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_desc_transpose<uint32_t><<<grid, 128, smem, stream>>>(
-          head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint32_t*)h->desc, eo_cnt,
-          pcs, (int)sigma);
+      const size_t smem = (size_t)4 * sigma * 33 * sizeof(double);
+      const unsigned grid = (unsigned)((pcs + 3) / 4);
+      if (h->wide) {
+        TRYC(cudaFuncSetAttribute(k_desc_transpose<uint64_t>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_desc_transpose<uint64_t><<<grid, 128, smem, stream>>>(
+            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint64_t*)h->desc, eo_cnt,
+            pcs, (int)sigma);
+      } else {
+        TRYC(cudaFuncSetAttribute(k_desc_transpose<uint32_t>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_desc_transpose<uint32_t><<<grid, 128, smem, stream>>>(
+            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint32_t*)h->desc, eo_cnt,
+            pcs, (int)sigma);
+      }
     }
     TRYC(cudaGetLastError());
   }
