@@ -625,21 +625,22 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
         head_bits, h->tile_ptr, h->row_ptr, m, pcs, (int)sigma, pos0, h->eo_ptr, h->eo);
     TRYC(cudaGetLastError());
   }
-  TRYC(cudaStreamSynchronize(stream));
   trace.mark("eo");
-  // gather locality over up to 4096 sampled tiles (drives the SpMV plan)
+  // gather locality over up to 4096 sampled tiles (drives the SpMV plan); its
+  // counter sits after the four scalars, read back with them in one sync
   h->lines_per_gather = 1.0;
+  unsigned long long lines = 0;
+  const int64_t samples = std::min<int64_t>(pcs, 4096);
   if (pcs > 0) {
-    const int64_t samples = std::min<int64_t>(pcs, 4096);
-    TRYC(cudaMemsetAsync(scal, 0, sizeof(unsigned long long), stream));
-    k_locality<<<(unsigned)((samples * 32 + 255) / 256), 256, 0, stream>>>(
-        h->col, pcs, (int)sigma, samples, reinterpret_cast<unsigned long long*>(scal));
+    auto* ctr = reinterpret_cast<unsigned long long*>(scal + 4);
+    TRYC(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), stream));
+    k_locality<<<(unsigned)((samples * 32 + 255) / 256), 256, 0, stream>>>(h->col, pcs, (int)sigma,
+                                                                         samples, ctr);
     TRYC(cudaGetLastError());
-    unsigned long long lines = 0;
-    TRYC(cudaMemcpyAsync(&lines, scal, sizeof lines, cudaMemcpyDeviceToHost, stream));
-    TRYC(cudaStreamSynchronize(stream));
-    h->lines_per_gather = (double)lines / (double)(samples * sigma);
+    TRYC(cudaMemcpyAsync(&lines, ctr, sizeof lines, cudaMemcpyDeviceToHost, stream));
   }
+  TRYC(cudaStreamSynchronize(stream));
+  if (pcs > 0) h->lines_per_gather = (double)lines / (double)(samples * sigma);
   trace.mark("locality");
 
   // ---- SpMV plan ----
