@@ -94,6 +94,7 @@ struct Handle {
   double lines_per_gather = 1.0;  // sampled x-gather locality (1 = coalesced, 32 = random)
   int x_mode = 0;                 // gather path chosen by the plan
   bool x_window = false;          // L2 persisting window on x
+  bool vr = false;                // values outside the TMA ring (k_spmv<SIG, true>)
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
   Pipeline* pipe = nullptr;  // created by the first host-vector SpMV
 };

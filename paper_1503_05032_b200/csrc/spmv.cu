@@ -186,19 +186,26 @@ __host__ __device__ constexpr int spmv_threads(int sigma) {
 // closed-segment slots per warp in shared memory (tiles rarely have more heads)
 constexpr int kClosedSlots = 128;
 constexpr int kEoSlots = 128;  // >= kClosedSlots - 1 heads of a shared-slot tile
+constexpr int kVrMaxSigma = 24;  // VR variants are instantiated up to this sigma
 
 // Outside the anonymous namespace: the sigma instantiations are reached
 // through a function-pointer switch, and the runtime must register each one.
-template <int SIG>
+// VR ("values in registers", random-gather plans, sigma <= kVrMaxSigma): the
+// ring carries only col_idx and the descriptor words; a tile's values are
+// loaded coalesced straight into registers together with its x gathers, so a
+// warp's ring is a third of the size and more of the SM's L1 stays free for
+// outstanding gather misses.
+template <int SIG, bool VR>
 __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   using W = typename std::conditional<(SIG <= 17), uint32_t, uint64_t>::type;
   constexpr int B = 32 * SIG;
   constexpr int CH = SIG <= 32 ? SIG : (SIG + 1) / 2;  // x gathers in flight per lane
+  static_assert(!VR || CH == SIG, "VR needs the whole tile's gathers in one batch");
   constexpr int CAPC = B < kClosedSlots ? B : kClosedSlots;
   constexpr uint64_t FMASK = (1ull << SIG) - 1;
-  constexpr bool EARLY_OK = SIG <= 18;  // a second x array fits in registers
-  constexpr uint32_t COL_OFF = B * 8, DESC_OFF = B * 12;
-  constexpr uint32_t TILE_BYTES = B * 12 + 32 * sizeof(W);
+  constexpr bool EARLY_OK = !VR && SIG <= 18;  // a second x array fits in registers
+  constexpr uint32_t COL_OFF = VR ? 0 : B * 8, DESC_OFF = COL_OFF + B * 4;
+  constexpr uint32_t TILE_BYTES = DESC_OFF + 32 * sizeof(W);
 
   // the calibration grid may launch now; it waits (griddepcontrol.wait) for
   // this grid to complete before reading the items
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)),
                  "r"(TILE_BYTES)
                  : "memory");
-    bulk_load(st, a.val + k * B, B * 8, bar, pol_s);
+    if (!VR) bulk_load(st, a.val + k * B, B * 8, bar, pol_s);
     bulk_load(st + COL_OFF, a.col + k * B, B * 4, bar, pol_s);
     bulk_load(st + DESC_OFF, desc + k * 32, 32 * sizeof(W), bar, pol_s);
   };
@@ -268,8 +275,15 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     // x gathers run one tile ahead: while tile k is spliced and written back,
     // the first CH gathers of tile k+1 (whose col_idx already sit in the next
     // ring stage) are in flight.
-    auto gather = [&](int st_idx, double(&xv)[CH]) {
+    // VR: the tile's values come in with its gathers (coalesced, streaming)
+    double va[VR ? CH : 1];
+    auto gather = [&](int st_idx, int64_t kt, double(&xv)[CH]) {
       const int32_t* sc = reinterpret_cast<const int32_t*>(ring + (size_t)st_idx * a.stage_bytes + COL_OFF);
+      if (VR) {
+  #pragma unroll
+        for (int u = 0; u < (VR ? CH : 0); ++u)
+          va[u] = ld_stream(a.val + kt * B + u * 32 + lane, pol_s);
+      }
       if (a.x_mode == 1) {
   #pragma unroll
         for (int u = 0; u < CH; ++u) xv[u] = ld_keep_na(a.x + sc[u * 32 + lane], pol_x);
@@ -289,7 +303,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     };
     double xa[CH];
     mbar_wait(bars, 0);
-    gather(0, xa);
+    gather(0, kb, xa);
 
     for (int64_t k = kb; k < ke; ++k) {
       const int slot = (int)((k - kb) & 31);
@@ -326,7 +340,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       double xn[CH];
       if (EARLY_OK && a.early_gather && k + 1 < ke) {
         if (!compute_only) mbar_wait(bars + sn, pn);
-        gather(sn, xn);
+        gather(sn, k + 1, xn);
       }
       const unsigned char* st = ring + (size_t)s * a.stage_bytes;
       const double* sv = reinterpret_cast<const double*>(st);
@@ -350,12 +364,17 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       // Every close at a bit flag goes to a slot: lane i's k-th flag ends the
       // segment of head yoff_i + k - 1 (k = 0: the piece continuing the column to
       // the left, "red"), stored at slot yoff_i + k (slot h + 1 = head h).  A
-      // tile whose slots fit in shared memory (the common case) runs the
-      // unrolled loop; tiles of very short rows use the per-warp global spill
-      // area through a compact loop that re-reads x (L1 hits).
+      // tile whose slots fit in shared memory (the common case) stores them
+      // there; tiles of very short rows (more heads than slots) use the
+      // per-warp global spill area.  Both use the gathered x registers.
       double sum = 0.0, red = 0.0;
-      if (fast) {
-        double* cp = closed + yoff;
+      // one unrolled loop for both slot areas: shared memory (to_smem) or the
+      // per-warp global spill area, which also keeps this lane's first close
+      // ("red") in a register
+      auto depth_loop = [&](auto to_smem) {
+        constexpr bool SM = decltype(to_smem)::value;
+        double* cp = SM ? closed + yoff : spill + yoff;
+        bool any = false;
   #pragma unroll
         for (int j0 = 0; j0 < SIG; j0 += CH) {
           double xv[CH];
@@ -372,25 +391,22 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
             const int j = j0 + u;
             if (j < SIG) {
               if ((fr >> j) & 1ull) {  // predicated: store, advance, restart
+                if (!SM) {
+                  red = any ? red : sum;
+                  any = true;
+                }
                 *cp++ = sum;
                 sum = 0.0;
               }
-              sum = fma(sv[j * 32 + lane], xv[u], sum);
+              sum = fma(VR ? va[VR ? u : 0] : sv[j * 32 + lane], xv[u], sum);
             }
           }
         }
-      } else {
-        double* sp = spill + yoff;
-  #pragma unroll 1
-        for (int j = 0; j < SIG; ++j) {
-          if ((fr >> j) & 1ull) {
-            if (sp == spill + yoff) red = sum;
-            *sp++ = sum;
-            sum = 0.0;
-          }
-          sum = fma(sv[j * 32 + lane], __ldg(a.x + sc[j * 32 + lane]), sum);
-        }
-      }
+      };
+      if (fast)
+        depth_loop(std::true_type{});
+      else
+        depth_loop(std::false_type{});
       // predicated stores on every path: the loads above are consumed here, before
       // the gathers go out, on flagged and unflagged tiles alike (a branch would
       // leave a possibly-outstanding load whose scoreboard the gathers reuse)
@@ -406,7 +422,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
         for (int u = 0; u < CH; ++u) xa[u] = xn[u];
       } else if (k + 1 < ke) {
         if (!compute_only) mbar_wait(bars + sn, pn);
-        gather(sn, xa);
+        gather(sn, k + 1, xa);
       }
       s = sn;
       phase = pn;
@@ -536,11 +552,25 @@ __global__ void k_fixup(const csr5g_partial* __restrict__ all, int world, int ra
 using SpmvFn = void (*)(SpmvArgs);
 
 // sigma is 1..48 at omega = 32 (the 64-bit descriptor limit, descriptor.cpp:22-36)
-SpmvFn spmv_fn(int sigma) {
+SpmvFn spmv_fn(int sigma, bool vr) {
+  if (vr) {
+    switch (sigma) {
+#define CSR5G_KV(S) \
+  case S:           \
+    return k_spmv<S, true>;
+      CSR5G_KV(1) CSR5G_KV(2) CSR5G_KV(3) CSR5G_KV(4) CSR5G_KV(5) CSR5G_KV(6) CSR5G_KV(7)
+      CSR5G_KV(8) CSR5G_KV(9) CSR5G_KV(10) CSR5G_KV(11) CSR5G_KV(12) CSR5G_KV(13) CSR5G_KV(14)
+      CSR5G_KV(15) CSR5G_KV(16) CSR5G_KV(17) CSR5G_KV(18) CSR5G_KV(19) CSR5G_KV(20)
+      CSR5G_KV(21) CSR5G_KV(22) CSR5G_KV(23) CSR5G_KV(24)
+#undef CSR5G_KV
+      default:
+        return nullptr;
+    }
+  }
   switch (sigma) {
 #define CSR5G_K(S) \
   case S:          \
-    return k_spmv<S>;
+    return k_spmv<S, false>;
     CSR5G_K(1) CSR5G_K(2) CSR5G_K(3) CSR5G_K(4) CSR5G_K(5) CSR5G_K(6) CSR5G_K(7) CSR5G_K(8)
     CSR5G_K(9) CSR5G_K(10) CSR5G_K(11) CSR5G_K(12) CSR5G_K(13) CSR5G_K(14) CSR5G_K(15)
     CSR5G_K(16) CSR5G_K(17) CSR5G_K(18) CSR5G_K(19) CSR5G_K(20) CSR5G_K(21) CSR5G_K(22)
@@ -572,11 +602,28 @@ int spmv_plan(Handle* h, int sms) {
   //    with <= 50% carveout, and fall to 65 / 44 G/s at a 100% carveout.
   const int sigma = (int)h->info.sigma;
   const int wbytes = h->wide ? 8 : 4;
-  const int64_t tile_bytes = h->B * 12 + 32 * wbytes;
+  const bool random = h->lines_per_gather >= 8.0;
+  // random plans with short tiles keep the values out of the ring (VR)
+  static const int vr_env = [] {
+    const char* e = std::getenv("CSR5G_VR");
+    return e ? std::atoi(e) : -1;
+  }();
+  h->vr = random && sigma <= kVrMaxSigma && vr_env != 0;
+  if (vr_env == 1 && sigma <= kVrMaxSigma) h->vr = true;
+  const int64_t tile_bytes = h->B * (h->vr ? 4 : 12) + 32 * wbytes;
   const int stage_bytes = (int)((tile_bytes + 127) / 128 * 128);
   const int closed_bytes = (int)(std::min<int64_t>(h->B, kClosedSlots) * 8);
-  const bool random = h->lines_per_gather >= 8.0;
   int budget = !random ? 226 * 1024 : 104 * 1024;
+  if (h->vr) {
+    // VR plans: a 2-stage col_idx ring is ~2-4 KB per warp, so warps are
+    // bounded by the thread cap or by how many misses the memory system
+    // absorbs: with x larger than L2 fewer warps win (R-MAT s24, x 134 MB:
+    // 6/8/10/12 warps -> 1.62/1.50/1.45/1.55 ms), with x inside L2 the most
+    // (mixed 2^23, x 67 MB: 11/12/16 warps -> 0.514/0.505/0.469 ms)
+    int l2 = 0;
+    CSR5G_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device));
+    budget = (double)h->info.n * 8.0 > 0.75 * (double)l2 ? 60 * 1024 : 72 * 1024;
+  }
   if (const char* e = std::getenv("CSR5G_BUDGET_KB")) budget = std::atoi(e) * 1024;  // experiments
   h->x_mode = random ? 1 : 4;  // random: no L1 allocation; local: plain ld.global.nc
   // No L2 persisting window on x by default: with the 2-stage random plan it
@@ -612,7 +659,7 @@ int spmv_plan(Handle* h, int sms) {
   h->stage_bytes = stage_bytes;
   h->bar_bytes = bars(nw, stages);
   h->smem_bytes = need(nw, stages);
-  CSR5G_CUDA(cudaFuncSetAttribute(spmv_fn((int)h->info.sigma),
+  CSR5G_CUDA(cudaFuncSetAttribute(spmv_fn((int)h->info.sigma, h->vr),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
   // Ask for the smallest shared-memory carveout that holds the ring: the rest
   // of the SM's 256 KB stays L1, which is where outstanding gather misses land
@@ -625,7 +672,7 @@ int spmv_plan(Handle* h, int sms) {
     const int need_bytes = h->smem_bytes + 1024;  // + the per-CTA reserved 1 KB
     int pct = (int)((100LL * need_bytes + max_smem - 1) / max_smem);
     pct = std::min(100, std::max(0, pct));
-    CSR5G_CUDA(cudaFuncSetAttribute(spmv_fn((int)h->info.sigma),
+    CSR5G_CUDA(cudaFuncSetAttribute(spmv_fn((int)h->info.sigma, h->vr),
                                     cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   }
   const int64_t max_warps = (int64_t)sms * nw;
@@ -751,7 +798,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
       cfg.attrs = attr;
       cfg.numAttrs = 1;
     }
-    CSR5G_CUDA(cudaLaunchKernelEx(&cfg, spmv_fn(a.sigma), a));
+    CSR5G_CUDA(cudaLaunchKernelEx(&cfg, spmv_fn(a.sigma, h->vr), a));
   }
   if (ev1) CSR5G_CUDA(cudaEventRecord(ev1, stream));
   if (stream_only) return CSR5G_OK;  // no items were produced
