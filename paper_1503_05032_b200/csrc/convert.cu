@@ -271,6 +271,71 @@ __global__ void k_eo(const uint32_t* __restrict__ head_bits, const uint32_t* __r
   }
 }
 
+// Per-tile SpMV work in nonzero-equivalents, for the warps' tile ranges:
+// B (stream + gathers) + w_head * heads + w_row * rows spanned (y stores,
+// empty rows zeroed).  Tiles spanning many short and empty rows cost several
+// times a tile of long rows; an equal-tile split gives the warps holding them
+// (unpermuted power-law matrices: the whole tail) most of the work.  Measured
+// on R-MAT s24 unpermuted: equal split 4.42 ms; weights (head, row) = (1,0)
+// 3.90, (0,1) 1.91, (1,1) 1.87, (4,2) 1.79 ms.
+__global__ void k_tile_work(const uint32_t* __restrict__ head_bits,
+                            const uint32_t* __restrict__ tile_ptr, int64_t pcs, int sigma,
+                            int w_head, int w_row, int64_t* __restrict__ work) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= pcs) return;
+  const uint32_t* wd = head_bits + t * sigma;  // a tile is sigma 32-bit words
+  int heads = (wd[0] & 1u) ? 0 : 1;           // bf[0] is forced
+  for (int i = 0; i < sigma; ++i) heads += __popc(wd[i]);
+  const int64_t rows = (int64_t)(tile_ptr[t + 1] & 0x7fffffffu) - (tile_ptr[t] & 0x7fffffffu) + 1;
+  work[t] = 32ll * sigma + (int64_t)w_head * heads + (int64_t)w_row * rows;
+}
+
+// Largest per-warp work of the equal-tile split (atomicMax into *out).
+__global__ void k_equal_split_max(const int64_t* __restrict__ prefix, int64_t pcs, int nw,
+                                  unsigned long long* __restrict__ out) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nw) return;
+  const int64_t b = (int64_t)w * pcs / nw, e = (int64_t)(w + 1) * pcs / nw;
+  if (e <= b) return;
+  const int64_t work = prefix[e - 1] - (b > 0 ? prefix[b - 1] : 0);
+  atomicMax(out, (unsigned long long)work);
+}
+
+// Warp tile ranges.  The equal-tile split (CSR5 tiles are equal-nnz units)
+// unless its busiest warp would carry more than 5/4 of the mean work; then
+// warp w starts at the first tile whose inclusive work prefix exceeds w/nw of
+// the total.  k_warp_bounds_fix then gives every warp at least one tile.
+__global__ void k_warp_bounds(const int64_t* __restrict__ prefix, int64_t pcs, int nw,
+                              const unsigned long long* __restrict__ equal_max,
+                              int64_t* __restrict__ begin) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w > nw) return;
+  if (w == 0 || w == nw) {
+    begin[w] = w == 0 ? 0 : pcs;
+    return;
+  }
+  const int64_t total = prefix[pcs - 1];
+  if ((double)*equal_max * nw <= 1.25 * (double)total) {
+    begin[w] = (int64_t)w * pcs / nw;
+    return;
+  }
+  const int64_t target = (int64_t)((__int128)total * w / nw);
+  int64_t lo = 0, hi = pcs;  // first t with prefix[t] > target
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (prefix[mid] <= target)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  begin[w] = lo;
+}
+
+__global__ void k_warp_bounds_fix(int64_t* __restrict__ begin, int nw) {
+  for (int w = 1; w < nw; ++w) begin[w] = max(begin[w], begin[w - 1] + 1);
+  for (int w = nw - 1; w >= 1; --w) begin[w] = min(begin[w], begin[w + 1] - 1);
+}
+
 // A few scalars of the held range, one thread: row_of_nonzero at two positions
 // and row_ptr at two rows (negative query = skip).
 __global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0, int64_t g1,
@@ -412,7 +477,7 @@ void free_handle(Handle* h) {
   free_pipeline(h->pipe);
   for (void* p : {(void*)h->row_ptr, (void*)h->tile_ptr, h->desc, (void*)h->eo_ptr, (void*)h->eo,
                   (void*)h->col, (void*)h->val, (void*)h->item_row, (void*)h->item_val,
-                  (void*)h->send, (void*)h->spill})
+                  (void*)h->send, (void*)h->spill, (void*)h->warp_begin})
     if (p) cudaFreeAsync(p, 0);
   cudaDeviceSynchronize();
   cudaSetDevice(prev);
@@ -482,8 +547,11 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   int64_t* eo_cnt = nullptr;
   int64_t* scal = nullptr;
   void* cub_tmp = nullptr;
+  void* cub_tmp2 = nullptr;
+  int64_t* work_prefix = nullptr;
   auto cleanup = [&](int code) {
-    for (void* p : {(void*)head_bits, (void*)empty_bits, (void*)eo_cnt, (void*)scal, cub_tmp})
+    for (void* p : {(void*)head_bits, (void*)empty_bits, (void*)eo_cnt, (void*)scal, cub_tmp,
+                    cub_tmp2, (void*)work_prefix})
       if (p) cudaFreeAsync(p, stream);
     if (code) free_handle(h);
     return code;
@@ -597,6 +665,31 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRY(dev_alloc(reinterpret_cast<char**>(&cub_tmp), cub_bytes, &alloc_ms, &tmp_bytes));
   TRYC(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, eo_cnt, h->eo_ptr, (int)(pcs + 1), stream));
 
+  // Work prefix for the warps' tile ranges (eo_cnt is free after its scan).
+  if (pcs > 0) {
+    static const int w_head = [] {
+      const char* e = std::getenv("CSR5G_WHEAD");
+      return e ? std::atoi(e) : 0;
+    }();
+    static const int w_row = [] {
+      const char* e = std::getenv("CSR5G_WROW");
+      return e ? std::atoi(e) : 1;
+    }();
+    k_tile_work<<<(unsigned)((pcs + 255) / 256), 256, 0, stream>>>(head_bits, h->tile_ptr, pcs,
+                                                                   (int)sigma, w_head, w_row,
+                                                                   eo_cnt);
+    TRYC(cudaGetLastError());
+    TRY(dev_alloc(&work_prefix, (size_t)pcs, &alloc_ms, &tmp_bytes));
+    size_t need = 0;
+    TRYC(cub::DeviceScan::InclusiveSum(nullptr, need, eo_cnt, work_prefix, (int)pcs, stream));
+    void* t2 = cub_tmp;
+    if (need > cub_bytes) {
+      TRY(dev_alloc(reinterpret_cast<char**>(&cub_tmp2), need, &alloc_ms, &tmp_bytes));
+      t2 = cub_tmp2;
+    }
+    TRYC(cub::DeviceScan::InclusiveSum(t2, need, eo_cnt, work_prefix, (int)pcs, stream));
+  }
+
   // Scalars of the held range.
   int64_t ptr_first = 0, ptr_close = 0, eo_total = 0;
   TRYC(cudaMemcpyAsync(&eo_total, h->eo_ptr + pcs, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
@@ -669,6 +762,19 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRY(dev_alloc(&h->item_row, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->item_val, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->spill, (size_t)std::max(h->nwarps, 1) * (B + 1), &alloc_ms, &bytes));
+  if (pcs > 0 && h->nwarps > 0) {
+    TRY(dev_alloc(&h->warp_begin, (size_t)h->nwarps + 1, &alloc_ms, &bytes));
+    auto* emax = reinterpret_cast<unsigned long long*>(scal + 6);
+    TRYC(cudaMemsetAsync(emax, 0, sizeof(unsigned long long), stream));
+    k_equal_split_max<<<(unsigned)((h->nwarps + 255) / 256), 256, 0, stream>>>(
+        work_prefix, pcs, h->nwarps, emax);
+    TRYC(cudaGetLastError());
+    k_warp_bounds<<<(unsigned)((h->nwarps + 1 + 255) / 256), 256, 0, stream>>>(
+        work_prefix, pcs, h->nwarps, emax, h->warp_begin);
+    TRYC(cudaGetLastError());
+    k_warp_bounds_fix<<<1, 1, 0, stream>>>(h->warp_begin, h->nwarps);
+    TRYC(cudaGetLastError());
+  }
   trace.mark("plan");
 
   // ---- info ----

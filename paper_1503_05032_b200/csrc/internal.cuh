@@ -42,6 +42,7 @@ struct SpmvArgs {
   double* item_val;
   csr5g_partial* send;
   double* spill;           // per-warp overflow slots for closed segment sums
+  const int64_t* warp_begin;  // warp w holds tiles [warp_begin[w], warp_begin[w+1])
   int64_t pcs;             // complete tiles held
   int64_t pos0;            // global nonzero position of local index 0
   int64_t next_row_after;  // first row after the last held complete tile's range
@@ -87,6 +88,7 @@ struct Handle {
   csr5g_partial* send = nullptr;
   csr5g_partial* send_ext = nullptr;  // caller-provided record slot
   double* spill = nullptr;            // nwarps * (B + 1) doubles
+  int64_t* warp_begin = nullptr;      // nwarps + 1 tile-range bounds, split by tile work
   int64_t next_row_after = 0, lead_rows = 0, tail_row_begin = 0, tail_pos = 0;
   int64_t first_row = 0, last_row = 0;
   bool first_owned = true, is_last = true, has_tail_item = false;

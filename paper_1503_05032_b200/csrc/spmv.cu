@@ -233,7 +233,10 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   const W* __restrict__ desc = static_cast<const W*>(a.desc);
 
   int64_t kb = 0, ke = 0;
-  if (has_tiles) {
+  if (has_tiles && a.warp_begin && !a.jitter) {
+    kb = a.warp_begin[w];
+    ke = a.warp_begin[w + 1];
+  } else if (has_tiles) {
     kb = range_begin(w, a.pcs, a.nwarps, a.jitter);
     ke = range_begin(w + 1, a.pcs, a.nwarps, a.jitter);
   }
@@ -710,6 +713,11 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.item_val = h->item_val;
   a.send = h->send_ext ? h->send_ext : h->send;
   a.spill = h->spill;
+  static const bool equal_split = [] {  // A/B: equal tile counts per warp
+    const char* e = std::getenv("CSR5G_EQUAL_SPLIT");
+    return e && std::atoi(e) != 0;
+  }();
+  a.warp_begin = equal_split ? nullptr : h->warp_begin;
   a.pcs = h->pcs;
   a.pos0 = h->t0 * h->B;
   a.next_row_after = h->next_row_after;

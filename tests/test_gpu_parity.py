@@ -258,3 +258,24 @@ def test_host_vector_paths(g, orc):
     with pytest.raises(ValueError, match="length"):
         g.spmv_host_batch(a5, [np.empty(a.n + 1)], [np.empty(a.m)])
     a5.release()
+
+
+def test_skewed_tile_work(g, orc):
+    """Tiles of long rows followed by tiles spanning thousands of short and
+    empty rows: the warps' tile ranges are split by work (k_warp_bounds), not
+    by count.  Arrays and y against the oracle, random-gather and local plans."""
+    rng = np.random.default_rng(8)
+    for n_long, n_short, n in ((2000, 300000, 50000), (300, 120000, 2000000)):
+        lens = np.concatenate([rng.integers(200, 400, n_long),
+                               rng.integers(0, 2, n_short) * rng.integers(1, 3, n_short)])
+        rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        cols = np.concatenate([np.sort(rng.choice(n, size=k, replace=False)) for k in lens])
+        a = Csr(len(lens), n, rp, cols.astype(np.int64), rng.uniform(0.5, 1.5, len(cols)))
+        x = orc.rng(4).random_x(n)
+        for sigma in (16, 32):
+            a5 = gpu_build(g, a, sigma)
+            compare_arrays(a5.export(), orc.build(a, 32, sigma), f"skew sigma={sigma}")
+            for mode in ("deterministic", "atomic"):
+                assert_y_close(gpu_y(g, a5, x, mode), orc.spmv(a, x, 32, sigma), a, x,
+                               f"skew sigma={sigma} {mode}")
+            a5.release()
