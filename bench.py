@@ -8,7 +8,8 @@ One step = one CSR5 SpMV y = A x over the whole matrix (one pass of the hot
 path).  At N=1 the workload is BASELINE config 2, the 3D 27-point stencil
 200^3 (213.8M nnz, sigma = 27 by the reference rule, 64-bit descriptors).
 Under torchrun (N>1) the matrix is tile-range sharded over the ranks with x
-replicated; a step includes the boundary-row exchange (NCCL).  Default
+replicated; a step includes the boundary-row exchange (NVLink P2P
+stores into the owner's mailbox, p2p.cu; no collective).  Default
 --scaling weak: the global matrix is N times the 1-GPU one (the stencil N
 times deeper along z, graphs log2 N scales larger: R-MAT s24 -> s27 at N=8,
 BASELINE config 5), so per-GPU work is fixed; --scaling strong shards the
@@ -600,6 +601,8 @@ def run_ours(args, workload_name, workload):
                        "desc_word_bits": info.word_bits, "mode": "deterministic",
                        "step": ("iterative: SpMV + y->x all-gather" if args.iterative else
                                 "SpMV (+ boundary exchange at N>1)"),
+                       "exchange": (os.environ.get("CSR5G_EXCHANGE", "p2p") if world > 1
+                                    else None),
                        "spmv_plan": {"lines_per_gather": round(info.lines_per_gather, 2),
                                      "warps_per_cta": info.warps_per_cta, "stages": info.stages,
                                      "smem_bytes": info.smem_bytes, "x_mode": info.x_mode,

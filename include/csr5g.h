@@ -137,6 +137,37 @@ CSR5G_API int csr5g_set_send_buffer(csr5g_matrix h, csr5g_partial *d_send);
 CSR5G_API int csr5g_fixup(csr5g_matrix h, const csr5g_partial *d_all, int32_t world, int32_t rank,
                 double *d_y, void *stream);
 
+/* NVLink P2P boundary exchange (the reference has no distributed
+ * backend).  One mailbox per rank in its own HBM, exported with a CUDA IPC
+ * handle and opened by every peer.  A shard that does not own its first row
+ * stores that row's partial straight into the owner's mailbox (dest) from
+ * its calibration kernel, then a ready flag; an owner stream-waits on the
+ * flags of its senders (the ranks sender_begin..sender_end-1 right after it
+ * whose first row is its last row), adds their partials in shard order and
+ * acknowledges.  No collective, no host sync per call.  Deterministic mode
+ * only.  Ranks that share one GPU must separate csr5g_mg_spmv_post and
+ * csr5g_mg_spmv_fixup with a host barrier (cross-process waits on one GPU
+ * are not safe); on distinct GPUs csr5g_mg_spmv does both. */
+#define CSR5G_IPC_HANDLE_BYTES 64
+#define CSR5G_MAX_WORLD 64
+typedef struct csr5g_mailbox_s *csr5g_mailbox;
+CSR5G_API int csr5g_mailbox_create(int device, int32_t world, int32_t rank, csr5g_mailbox *out);
+CSR5G_API int csr5g_mailbox_ipc_handle(csr5g_mailbox mb, void *handle_out /* 64 bytes */);
+/* map another process's mailbox (its csr5g_mailbox_ipc_handle bytes) */
+CSR5G_API int csr5g_mailbox_open_peer(csr5g_mailbox mb, int32_t peer, const void *handle /* 64 bytes */);
+/* link a mailbox of the same process (single-process emulation, tests) */
+CSR5G_API int csr5g_mailbox_link_local(csr5g_mailbox mb, int32_t peer, csr5g_mailbox peer_mb);
+/* protocol violations seen by this rank's fix-ups (0 = none; synchronous) */
+CSR5G_API int csr5g_mailbox_errors(csr5g_mailbox mb, uint32_t *errors);
+CSR5G_API int csr5g_mailbox_release(csr5g_mailbox mb);
+CSR5G_API int csr5g_mg_bind(csr5g_matrix h, csr5g_mailbox mb, int32_t dest, int32_t sender_begin,
+                            int32_t sender_end);
+CSR5G_API int csr5g_mg_spmv_post(csr5g_matrix h, const double *d_x, double *d_y, void *stream,
+                                 void *ev_tiles_begin, void *ev_tiles_end);
+CSR5G_API int csr5g_mg_spmv_fixup(csr5g_matrix h, double *d_y, void *stream);
+CSR5G_API int csr5g_mg_spmv(csr5g_matrix h, const double *d_x, double *d_y, void *stream,
+                            void *ev_tiles_begin, void *ev_tiles_end);
+
 /* format.cpp:254-265 csr5_to_csr: undo the tile transposition into the
  * caller's device buffers (col_idx int32[nnz_held], val f64[nnz_held]). */
 CSR5G_API int csr5g_to_csr(csr5g_matrix h, int32_t *d_col_idx, double *d_val, void *stream);

@@ -13,6 +13,7 @@ LIB_PATH = os.environ.get("CSR5G_LIB_OVERRIDE") or os.path.join(HERE, "libcsr5g.
 
 OK, EINVAL, ERUNTIME, ERANGE, ECUDA, ENOMEM = 0, 1, 2, 3, 4, 5
 MODE_DETERMINISTIC, MODE_ATOMIC = 0, 1
+IPC_HANDLE_BYTES, MAX_WORLD = 64, 64
 
 
 class Csr5CudaError(RuntimeError):
@@ -70,6 +71,16 @@ SIGNATURES = {
     "csr5g_shard_send_record": (C.c_int, [_vp, C.POINTER(_vp)]),
     "csr5g_set_send_buffer": (C.c_int, [_vp, _vp]),
     "csr5g_fixup": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp]),
+    "csr5g_mailbox_create": (C.c_int, [C.c_int, _i32, _i32, C.POINTER(_vp)]),
+    "csr5g_mailbox_ipc_handle": (C.c_int, [_vp, _vp]),
+    "csr5g_mailbox_open_peer": (C.c_int, [_vp, _i32, _vp]),
+    "csr5g_mailbox_link_local": (C.c_int, [_vp, _i32, _vp]),
+    "csr5g_mailbox_errors": (C.c_int, [_vp, C.POINTER(C.c_uint32)]),
+    "csr5g_mailbox_release": (C.c_int, [_vp]),
+    "csr5g_mg_bind": (C.c_int, [_vp, _vp, _i32, _i32, _i32]),
+    "csr5g_mg_spmv_post": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "csr5g_mg_spmv_fixup": (C.c_int, [_vp, _vp, _vp]),
+    "csr5g_mg_spmv": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "csr5g_to_csr": (C.c_int, [_vp, _vp, _vp, _vp]),
     "csr5g_release": (C.c_int, [_vp]),
     "csr5g_build_host": (C.c_int, [C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, C.POINTER(Params),

@@ -475,6 +475,7 @@ void free_handle(Handle* h) {
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
   free_pipeline(h->pipe);
+  free_binding(h->mg);
   for (void* p : {(void*)h->row_ptr, (void*)h->tile_ptr, h->desc, (void*)h->eo_ptr, (void*)h->eo,
                   (void*)h->col, (void*)h->val, (void*)h->item_row, (void*)h->item_val,
                   (void*)h->send, (void*)h->spill, (void*)h->warp_begin})

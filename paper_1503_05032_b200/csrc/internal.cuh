@@ -70,6 +70,7 @@ struct SpmvArgs {
 };
 
 struct Pipeline;  // pipeline.cu: host-vector copy/compute pipeline
+struct Binding;   // p2p.cu: a shard's NVLink boundary exchange
 
 struct Handle {
   int device = 0;
@@ -87,6 +88,9 @@ struct Handle {
   double* item_val = nullptr;
   csr5g_partial* send = nullptr;
   csr5g_partial* send_ext = nullptr;  // caller-provided record slot
+  uint32_t* send_flag = nullptr;      // p2p.cu: owner's ready flag for this shard's record
+  uint32_t send_epoch = 0;            // value stored into send_flag by the current call
+  Binding* mg = nullptr;              // p2p.cu: NVLink boundary exchange of this shard
   double* spill = nullptr;            // nwarps * (B + 1) doubles
   int64_t* warp_begin = nullptr;      // nwarps + 1 tile-range bounds, split by tile work
   int64_t next_row_after = 0, lead_rows = 0, tail_row_begin = 0, tail_pos = 0;
@@ -127,6 +131,7 @@ int spmv_plan(Handle* h, int sms);
 int spmv_host_batch(Handle* h, const double* const* xs, double* const* ys, int64_t count,
                     int mode, cudaStream_t stream);
 void free_pipeline(Pipeline* p);
+void free_binding(Binding* b);
 int csr_spmv(int device, int kernel, int64_t m, int64_t n, int64_t nnz, const int64_t* rp,
              const int32_t* col, const double* val, const double* x, double* y,
              cudaStream_t stream);

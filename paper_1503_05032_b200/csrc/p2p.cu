@@ -1,0 +1,322 @@
+// p2p.cu -- NVLink P2P boundary exchange of the multi-GPU driver.
+//
+// The reference has no distributed backend; this is the shard fix-up the
+// north star names: "fixes up the one or two boundary rows per shard with
+// NVLink P2P adds".  A row whose nonzeros straddle a shard edge gets one
+// partial from every shard it touches; its owner is the shard holding its
+// first nonzero (mg.py).  Shard r sends at most one partial (its first row,
+// when it does not own it) to one static destination, and receives partials
+// from a contiguous range of later shards (a row can span whole shards).
+//
+// Every rank owns one mailbox in its own HBM (cudaMalloc, exported with a CUDA
+// IPC handle, opened by every peer with peer access over NVLink):
+//   slot[g]  csr5g_partial  the record shard g stored here (remote store)
+//   ready[g] u32            epoch of the call that stored slot[g]
+//   ack      u32            epoch of the last call whose record the destination consumed
+//   err      u32            protocol violations seen by k_fixup_p2p (tests read it)
+// Per call (epoch e, host counter, one per binding):
+//   sender r:  stream-wait ack >= e-1 (the owner consumed the previous record;
+//              single-buffered slot), then the SpMV; k_calibrate stores the
+//              record into dest's slot[r], fences at system scope and stores
+//              ready[r] = e with release semantics (spmv.cu write_run).
+//   owner o:   stream-wait ready[g] >= e for every sender g (cuStreamWaitValue32
+//              on LOCAL memory: the front end waits, no SM spins), then
+//              k_fixup_p2p adds the partials to y[last_row] in shard order
+//              (deterministic) and stores ack = e into every sender's mailbox.
+// No collective and no host synchronisation per call; the transfers are one
+// 16-byte store plus one flag each way per shard edge.  Ranks sharing one GPU
+// (functional tests) must not rely on stream waits across processes: mg.py
+// then separates the two phases with a host barrier, so every wait is already
+// satisfied when it is enqueued (B200_PROFILING: no cross-rank waits on one GPU).
+#include <cuda.h>
+
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+namespace csr5g {
+
+constexpr int kMaxWorld = 64;
+
+struct MailboxDev {
+  csr5g_partial slot[kMaxWorld];
+  uint32_t ready[kMaxWorld];
+  uint32_t ack;
+  uint32_t err;
+};
+
+struct Mailbox {
+  int device = 0, world = 0, rank = 0;
+  MailboxDev* local = nullptr;            // this rank's mailbox (own HBM)
+  MailboxDev* peer[kMaxWorld] = {};       // every rank's mailbox, mapped here
+  bool ipc_opened[kMaxWorld] = {};
+  uint32_t** d_peer_ack = nullptr;        // device table: &peer[g]->ack
+};
+
+struct Binding {
+  Mailbox* mb = nullptr;
+  int dest = -1, sb = 0, se = 0;
+  uint32_t epoch = 0;
+};
+
+void free_binding(Binding* b) { delete b; }
+
+namespace {
+
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+int wait_value_fn(WaitValueFn* out) {
+  static WaitValueFn fn = nullptr;
+  static cudaError_t rc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    cudaError_t e = cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &p, 12000,
+                                                     cudaEnableDefault, &q);
+    if (e == cudaSuccess && q != cudaDriverEntryPointSuccess) e = cudaErrorNotSupported;
+    fn = reinterpret_cast<WaitValueFn>(p);
+    return e;
+  }();
+  if (rc != cudaSuccess) return cuda_fail(rc, "cudaGetDriverEntryPoint(cuStreamWaitValue32)");
+  *out = fn;
+  return CSR5G_OK;
+}
+
+int stream_wait_geq(cudaStream_t s, const uint32_t* addr, uint32_t value) {
+  WaitValueFn fn = nullptr;
+  if (int rc = wait_value_fn(&fn)) return rc;
+  const CUresult r = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), value,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS)
+    return fail(CSR5G_ECUDA, "cuStreamWaitValue32 failed (CUresult " + std::to_string((int)r) + ")");
+  return CSR5G_OK;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One thread: y[row] += partials of senders [sb, se) in shard order, then ack.
+__global__ void k_fixup_p2p(MailboxDev* mb, uint32_t* const* peer_ack, int sb, int se,
+                            int64_t row, double* __restrict__ y, uint32_t epoch) {
+  double acc = y[row];
+  for (int g = sb; g < se; ++g) {
+    if (ld_acquire_sys(&mb->ready[g]) != epoch) atomicOr(&mb->err, 1u);
+    const volatile csr5g_partial* r = &mb->slot[g];
+    if (r->row != row) atomicOr(&mb->err, 2u);
+    else acc += r->value;
+  }
+  y[row] = acc;
+  __threadfence_system();
+  for (int g = sb; g < se; ++g) st_release_sys(peer_ack[g], epoch);
+}
+
+}  // namespace
+
+int mg_post(Handle* h, const double* d_x, double* d_y, cudaStream_t stream, cudaEvent_t ev0,
+            cudaEvent_t ev1) {
+  Binding* b = h->mg;
+  if (!b) return fail(CSR5G_EINVAL, "csr5g: shard is not bound to a mailbox (csr5g_mg_bind)");
+  CSR5G_CUDA(cudaSetDevice(h->device));
+  ++b->epoch;
+  csr5g_partial* const saved = h->send_ext;
+  if (b->dest >= 0) {
+    if (int rc = stream_wait_geq(stream, &b->mb->local->ack, b->epoch - 1)) return rc;
+    h->send_ext = &b->mb->peer[b->dest]->slot[b->mb->rank];
+    h->send_flag = &b->mb->peer[b->dest]->ready[b->mb->rank];
+  } else {
+    h->send_ext = nullptr;
+    h->send_flag = nullptr;
+  }
+  h->send_epoch = b->epoch;
+  const int rc = launch_spmv(h, d_x, d_y, CSR5G_MODE_DETERMINISTIC, stream, ev0, ev1);
+  h->send_ext = saved;
+  h->send_flag = nullptr;
+  return rc;
+}
+
+int mg_fixup(Handle* h, double* d_y, cudaStream_t stream) {
+  Binding* b = h->mg;
+  if (!b) return fail(CSR5G_EINVAL, "csr5g: shard is not bound to a mailbox (csr5g_mg_bind)");
+  if (b->se <= b->sb) return CSR5G_OK;
+  CSR5G_CUDA(cudaSetDevice(h->device));
+  for (int g = b->sb; g < b->se; ++g)
+    if (int rc = stream_wait_geq(stream, &b->mb->local->ready[g], b->epoch)) return rc;
+  k_fixup_p2p<<<1, 1, 0, stream>>>(b->mb->local, b->mb->d_peer_ack, b->sb, b->se, h->last_row,
+                                   d_y, b->epoch);
+  CSR5G_CUDA(cudaGetLastError());
+  return CSR5G_OK;
+}
+
+}  // namespace csr5g
+
+using namespace csr5g;
+
+struct csr5g_mailbox_s {
+  Mailbox* m;
+};
+
+struct csr5g_matrix_s {
+  Handle* h;
+};
+
+namespace {
+
+int refresh_peer_table(Mailbox* m) {
+  uint32_t* acks[kMaxWorld] = {};
+  for (int g = 0; g < m->world; ++g) acks[g] = m->peer[g] ? &m->peer[g]->ack : nullptr;
+  CSR5G_CUDA(cudaMemcpy(m->d_peer_ack, acks, sizeof(uint32_t*) * m->world, cudaMemcpyHostToDevice));
+  return CSR5G_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int csr5g_mailbox_create(int device, int32_t world, int32_t rank, csr5g_mailbox* out) {
+  if (!out) return fail(CSR5G_EINVAL, "csr5g: out is NULL");
+  *out = nullptr;
+  if (world < 1 || world > kMaxWorld)
+    return fail(CSR5G_EINVAL, "csr5g: world must be in [1, " + std::to_string(kMaxWorld) + "]");
+  if (rank < 0 || rank >= world) return fail(CSR5G_EINVAL, "csr5g: rank outside [0, world)");
+  CSR5G_CUDA(cudaSetDevice(device));
+  auto* m = new Mailbox;
+  m->device = device;
+  m->world = world;
+  m->rank = rank;
+  cudaError_t e = cudaMalloc(&m->local, sizeof(MailboxDev));
+  if (e == cudaSuccess) e = cudaMemset(m->local, 0, sizeof(MailboxDev));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_peer_ack, sizeof(uint32_t*) * kMaxWorld);
+  if (e != cudaSuccess) {
+    cudaFree(m->local);
+    delete m;
+    return cuda_fail(e, "csr5g_mailbox_create");
+  }
+  // every slot starts as "no record" (row -1)
+  csr5g_partial none[kMaxWorld];
+  for (auto& r : none) r = csr5g_partial{-1, 0.0};
+  CSR5G_CUDA(cudaMemcpy(m->local->slot, none, sizeof none, cudaMemcpyHostToDevice));
+  m->peer[rank] = m->local;
+  if (int rc = refresh_peer_table(m)) return rc;
+  *out = new csr5g_mailbox_s{m};
+  return CSR5G_OK;
+}
+
+int csr5g_mailbox_ipc_handle(csr5g_mailbox mb, void* handle64) {
+  if (!mb || !handle64) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == CSR5G_IPC_HANDLE_BYTES, "IPC handle size");
+  CSR5G_CUDA(cudaSetDevice(mb->m->device));
+  cudaIpcMemHandle_t hd;
+  CSR5G_CUDA(cudaIpcGetMemHandle(&hd, mb->m->local));
+  std::memcpy(handle64, &hd, sizeof hd);
+  return CSR5G_OK;
+}
+
+int csr5g_mailbox_open_peer(csr5g_mailbox mb, int32_t peer, const void* handle64) {
+  if (!mb || !handle64) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  Mailbox* m = mb->m;
+  if (peer < 0 || peer >= m->world || peer == m->rank)
+    return fail(CSR5G_EINVAL, "csr5g: peer must be another rank in [0, world)");
+  if (m->peer[peer]) return fail(CSR5G_EINVAL, "csr5g: peer mailbox already linked");
+  CSR5G_CUDA(cudaSetDevice(m->device));
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle64, sizeof hd);
+  void* p = nullptr;
+  CSR5G_CUDA(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+  m->peer[peer] = static_cast<MailboxDev*>(p);
+  m->ipc_opened[peer] = true;
+  return refresh_peer_table(m);
+}
+
+int csr5g_mailbox_link_local(csr5g_mailbox mb, int32_t peer, csr5g_mailbox peer_mb) {
+  if (!mb || !peer_mb) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  Mailbox* m = mb->m;
+  if (peer < 0 || peer >= m->world || peer == m->rank || peer_mb->m->rank != peer)
+    return fail(CSR5G_EINVAL, "csr5g: peer must be another rank in [0, world)");
+  if (m->peer[peer]) return fail(CSR5G_EINVAL, "csr5g: peer mailbox already linked");
+  if (peer_mb->m->device != m->device) {
+    int ok = 0;
+    CSR5G_CUDA(cudaDeviceCanAccessPeer(&ok, m->device, peer_mb->m->device));
+    if (!ok) return fail(CSR5G_ECUDA, "csr5g: no peer access between the two devices");
+    CSR5G_CUDA(cudaSetDevice(m->device));
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer_mb->m->device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+      return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    cudaGetLastError();
+  }
+  m->peer[peer] = peer_mb->m->local;
+  CSR5G_CUDA(cudaSetDevice(m->device));
+  return refresh_peer_table(m);
+}
+
+int csr5g_mailbox_errors(csr5g_mailbox mb, uint32_t* errors) {
+  if (!mb || !errors) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  CSR5G_CUDA(cudaSetDevice(mb->m->device));
+  CSR5G_CUDA(cudaMemcpy(errors, &mb->m->local->err, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return CSR5G_OK;
+}
+
+int csr5g_mailbox_release(csr5g_mailbox mb) {
+  if (!mb) return CSR5G_OK;
+  Mailbox* m = mb->m;
+  cudaSetDevice(m->device);
+  cudaDeviceSynchronize();
+  for (int g = 0; g < m->world; ++g)
+    if (m->ipc_opened[g]) cudaIpcCloseMemHandle(m->peer[g]);
+  cudaFree(m->d_peer_ack);
+  cudaFree(m->local);
+  delete m;
+  delete mb;
+  return CSR5G_OK;
+}
+
+int csr5g_mg_bind(csr5g_matrix h, csr5g_mailbox mb, int32_t dest, int32_t sender_begin,
+                  int32_t sender_end) {
+  if (!h || !mb) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  Handle* hh = h->h;
+  Mailbox* m = mb->m;
+  if (hh->device != m->device) return fail(CSR5G_EINVAL, "csr5g: mailbox is on another device");
+  const bool first_owned = hh->first_owned || hh->pcs == 0;
+  if ((dest >= 0) == first_owned)
+    return fail(CSR5G_EINVAL, first_owned ? "csr5g: shard owns its first row; dest must be -1"
+                                          : "csr5g: shard does not own its first row; dest required");
+  if (dest >= m->rank) return fail(CSR5G_EINVAL, "csr5g: dest must be an earlier rank");
+  if (sender_end > sender_begin &&
+      (sender_begin != m->rank + 1 || sender_end > m->world || hh->is_last))
+    return fail(CSR5G_EINVAL, "csr5g: senders must be the ranks right after this one");
+  for (int g = sender_begin; g < sender_end; ++g)
+    if (!m->peer[g]) return fail(CSR5G_EINVAL, "csr5g: sender mailbox not linked");
+  if (dest >= 0 && !m->peer[dest]) return fail(CSR5G_EINVAL, "csr5g: dest mailbox not linked");
+  if (!hh->mg) hh->mg = new Binding;
+  hh->mg->mb = m;
+  hh->mg->dest = dest;
+  hh->mg->sb = sender_begin;
+  hh->mg->se = std::max(sender_begin, sender_end);
+  return CSR5G_OK;
+}
+
+int csr5g_mg_spmv_post(csr5g_matrix h, const double* d_x, double* d_y, void* stream, void* ev0,
+                       void* ev1) {
+  if (!h || !d_y || (!d_x && h->h->info.n > 0)) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  return mg_post(h->h, d_x, d_y, static_cast<cudaStream_t>(stream),
+                 static_cast<cudaEvent_t>(ev0), static_cast<cudaEvent_t>(ev1));
+}
+
+int csr5g_mg_spmv_fixup(csr5g_matrix h, double* d_y, void* stream) {
+  if (!h || !d_y) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  return mg_fixup(h->h, d_y, static_cast<cudaStream_t>(stream));
+}
+
+int csr5g_mg_spmv(csr5g_matrix h, const double* d_x, double* d_y, void* stream, void* ev0,
+                  void* ev1) {
+  if (int rc = csr5g_mg_spmv_post(h, d_x, d_y, stream, ev0, ev1)) return rc;
+  return csr5g_mg_spmv_fixup(h, d_y, stream);
+}
+
+}  // extern "C"

@@ -100,11 +100,19 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
   return ((uint64_t)hi << 32) | lo;
 }
 
+// The send record goes to local memory (collective exchange) or straight into
+// the owner rank's mailbox over NVLink (p2p.cu), followed there by its ready
+// flag: value stores, system-scope fence, then the flag store with release.
 __device__ __forceinline__ void write_run(int64_t row, double v, double* y, int64_t first_row,
-                                          int first_owned, csr5g_partial* send) {
+                                          int first_owned, csr5g_partial* send, uint32_t* flag,
+                                          uint32_t epoch) {
   if (!first_owned && row == first_row) {
     send->row = row;
     send->value = v;
+    if (flag) {
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+    }
   } else {
     y[row] = v;
   }
@@ -117,7 +125,7 @@ __device__ __forceinline__ void write_run(int64_t row, double v, double* y, int6
 __device__ void calibrate_window(const int64_t* __restrict__ item_row,
                                  const double* __restrict__ item_val, int64_t N, int64_t base,
                                  double* __restrict__ y, int64_t first_row, int first_owned,
-                                 csr5g_partial* send) {
+                                 csr5g_partial* send, uint32_t* flag, uint32_t epoch) {
   const int lane = threadIdx.x & 31;
   if (base == 0 && lane == 0) {
     send->row = -1;
@@ -147,7 +155,7 @@ __device__ void calibrate_window(const int64_t* __restrict__ item_row,
     rk = __shfl_sync(kFull, key, ls);
     cont = (base + 32 < N) && __ldcg(item_row + base + 32) == rk;
   }
-  if (start && !(cont && lane == ls)) write_run(key, v, y, first_row, first_owned, send);
+  if (start && !(cont && lane == ls)) write_run(key, v, y, first_row, first_owned, send, flag, epoch);
   if (cont) {
     double total = __shfl_sync(kFull, v, ls);
     for (int64_t pos = base + 32;; pos += 32) {
@@ -160,20 +168,21 @@ __device__ void calibrate_window(const int64_t* __restrict__ item_row,
       total += s;
       if (mm != kFull) break;
     }
-    if (lane == 0) write_run(rk, total, y, first_row, first_owned, send);
+    if (lane == 0) write_run(rk, total, y, first_row, first_owned, send, flag, epoch);
   }
 }
 
 __global__ void k_calibrate(const int64_t* __restrict__ item_row,
                             const double* __restrict__ item_val, int64_t N, double* __restrict__ y,
-                            int64_t first_row, int first_owned, csr5g_partial* send) {
+                            int64_t first_row, int first_owned, csr5g_partial* send,
+                            uint32_t* flag, uint32_t epoch) {
   // launched as a programmatic dependent of k_spmv: its launch overlaps the
   // SpMV; the items are read only once that grid has completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane;
   if (base >= N) return;
-  calibrate_window(item_row, item_val, N, base, y, first_row, first_owned, send);
+  calibrate_window(item_row, item_val, N, base, y, first_row, first_owned, send, flag, epoch);
 }
 
 }  // namespace
@@ -822,7 +831,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     cfg.numAttrs = pdl_on ? 1 : 0;
     CSR5G_CUDA(cudaLaunchKernelEx(&cfg, k_calibrate, (const int64_t*)h->item_row,
                                   (const double*)h->item_val, items, d_y, h->first_row,
-                                  (int)h->first_owned, a.send));
+                                  (int)h->first_owned, a.send, h->send_flag, h->send_epoch));
   } else if (!atomic) {
     const csr5g_partial none{-1, 0.0};
     CSR5G_CUDA(cudaMemcpyAsync(a.send, &none, sizeof none, cudaMemcpyHostToDevice, stream));

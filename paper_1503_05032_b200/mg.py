@@ -9,25 +9,34 @@ of the single-device arrays (bit for bit).  x is replicated.
 Per SpMV there is one real exchange step: a row whose nonzeros straddle a
 shard edge gets a partial sum from each shard.  The row's owner is the shard
 holding its first nonzero.  Each shard has at most one partial to send (its
-first row, when it does not own it); the driver all-gathers the 16-byte
-records and every owner adds the partials of later shards in shard order
-(csr5g_fixup) -- deterministic.  In the iterative mode (y -> x, square A) the
-owned row ranges of y are all-gathered (one NCCL all-gather, ranges padded to
-the longest) into every rank's x.
+first row, when it does not own it), to a destination fixed by the matrix
+structure (plan_exchange).  The default exchange is NVLink P2P (p2p.cu):
+the shard's calibration kernel stores the 16-byte partial straight into the
+owner's mailbox and raises a flag; the owner's stream waits on the flags of
+its senders, adds their partials in shard order (deterministic) and
+acknowledges -- no collective, no host sync.  CSR5G_EXCHANGE=collective
+selects the earlier form (all-gather of every shard's record, csr5g_fixup).
+In the iterative mode (y -> x, square A) the owned row ranges of y are
+all-gathered (one NCCL all-gather, ranges padded to the longest) into every
+rank's x.
 
 The reference has no distributed backend; this is new ("Multi-GPU
-driver").  Host logic is covered by world_size-2 gloo tests on CPU
+driver").  Host logic is covered by world_size-2/3 gloo tests on CPU
 (tests/test_mg_gloo.py); the CUDA calls are exercised shard by shard on one
-device (emulate_shards_on_one_device).
+device (emulate_shards_on_one_device, mailboxes linked in one process) and by
+several ranks sharing one GPU (tests/test_gpu_multirank.py; the two phases
+then separated by host barriers, since ranks on one GPU must never wait on
+each other inside the stream).
 """
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import check, lib
+from ._lib import IPC_HANDLE_BYTES, check, lib
 
 
 def plan_tiles(pc: int, world: int) -> list[tuple[int, int]]:
@@ -66,6 +75,33 @@ def shard_view(nnz: int, sigma: int, rank: int, world: int) -> ShardView | None:
 def owned_ranges(infos) -> list[tuple[int, int]]:
     """Rows each shard writes in y (contiguous, covering [0, m))."""
     return [(int(i.own_row_begin), int(i.own_row_end)) for i in infos]
+
+
+def plan_exchange(firsts, owns):
+    """Static routing of the boundary partials (host logic, shared with the
+    gloo tests).
+
+    firsts[g] = (first_row, first_owned) of shard g, owns[g] = its owned row
+    range [lo, hi) (empty for a shard lying inside one row).  Returns
+    dest[g] (the rank owning shard g's first row, -1 when g owns it) and
+    senders[g] = (sb, se): the later ranks whose partial g receives, always the
+    contiguous block right after g."""
+    w = len(firsts)
+    dest = [-1] * w
+    for g, (row, owned) in enumerate(firsts):
+        if owned:
+            continue
+        hits = [o for o in range(g) if owns[o][0] <= row < owns[o][1]]
+        if len(hits) != 1:
+            raise RuntimeError(f"shard {g}: row {row} has {len(hits)} owners among {owns[:g]}")
+        dest[g] = hits[0]
+    senders = []
+    for g in range(w):
+        src = [s for s in range(w) if dest[s] == g]
+        if src and src != list(range(g + 1, g + 1 + len(src))):
+            raise RuntimeError(f"shard {g}: senders {src} are not the ranks right after it")
+        senders.append((g + 1, g + 1 + len(src)) if src else (0, 0))
+    return dest, senders
 
 
 def _staged(dist, group=None) -> bool:
@@ -131,11 +167,73 @@ class Csr5Sharded:
         self.table = torch.zeros(2 * world, dtype=torch.int64, device=dev)
         if self.active:
             check(lib().csr5g_set_send_buffer(self.a5.handle, C.c_void_p(self.send.data_ptr())))
-        own = torch.tensor([self.own[0], self.own[1]], dtype=torch.int64, device=dev)
-        allown = torch.zeros(2 * world, dtype=torch.int64, device=dev)
+        first = (self.a5.info.first_row, int(rank == 0 or self.own[0] == self.a5.info.first_row)) \
+            if self.active else (m, 1)
+        own = torch.tensor([self.own[0], self.own[1], first[0], first[1]], dtype=torch.int64,
+                           device=dev)
+        allown = torch.zeros(4 * world, dtype=torch.int64, device=dev)
         all_gather_flat(dist, allown, own, group)
         t = allown.cpu().tolist()
-        self.ranges = [(t[2 * g], t[2 * g + 1]) for g in range(world)]
+        self.ranges = [(t[4 * g], t[4 * g + 1]) for g in range(world)]
+        self.exchange = os.environ.get("CSR5G_EXCHANGE", "p2p")
+        self.mailbox = None
+        if self.exchange == "p2p":
+            w = self.world_eff
+            firsts = [(t[4 * g + 2], t[4 * g + 3]) for g in range(w)]
+            self.dest, self.senders = plan_exchange(firsts, self.ranges[:w])
+            self._connect(dev)
+        elif self.exchange != "collective":
+            raise ValueError(f"CSR5G_EXCHANGE={self.exchange}: expected p2p or collective")
+
+    def _connect(self, dev):
+        """Mailbox per rank; IPC handles all-gathered once; each rank maps the
+        mailboxes it stores into (dest) and acknowledges (senders)."""
+        torch, dist = self.torch, self.dist
+        L = lib()
+        mb = C.c_void_p()
+        check(L.csr5g_mailbox_create(dev.index or 0, self.world, self.rank, C.byref(mb)))
+        self.mailbox = mb
+        hbuf = (C.c_uint8 * IPC_HANDLE_BYTES)()
+        check(L.csr5g_mailbox_ipc_handle(mb, hbuf))
+        mine = torch.tensor(list(hbuf), dtype=torch.uint8, device=dev)
+        allh = torch.zeros(IPC_HANDLE_BYTES * self.world, dtype=torch.uint8, device=dev)
+        all_gather_flat(dist, allh, mine, self.group)
+        allh = allh.cpu().numpy()
+        # ranks sharing one GPU must not wait on each other inside a stream:
+        # spmv() then separates post and fix-up with host barriers
+        uid = torch.tensor(list(torch.cuda.get_device_properties(dev).uuid.bytes), dtype=torch.uint8,
+                           device=dev)
+        allu = torch.zeros(16 * self.world, dtype=torch.uint8, device=dev)
+        all_gather_flat(dist, allu, uid, self.group)
+        allu = allu.cpu().numpy().reshape(self.world, 16)
+        self.shared_gpu = len({bytes(u) for u in allu}) < self.world
+        if not self.active:
+            return
+        d = self.dest[self.rank]
+        sb, se = self.senders[self.rank]
+        for peer in sorted(set(([d] if d >= 0 else []) + list(range(sb, se)))):
+            h = allh[IPC_HANDLE_BYTES * peer:IPC_HANDLE_BYTES * (peer + 1)]
+            check(L.csr5g_mailbox_open_peer(mb, peer, (C.c_uint8 * IPC_HANDLE_BYTES)(*h.tolist())))
+        check(L.csr5g_mg_bind(self.a5.handle, mb, d, sb, se))
+
+    def mailbox_errors(self) -> int:
+        """Protocol violations seen by this rank's fix-ups (synchronous)."""
+        if self.mailbox is None:
+            return 0
+        e = C.c_uint32()
+        check(lib().csr5g_mailbox_errors(self.mailbox, C.byref(e)))
+        return e.value
+
+    def close(self):
+        if self.mailbox is not None:
+            self.torch.cuda.synchronize()
+            if self.shared_gpu:  # no rank unmaps a mailbox a peer still writes into
+                self.dist.barrier(group=self.group)
+            if self.a5 is not None:
+                self.a5.release()
+                self.a5 = None
+            check(lib().csr5g_mailbox_release(self.mailbox))
+            self.mailbox = None
 
     @staticmethod
     def slices_for(nnz: int, sigma: int, rank: int, world: int):
@@ -147,6 +245,8 @@ class Csr5Sharded:
         (csr5.Event pair) brackets this rank's tile kernel."""
         from .csr5 import spmv_csr5, spmv_csr5_evt
         torch = self.torch
+        if self.exchange == "p2p":
+            return self._spmv_p2p(x, y, events)
         if self.active and events is not None:
             spmv_csr5_evt(self.a5, x, y, events[0], events[1])
         elif self.active:
@@ -158,6 +258,26 @@ class Csr5Sharded:
             check(lib().csr5g_fixup(self.a5.handle, C.c_void_p(self.table.data_ptr()),
                                     self.world_eff, self.rank, C.c_void_p(y.data_ptr()),
                                     C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return y
+
+    def _spmv_p2p(self, x, y, events):
+        torch, L = self.torch, lib()
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        ev = (events[0].p, events[1].p) if events is not None else (None, None)
+        xp, yp = C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr())
+        if not self.shared_gpu:
+            if self.active:
+                check(L.csr5g_mg_spmv(self.a5.handle, xp, yp, stream, ev[0], ev[1]))
+            return y
+        # ranks on one GPU: every wait is satisfied before it is enqueued
+        if self.active:
+            check(L.csr5g_mg_spmv_post(self.a5.handle, xp, yp, stream, ev[0], ev[1]))
+        torch.cuda.current_stream().synchronize()
+        self.dist.barrier(group=self.group)
+        if self.active:
+            check(L.csr5g_mg_spmv_fixup(self.a5.handle, yp, stream))
+        torch.cuda.current_stream().synchronize()
+        self.dist.barrier(group=self.group)
         return y
 
     def gather_y_into_x(self, y, x):
@@ -242,3 +362,58 @@ def emulate_shards_on_one_device(a, x: np.ndarray, sigma: int, world: int) -> np
     for (l0, h0), (l1, h1) in zip(ranges, ranges[1:]):
         assert h0 == l1, ranges
     return y.cpu().numpy()
+
+
+def emulate_p2p_on_one_device(a, xs, sigma: int, world: int):
+    """The P2P exchange (p2p.cu) with every shard in this process on one
+    device: mailboxes linked directly, one stream, all posts of a call before
+    its fix-ups (so every stream wait is already satisfied -- no shard ever
+    waits on another).  xs: list of x vectors, one SpMV call each (epochs
+    advance, acks recycle the slots).  Returns [y per call], mailbox errors."""
+    import torch
+
+    L = lib()
+    shards = _shards_on_device(a, sigma, world)
+    w = len(shards)
+    infos = [s.info for s in shards]
+    owns = [(i.own_row_begin, i.own_row_end) for i in infos]
+    firsts = [(i.first_row, int(g == 0 or i.own_row_begin == i.first_row))
+              for g, i in enumerate(infos)]
+    dest, senders = plan_exchange(firsts, owns)
+    boxes = []
+    for g in range(w):
+        mb = C.c_void_p()
+        check(L.csr5g_mailbox_create(torch.cuda.current_device(), w, g, C.byref(mb)))
+        boxes.append(mb)
+    try:
+        for g in range(w):
+            peers = set(([dest[g]] if dest[g] >= 0 else []) + list(range(*senders[g])))
+            for p in sorted(peers):
+                check(L.csr5g_mailbox_link_local(boxes[g], p, boxes[p]))
+            check(L.csr5g_mg_bind(shards[g].handle, boxes[g], dest[g], *senders[g]))
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        outs = []
+        for x in xs:
+            xd = torch.as_tensor(np.ascontiguousarray(x, np.float64)).cuda()
+            ys = [torch.full((a.m,), float("nan"), dtype=torch.float64, device="cuda")
+                  for _ in range(w)]
+            for g in reversed(range(w)):  # senders post before their owners
+                check(L.csr5g_mg_spmv_post(shards[g].handle, C.c_void_p(xd.data_ptr()),
+                                           C.c_void_p(ys[g].data_ptr()), stream, None, None))
+            for g in range(w):
+                check(L.csr5g_mg_spmv_fixup(shards[g].handle, C.c_void_p(ys[g].data_ptr()), stream))
+            y = torch.full((a.m,), float("nan"), dtype=torch.float64, device="cuda")
+            for g, (lo, hi) in enumerate(owns):
+                y[lo:hi] = ys[g][lo:hi]
+            outs.append(y.cpu().numpy())
+        errs = []
+        for mb in boxes:
+            e = C.c_uint32()
+            check(L.csr5g_mailbox_errors(mb, C.byref(e)))
+            errs.append(e.value)
+        return outs, errs, dest, senders
+    finally:
+        for s in shards:
+            s.release()
+        for mb in boxes:
+            L.csr5g_mailbox_release(mb)

@@ -229,6 +229,30 @@ def test_shards_concatenate_and_fix_up(g, orc):
             assert np.array_equal(tp, full.tile_ptr)
 
 
+def test_p2p_exchange_on_one_device(g, orc):
+    """The NVLink P2P boundary exchange (p2p.cu) with all shards in one process:
+    partials stored into the owners' mailboxes by the calibration kernel,
+    flags/acks over several calls (epochs), y equal to the collective form and
+    within tolerance of the oracle, no protocol errors."""
+    from paper_1503_05032_b200 import mg
+    rng = orc.rng(9)
+    cases = [orc.generate_synthetic(1, 300, 30000, 60000, 3, 0.5),  # one row spans shards
+             orc.generate_synthetic(2, 5000, 4000, 120000, 4),
+             orc.generate_synthetic(0, 2000, 2000, 54000, 5)]
+    for a in cases:
+        sigma = orc.select_sigma(a.nnz / a.m)
+        xs = [rng.random_x(a.n) for _ in range(3)]
+        for world in (2, 3, 8):
+            ys, errs, dest, senders = mg.emulate_p2p_on_one_device(a, xs, sigma, world)
+            assert errs == [0] * len(errs), (world, errs)
+            for x, y in zip(xs, ys):
+                assert_y_close(y, orc.spmv(a, x, 32, sigma), a, x, f"p2p world={world}")
+                y_coll = mg.emulate_shards_on_one_device(a, x, sigma, world)
+                assert np.array_equal(y, y_coll), f"p2p != collective, world={world}"
+        if a.m == 300:  # the long row: one owner receives from several shards
+            assert max(se - sb for sb, se in senders) >= 2, senders
+
+
 def test_host_vector_paths(g, orc):
     """csr5g_spmv_host and the pipelined csr5g_spmv_host_batch (pinned and
     pageable host vectors, batches longer than the two buffer pairs, a second

@@ -133,6 +133,33 @@ def test_plan_tiles_partition():
     assert mg.effective_world(3, 8) == 3 and mg.effective_world(0, 8) == 1
 
 
+def test_plan_exchange_routes_partials_to_owners(orc):
+    """mg.plan_exchange (the static routing of the P2P exchange) against the
+    CPU emulation of the shard semantics: every non-owned first row goes to
+    the shard whose owned range contains it; senders are contiguous."""
+    for kind, m, n, nnz, seed, frac, sigma in [(1, 300, 30000, 60000, 3, 0.5, 4),
+                                               (2, 5000, 4000, 120000, 4, 0.0, 16),
+                                               (0, 2000, 2000, 54000, 5, 0.0, 27),
+                                               (1, 300, 30000, 60000, 7, 0.5, 2)]:
+        a = orc.generate_synthetic(kind, m, n, nnz, seed, frac)
+        x = np.ones(a.n)
+        for world in (2, 3, 8, 16):
+            w = mg.effective_world(a.nnz // (32 * sigma), world)
+            sh = [emulate_shard(a.row_ptr, a.col_idx, a.val, x, a.m, a.nnz, sigma, g, w)
+                  for g in range(w)]
+            dest, senders = mg.plan_exchange([(s["first_row"], s["first_owned"]) for s in sh],
+                                             [s["own"] for s in sh])
+            for g, s in enumerate(sh):
+                if s["first_owned"]:
+                    assert dest[g] == -1
+                else:
+                    lo, hi = sh[dest[g]]["own"]
+                    assert lo <= s["first_row"] < hi and dest[g] < g
+                sb, se = senders[g]
+                assert all(dest[r] == g for r in range(sb, se))
+                assert sum(d == g for d in dest) == se - sb
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_spmv_gloo(orc, world):
     # square matrices (iterative mode): one long row spanning shards, a skewed
