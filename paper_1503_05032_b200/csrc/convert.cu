@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -241,6 +242,15 @@ __global__ void __launch_bounds__(512) k_desc_transpose_tma(
 
 // empty_offset entries of flagged tiles (format.cpp:123-136): for every head
 // in column-major order, row_of_nonzero(g) - tile_row.
+// Heads of a flagged tile in order: head 0 is tile_row (eo = 0); the others
+// are the non-empty rows r in (tile_row, next_row] whose first nonzero lies
+// strictly inside the tile -- row_of_nonzero (format.cpp:42-50) of a head
+// position is the rightmost row of its equal row_ptr run, i.e. the non-empty
+// row starting there.  Tiles spanning at most kEoScanRows rows: the warp scans
+// row_ptr over the span (coalesced; the spans of all tiles overlap only at
+// their ends, so the scans read row_ptr about once in total).  Wider spans
+// (long empty-row runs): one binary search per head, bounded by the span.
+constexpr int64_t kEoScanRows = 2048;
 __global__ void k_eo(const uint32_t* __restrict__ head_bits, const uint32_t* __restrict__ tile_ptr,
                      const int64_t* __restrict__ rp, int64_t m, int64_t pcs, int sigma,
                      int64_t pos0, const int64_t* __restrict__ eo_ptr, int32_t* __restrict__ eo) {
@@ -252,6 +262,24 @@ __global__ void k_eo(const uint32_t* __restrict__ head_bits, const uint32_t* __r
   const int B = 32 * sigma;
   const int64_t tile_row = tp & 0x7fffffffu;
   const int64_t next_row = tile_ptr[k + 1] & 0x7fffffffu;
+  if (next_row - tile_row <= kEoScanRows) {
+    const int64_t start = pos0 + k * B, end = start + B;
+    int64_t out = eo_ptr[k];
+    if (lane == 0) eo[out] = 0;
+    ++out;
+    for (int64_t base = tile_row + 1; base <= next_row; base += 32) {
+      const int64_t r = base + lane;
+      const bool valid = r <= next_row;
+      const int64_t a = valid ? rp[r] : 0;
+      int64_t b = __shfl_down_sync(kFull, a, 1);
+      if (valid && (lane == 31 || r + 1 > next_row)) b = rp[r + 1];
+      const bool head = valid && a > start && a < end && b > a;
+      const uint32_t hm = __ballot_sync(kFull, head);
+      if (head) eo[out + __popc(hm & ((1u << lane) - 1))] = (int32_t)(r - tile_row);
+      out += __popc(hm);
+    }
+    return;
+  }
   uint64_t bits = column_bits(head_bits, k, B, sigma, lane);
   const int cnt = __popcll(bits);
   int incl = cnt;
@@ -331,9 +359,53 @@ __global__ void k_warp_bounds(const int64_t* __restrict__ prefix, int64_t pcs, i
   begin[w] = lo;
 }
 
-__global__ void k_warp_bounds_fix(int64_t* __restrict__ begin, int nw) {
-  for (int w = 1; w < nw; ++w) begin[w] = max(begin[w], begin[w - 1] + 1);
-  for (int w = nw - 1; w >= 1; --w) begin[w] = min(begin[w], begin[w + 1] - 1);
+// Every warp gets at least one tile: the serial passes
+//   for w = 1..nw-1:  b[w] = max(b[w], b[w-1] + 1)
+//   for w = nw-1..1:  b[w] = min(b[w], b[w+1] - 1)      (b[0] = 0, b[nw] = pcs)
+// are b'[w] = w + max_{j<=w}(b[j] - j) and b''[w] = w + min_{j>=w}(b'[j] - j):
+// a prefix max and a suffix min, done by one CTA (nw <= 32 * 1024).
+constexpr int kFixThreads = 1024;
+__global__ void __launch_bounds__(kFixThreads) k_warp_bounds_fix(int64_t* __restrict__ begin,
+                                                                  int nw) {
+  __shared__ int64_t part[kFixThreads];
+  const int t = threadIdx.x;
+  const int per = (nw + kFixThreads - 1) / kFixThreads;
+  // forward over j in [0, nw): inclusive prefix max of begin[j] - j
+  int lo = min(nw, t * per), hi = min(nw, lo + per);
+  int64_t m = LLONG_MIN;
+  for (int j = lo; j < hi; ++j) m = max(m, begin[j] - j);
+  part[t] = m;
+  __syncthreads();
+  for (int d = 1; d < kFixThreads; d <<= 1) {
+    const int64_t o = t >= d ? part[t - d] : LLONG_MIN;
+    __syncthreads();
+    part[t] = max(part[t], o);
+    __syncthreads();
+  }
+  int64_t run = t > 0 ? part[t - 1] : LLONG_MIN;
+  for (int j = lo; j < hi; ++j) {
+    run = max(run, begin[j] - j);
+    if (j >= 1) begin[j] = j + run;
+  }
+  __syncthreads();
+  // backward over j in [1, nw] (begin[nw] = pcs fixed): suffix min of begin[j] - j
+  lo = 1 + min(nw, t * per);
+  hi = 1 + min(nw, t * per + per);
+  m = LLONG_MAX;
+  for (int j = lo; j < hi; ++j) m = min(m, begin[j] - j);
+  part[t] = m;
+  __syncthreads();
+  for (int d = 1; d < kFixThreads; d <<= 1) {
+    const int64_t o = t + d < kFixThreads ? part[t + d] : LLONG_MAX;
+    __syncthreads();
+    part[t] = min(part[t], o);
+    __syncthreads();
+  }
+  run = t + 1 < kFixThreads ? part[t + 1] : LLONG_MAX;
+  for (int j = hi - 1; j >= lo; --j) {
+    run = min(run, begin[j] - j);
+    if (j < nw) begin[j] = j + run;
+  }
 }
 
 // A few scalars of the held range, one thread: row_of_nonzero at two positions
@@ -773,7 +845,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     k_warp_bounds<<<(unsigned)((h->nwarps + 1 + 255) / 256), 256, 0, stream>>>(
         work_prefix, pcs, h->nwarps, emax, h->warp_begin);
     TRYC(cudaGetLastError());
-    k_warp_bounds_fix<<<1, 1, 0, stream>>>(h->warp_begin, h->nwarps);
+    k_warp_bounds_fix<<<1, kFixThreads, 0, stream>>>(h->warp_begin, h->nwarps);
     TRYC(cudaGetLastError());
   }
   trace.mark("plan");

@@ -80,6 +80,41 @@ def summarize(rep, workload, out_txt):
     print("\n".join(lines))
 
 
+CONV_KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+             "lts__t_sector_hit_rate.pct", "sm__warps_active.avg.per_cycle_active",
+             "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
+             "launch__block_size", "launch__registers_per_thread"]
+
+
+def kernels(rep, workload, out_txt):
+    """Every captured launch (converter kernels): duration, DRAM bytes and
+    achieved DRAM GB/s, L2 hit rate, top stall."""
+    rows = ncu_csv(rep, "raw")
+    hdr, units = rows[0], rows[1]
+    kname = hdr.index("Kernel Name")
+    lines = [f"ncu --set full, converter kernels: {os.path.basename(rep)} (workload {workload})"]
+    for d in rows[2:]:
+        name = d[kname].split("(")[0].replace("void ", "")
+        lines.append(f"kernel: {name}")
+        for k in CONV_KEYS:
+            if k in hdr:
+                lines.append(f"  {k:58s} {d[hdr.index(k)]:>16s} {units[hdr.index(k)]}")
+        rd = to_bytes(d[hdr.index("dram__bytes_read.sum")], units[hdr.index("dram__bytes_read.sum")])
+        wr = to_bytes(d[hdr.index("dram__bytes_write.sum")], units[hdr.index("dram__bytes_write.sum")])
+        t = float(d[hdr.index("gpu__time_duration.sum")]) * {
+            "nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}.get(units[hdr.index("gpu__time_duration.sum")], 1e-9)
+        lines.append(f"  dram read+write {rd + wr:.0f} bytes -> {(rd + wr) / t / 1e9:.0f} GB/s")
+        stalls = sorted(((float(d[i]), h) for i, h in enumerate(hdr)
+                         if h.startswith("smsp__pcsamp_warps_issue_stalled") and
+                         not h.endswith("not_issued") and d[i].replace(".", "").isdigit()),
+                        reverse=True)[:3]
+        lines.append("  top stalls: " + ", ".join(f"{h.split('stalled_')[1]}={v:.0f}" for v, h in stalls))
+    with open(out_txt, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
 def launches(csv_path, out_txt):
     rows = list(csv.reader(open(csv_path)))
     start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
@@ -104,7 +139,9 @@ def launches(csv_path, out_txt):
 
 
 if __name__ == "__main__":
-    if sys.argv[1] == "--launches":
+    if sys.argv[1] == "--kernels":
+        kernels(sys.argv[2], sys.argv[3], sys.argv[4])
+    elif sys.argv[1] == "--launches":
         launches(sys.argv[2], sys.argv[3])
     else:
         summarize(sys.argv[1], sys.argv[2], sys.argv[3])

@@ -119,6 +119,12 @@ def hard_shapes(orc):
     c2 = [j for k in range(3000) for j in range(3)]
     yield "alternating empties", orc.coo_to_csr(r2, c2, np.linspace(0.5, 1.5, len(r2)), 7000, 5)
     yield "random skew", orc.generate_synthetic(2, 5000, 3000, 40000, rng())
+    # many heads per flagged tile over a wide row span (> 2048 rows: k_eo's
+    # binary-search path) and a narrow one (its row_ptr scan path)
+    for gap, name in ((97, "wide gappy heads"), (3, "narrow gappy heads")):
+        r4 = [gap * k + 1 for k in range(2500) for _ in range(2)]
+        c4 = [(7 * k + j) % 600 for k in range(2500) for j in range(2)]
+        yield name, orc.coo_to_csr(r4, c4, np.linspace(0.5, 1.5, len(r4)), gap * 2500 + 5, 600)
     # regions of singleton rows (tiles with more heads than the shared-memory
     # slots: spill path) between regions of long rows (shared-memory path), so
     # both kinds of tile alternate inside one warp's tile range
