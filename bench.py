@@ -317,7 +317,8 @@ def run_ours(args, workload_name, workload):
         col_s, val_s = W.entries(lo, hi)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sh = mg.Csr5Sharded(W.row_ptr, col_s, val_s, m, n, nnz, sigma, rank, world)
+        sh = mg.Csr5Sharded(W.row_ptr, col_s, val_s, m, n, nnz, sigma, rank, world,
+                            iterative=args.iterative and m == n)
         torch.cuda.synchronize()
         conv_ms = (time.perf_counter() - t0) * 1e3
         del col_s, val_s
@@ -349,6 +350,25 @@ def run_ours(args, workload_name, workload):
         W.drop()
     if not err <= 1e-12:
         raise SystemExit(f"correctness guard: max relative error {err} > 1e-12")
+    it_ctr = [0]
+    if world > 1 and sh.iterative:
+        # fused y -> x (p2p.cu): one step from x must leave every active rank
+        # with the same x_1, whose owned rows are the y just checked (bit for bit)
+        sh.x_buffer(0).copy_(x)
+        x1 = sh.spmv_iter(0)
+        it_ctr[0] = 1
+        torch.cuda.synchronize()
+        same = bool(torch.equal(x1[own[0]:own[1]], y[own[0]:own[1]])) if sh.active else True
+        h = torch.tensor([int(sh.active), int(same),
+                          int(x1.view(torch.int64).sum().item()) if sh.active else 0],
+                         dtype=torch.int64, device=dev if dist.get_backend() == "nccl" else "cpu")
+        hs = [torch.empty_like(h) for _ in range(world)]
+        dist.all_gather(hs, h)
+        act = [v for v in hs if int(v[0])]
+        if not all(int(v[1]) for v in act) or len({int(v[2]) for v in act}) != 1:
+            raise SystemExit("correctness guard: fused iterative x_1 differs between ranks or from y")
+        if sh.mailbox_errors():
+            raise SystemExit("correctness guard: P2P mailbox protocol errors")
 
     def barrier():
         if dist is not None:
@@ -390,6 +410,9 @@ def run_ours(args, workload_name, workload):
             if world == 1:  # ping-pong: y of this step is x of the next
                 csr5.spmv_csr5(a5, bufs[0], bufs[1])
                 bufs.reverse()
+            elif sh.iterative:  # fused: the SpMV stores y into every rank's next x
+                sh.spmv_iter(it_ctr[0])
+                it_ctr[0] += 1
             else:
                 run()
                 sh.gather_y_into_x(y, x)
@@ -599,7 +622,9 @@ def run_ours(args, workload_name, workload):
             "config": {"workload": workload_name, "desc": workload["desc"], "m": m, "n": n,
                        "nnz": nnz, "omega": 32, "sigma": sigma, "p": info.p,
                        "desc_word_bits": info.word_bits, "mode": "deterministic",
-                       "step": ("iterative: SpMV + y->x all-gather" if args.iterative else
+                       "step": (("iterative: SpMV with y stored into every rank's next x over "
+                                 "NVLink (fused, p2p.cu)" if world > 1 and sh.iterative else
+                                 "iterative: SpMV + y->x all-gather") if args.iterative else
                                 "SpMV (+ boundary exchange at N>1)"),
                        "exchange": (os.environ.get("CSR5G_EXCHANGE", "p2p") if world > 1
                                     else None),

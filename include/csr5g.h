@@ -151,7 +151,11 @@ CSR5G_API int csr5g_fixup(csr5g_matrix h, const csr5g_partial *d_all, int32_t wo
 #define CSR5G_IPC_HANDLE_BYTES 64
 #define CSR5G_MAX_WORLD 64
 typedef struct csr5g_mailbox_s *csr5g_mailbox;
-CSR5G_API int csr5g_mailbox_create(int device, int32_t world, int32_t rank, csr5g_mailbox *out);
+/* vec_len > 0 (iterative mode, = m = n): the mailbox also holds the two x
+ * buffers of the y -> x ping-pong, x_k = vector(k & 1). */
+CSR5G_API int csr5g_mailbox_create(int device, int32_t world, int32_t rank, int64_t vec_len,
+                                   csr5g_mailbox *out);
+CSR5G_API int csr5g_mailbox_vector(csr5g_mailbox mb, int32_t which, double **d_vec);
 CSR5G_API int csr5g_mailbox_ipc_handle(csr5g_mailbox mb, void *handle_out /* 64 bytes */);
 /* map another process's mailbox (its csr5g_mailbox_ipc_handle bytes) */
 CSR5G_API int csr5g_mailbox_open_peer(csr5g_mailbox mb, int32_t peer, const void *handle /* 64 bytes */);
@@ -160,13 +164,26 @@ CSR5G_API int csr5g_mailbox_link_local(csr5g_mailbox mb, int32_t peer, csr5g_mai
 /* protocol violations seen by this rank's fix-ups (0 = none; synchronous) */
 CSR5G_API int csr5g_mailbox_errors(csr5g_mailbox mb, uint32_t *errors);
 CSR5G_API int csr5g_mailbox_release(csr5g_mailbox mb);
+/* active_world: ranks holding tiles (0 .. active_world-1) */
 CSR5G_API int csr5g_mg_bind(csr5g_matrix h, csr5g_mailbox mb, int32_t dest, int32_t sender_begin,
-                            int32_t sender_end);
+                            int32_t sender_end, int32_t active_world);
 CSR5G_API int csr5g_mg_spmv_post(csr5g_matrix h, const double *d_x, double *d_y, void *stream,
                                  void *ev_tiles_begin, void *ev_tiles_end);
 CSR5G_API int csr5g_mg_spmv_fixup(csr5g_matrix h, double *d_y, void *stream);
 CSR5G_API int csr5g_mg_spmv(csr5g_matrix h, const double *d_x, double *d_y, void *stream,
                             void *ev_tiles_begin, void *ev_tiles_end);
+/* Fused iterative step it (x_{it+1} = A x_it, square A, <= 8 active ranks):
+ * waits until every active peer stored its rows of x_it here, runs the SpMV
+ * from vector(it & 1) into vector((it+1) & 1), every final y value also
+ * stored into each peer's vector((it+1) & 1) over NVLink by the kernels that
+ * produce it, then the boundary fix-up (mirrored) and the ready signal to
+ * every peer.  No all-gather.  post/finish split as above for ranks sharing
+ * one GPU (host barrier between and after). */
+CSR5G_API int csr5g_mg_iter_post(csr5g_matrix h, int64_t it, void *stream, void *ev_tiles_begin,
+                                 void *ev_tiles_end);
+CSR5G_API int csr5g_mg_iter_finish(csr5g_matrix h, int64_t it, void *stream);
+CSR5G_API int csr5g_mg_iter(csr5g_matrix h, int64_t it, void *stream, void *ev_tiles_begin,
+                            void *ev_tiles_end);
 
 /* format.cpp:254-265 csr5_to_csr: undo the tile transposition into the
  * caller's device buffers (col_idx int32[nnz_held], val f64[nnz_held]). */

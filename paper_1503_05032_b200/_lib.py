@@ -71,16 +71,20 @@ SIGNATURES = {
     "csr5g_shard_send_record": (C.c_int, [_vp, C.POINTER(_vp)]),
     "csr5g_set_send_buffer": (C.c_int, [_vp, _vp]),
     "csr5g_fixup": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp]),
-    "csr5g_mailbox_create": (C.c_int, [C.c_int, _i32, _i32, C.POINTER(_vp)]),
+    "csr5g_mailbox_create": (C.c_int, [C.c_int, _i32, _i32, _i64, C.POINTER(_vp)]),
+    "csr5g_mailbox_vector": (C.c_int, [_vp, _i32, C.POINTER(_vp)]),
     "csr5g_mailbox_ipc_handle": (C.c_int, [_vp, _vp]),
     "csr5g_mailbox_open_peer": (C.c_int, [_vp, _i32, _vp]),
     "csr5g_mailbox_link_local": (C.c_int, [_vp, _i32, _vp]),
     "csr5g_mailbox_errors": (C.c_int, [_vp, C.POINTER(C.c_uint32)]),
     "csr5g_mailbox_release": (C.c_int, [_vp]),
-    "csr5g_mg_bind": (C.c_int, [_vp, _vp, _i32, _i32, _i32]),
+    "csr5g_mg_bind": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32]),
     "csr5g_mg_spmv_post": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "csr5g_mg_spmv_fixup": (C.c_int, [_vp, _vp, _vp]),
     "csr5g_mg_spmv": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "csr5g_mg_iter_post": (C.c_int, [_vp, _i64, _vp, _vp, _vp]),
+    "csr5g_mg_iter_finish": (C.c_int, [_vp, _i64, _vp]),
+    "csr5g_mg_iter": (C.c_int, [_vp, _i64, _vp, _vp, _vp]),
     "csr5g_to_csr": (C.c_int, [_vp, _vp, _vp, _vp]),
     "csr5g_release": (C.c_int, [_vp]),
     "csr5g_build_host": (C.c_int, [C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, C.POINTER(Params),

@@ -27,6 +27,23 @@ constexpr int kSpmvThreads = 256;
 constexpr int kSpmvWarpsPerBlock = kSpmvThreads / 32;
 constexpr uint32_t kFull = 0xffffffffu;
 
+// Peer copies of y (p2p.cu, fused iterative y -> x): every final y value is
+// also stored into each peer's next-x buffer over NVLink.  skip_row: a row
+// whose value here is still partial (an owner's boundary row before the
+// fix-up, which mirrors the total itself).
+constexpr int kMaxMirror = 7;  // one NVSwitch box: 8 GPUs
+struct Mirrors {
+  double* p[kMaxMirror];
+  int32_t n;
+  int64_t skip_row;
+};
+
+__device__ __forceinline__ void mirror_store(const Mirrors& m, int64_t r, double v) {
+#pragma unroll
+  for (int g = 0; g < kMaxMirror; ++g)
+    if (g < m.n) m.p[g][r] = v;
+}
+
 // Everything the SpMV kernels read, passed by value.
 struct SpmvArgs {
   const int64_t* row_ptr;
@@ -67,6 +84,7 @@ struct SpmvArgs {
   int32_t early_gather;    // random gathers: issue tile k+1's gathers before tile k's depth loop
   float x_frac;            // share of x lines given evict_last (the rest evict_first)
   int32_t y_hint;          // y stores: 1 = L2 evict_first, no L1 allocation
+  Mirrors mir;             // fused iterative mode: peer next-x buffers (n = 0: none)
 };
 
 struct Pipeline;  // pipeline.cu: host-vector copy/compute pipeline
@@ -90,6 +108,7 @@ struct Handle {
   csr5g_partial* send_ext = nullptr;  // caller-provided record slot
   uint32_t* send_flag = nullptr;      // p2p.cu: owner's ready flag for this shard's record
   uint32_t send_epoch = 0;            // value stored into send_flag by the current call
+  Mirrors mir{};                      // p2p.cu: peer copies of y for the current call
   Binding* mg = nullptr;              // p2p.cu: NVLink boundary exchange of this shard
   double* spill = nullptr;            // nwarps * (B + 1) doubles
   int64_t* warp_begin = nullptr;      // nwarps + 1 tile-range bounds, split by tile work

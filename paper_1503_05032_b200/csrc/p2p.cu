@@ -28,6 +28,19 @@
 // (functional tests) must not rely on stream waits across processes: mg.py
 // then separates the two phases with a host barrier, so every wait is already
 // satisfied when it is enqueued (B200_PROFILING: no cross-rank waits on one GPU).
+//
+// Fused iterative mode (y -> x, square A).  Instead of an all-gather of the
+// owned y ranges after the SpMV, every kernel that stores a final y value
+// (tile write-back, tail rows, calibration, fix-up) also stores it into each
+// peer's next-x buffer over NVLink (Mirrors, internal.cuh): the exchange
+// rides on the SpMV's own stores and overlaps its HBM stream.  Each mailbox
+// carries the two x buffers of the ping-pong (x_k = vec[k & 1]) and an
+// xready[g] flag per rank.  Iteration k on rank r:
+//   wait xready[g] >= k for every active peer g (their rows of x_k landed;
+//   also: they finished iteration k-1, so nobody still reads the buffer r is
+//   about to overwrite on them), SpMV x_k -> y = vec[(k+1) & 1] with mirrors,
+//   boundary fix-up (mirrored), then k_signal: system fence and
+//   xready[r] = k + 1 on every peer.
 #include <cuda.h>
 
 #include <cstring>
@@ -42,21 +55,31 @@ constexpr int kMaxWorld = 64;
 struct MailboxDev {
   csr5g_partial slot[kMaxWorld];
   uint32_t ready[kMaxWorld];
+  uint32_t xready[kMaxWorld];  // iteration whose x rows rank g has stored here
   uint32_t ack;
   uint32_t err;
 };
+constexpr size_t kVecOffset = 4096;  // x buffers follow the header in one allocation
+static_assert(sizeof(MailboxDev) <= kVecOffset, "mailbox header");
 
 struct Mailbox {
   int device = 0, world = 0, rank = 0;
+  int64_t vec_len = 0;                    // x buffers (iterative mode), 0 = none
   MailboxDev* local = nullptr;            // this rank's mailbox (own HBM)
   MailboxDev* peer[kMaxWorld] = {};       // every rank's mailbox, mapped here
   bool ipc_opened[kMaxWorld] = {};
   uint32_t** d_peer_ack = nullptr;        // device table: &peer[g]->ack
+  uint32_t** d_peer_xready = nullptr;     // device table: &peer[g]->xready[rank]
+  double* vec(const MailboxDev* d, int64_t which) const {
+    return reinterpret_cast<double*>(reinterpret_cast<char*>(const_cast<MailboxDev*>(d)) +
+                                     kVecOffset) +
+           (which & 1) * vec_len;
+  }
 };
 
 struct Binding {
   Mailbox* mb = nullptr;
-  int dest = -1, sb = 0, se = 0;
+  int dest = -1, sb = 0, se = 0, active = 1;
   uint32_t epoch = 0;
 };
 
@@ -82,6 +105,7 @@ int wait_value_fn(WaitValueFn* out) {
   return CSR5G_OK;
 }
 
+// The stream's front end waits until *addr >= value (cyclic compare); no SM spins.
 int stream_wait_geq(cudaStream_t s, const uint32_t* addr, uint32_t value) {
   WaitValueFn fn = nullptr;
   if (int rc = wait_value_fn(&fn)) return rc;
@@ -102,9 +126,10 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// One thread: y[row] += partials of senders [sb, se) in shard order, then ack.
+// One thread: y[row] += partials of senders [sb, se) in shard order (mirrored
+// to the peers' next x in the iterative mode), then ack every sender.
 __global__ void k_fixup_p2p(MailboxDev* mb, uint32_t* const* peer_ack, int sb, int se,
-                            int64_t row, double* __restrict__ y, uint32_t epoch) {
+                            int64_t row, double* __restrict__ y, uint32_t epoch, Mirrors mir) {
   double acc = y[row];
   for (int g = sb; g < se; ++g) {
     if (ld_acquire_sys(&mb->ready[g]) != epoch) atomicOr(&mb->err, 1u);
@@ -113,8 +138,18 @@ __global__ void k_fixup_p2p(MailboxDev* mb, uint32_t* const* peer_ack, int sb, i
     else acc += r->value;
   }
   y[row] = acc;
+  mirror_store(mir, row, acc);
   __threadfence_system();
   for (int g = sb; g < se; ++g) st_release_sys(peer_ack[g], epoch);
+}
+
+// Iterative mode: this rank's rows of x_{k+1} are stored on every peer ->
+// raise xready[rank] = k + 1 there (after a system-scope fence; the SpMV,
+// calibration and fix-up kernels that stored the rows precede it in the stream).
+__global__ void k_signal(uint32_t* const* peer_xready, int n, uint32_t value) {
+  __threadfence_system();
+  for (int g = threadIdx.x; g < n; g += blockDim.x)
+    if (peer_xready[g]) st_release_sys(peer_xready[g], value);
 }
 
 }  // namespace
@@ -149,7 +184,66 @@ int mg_fixup(Handle* h, double* d_y, cudaStream_t stream) {
   for (int g = b->sb; g < b->se; ++g)
     if (int rc = stream_wait_geq(stream, &b->mb->local->ready[g], b->epoch)) return rc;
   k_fixup_p2p<<<1, 1, 0, stream>>>(b->mb->local, b->mb->d_peer_ack, b->sb, b->se, h->last_row,
-                                   d_y, b->epoch);
+                                   d_y, b->epoch, h->mir);
+  CSR5G_CUDA(cudaGetLastError());
+  return CSR5G_OK;
+}
+
+namespace {
+
+int iter_check(Handle* h) {
+  Binding* b = h->mg;
+  if (!b) return fail(CSR5G_EINVAL, "csr5g: shard is not bound to a mailbox (csr5g_mg_bind)");
+  Mailbox* m = b->mb;
+  if (m->vec_len <= 0) return fail(CSR5G_EINVAL, "csr5g: mailbox has no x buffers (vec_len = 0)");
+  if (m->vec_len != h->info.m || h->info.m != h->info.n)
+    return fail(CSR5G_EINVAL, "csr5g: iterative mode needs a square matrix and vec_len = m");
+  if (b->active - 1 > kMaxMirror)
+    return fail(CSR5G_EINVAL, "csr5g: iterative P2P mode supports at most " +
+                                  std::to_string(kMaxMirror + 1) + " active ranks");
+  for (int g = 0; g < b->active; ++g)
+    if (!m->peer[g]) return fail(CSR5G_EINVAL, "csr5g: iterative mode needs every active peer linked");
+  return CSR5G_OK;
+}
+
+// Peer next-x buffers of iteration it (skip_row: an owner's boundary row is
+// mirrored by its fix-up, with the total).
+Mirrors iter_mirrors(Handle* h, int64_t it) {
+  Binding* b = h->mg;
+  Mailbox* m = b->mb;
+  Mirrors mir{};
+  for (int g = 0; g < b->active; ++g)
+    if (g != m->rank) mir.p[mir.n++] = m->vec(m->peer[g], it + 1);
+  mir.skip_row = b->se > b->sb ? h->last_row : -1;
+  return mir;
+}
+
+}  // namespace
+
+int mg_iter_post(Handle* h, int64_t it, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1) {
+  if (int rc = iter_check(h)) return rc;
+  Binding* b = h->mg;
+  Mailbox* m = b->mb;
+  CSR5G_CUDA(cudaSetDevice(h->device));
+  for (int g = 0; g < b->active; ++g)
+    if (g != m->rank)
+      if (int rc = stream_wait_geq(stream, &m->local->xready[g], (uint32_t)it)) return rc;
+  h->mir = iter_mirrors(h, it);
+  const int rc = mg_post(h, m->vec(m->local, it), m->vec(m->local, it + 1), stream, ev0, ev1);
+  h->mir = Mirrors{};
+  return rc;
+}
+
+int mg_iter_finish(Handle* h, int64_t it, cudaStream_t stream) {
+  if (int rc = iter_check(h)) return rc;
+  Binding* b = h->mg;
+  Mailbox* m = b->mb;
+  h->mir = iter_mirrors(h, it);
+  h->mir.skip_row = -1;
+  int rc = mg_fixup(h, m->vec(m->local, it + 1), stream);
+  h->mir = Mirrors{};
+  if (rc) return rc;
+  k_signal<<<1, 32, 0, stream>>>(m->d_peer_xready, b->active, (uint32_t)(it + 1));
   CSR5G_CUDA(cudaGetLastError());
   return CSR5G_OK;
 }
@@ -170,8 +264,13 @@ namespace {
 
 int refresh_peer_table(Mailbox* m) {
   uint32_t* acks[kMaxWorld] = {};
-  for (int g = 0; g < m->world; ++g) acks[g] = m->peer[g] ? &m->peer[g]->ack : nullptr;
+  uint32_t* xr[kMaxWorld] = {};
+  for (int g = 0; g < m->world; ++g) {
+    acks[g] = m->peer[g] ? &m->peer[g]->ack : nullptr;
+    xr[g] = (m->peer[g] && g != m->rank) ? &m->peer[g]->xready[m->rank] : nullptr;
+  }
   CSR5G_CUDA(cudaMemcpy(m->d_peer_ack, acks, sizeof(uint32_t*) * m->world, cudaMemcpyHostToDevice));
+  CSR5G_CUDA(cudaMemcpy(m->d_peer_xready, xr, sizeof(uint32_t*) * m->world, cudaMemcpyHostToDevice));
   return CSR5G_OK;
 }
 
@@ -179,22 +278,29 @@ int refresh_peer_table(Mailbox* m) {
 
 extern "C" {
 
-int csr5g_mailbox_create(int device, int32_t world, int32_t rank, csr5g_mailbox* out) {
+int csr5g_mailbox_create(int device, int32_t world, int32_t rank, int64_t vec_len,
+                         csr5g_mailbox* out) {
   if (!out) return fail(CSR5G_EINVAL, "csr5g: out is NULL");
   *out = nullptr;
   if (world < 1 || world > kMaxWorld)
     return fail(CSR5G_EINVAL, "csr5g: world must be in [1, " + std::to_string(kMaxWorld) + "]");
   if (rank < 0 || rank >= world) return fail(CSR5G_EINVAL, "csr5g: rank outside [0, world)");
+  if (vec_len < 0) return fail(CSR5G_EINVAL, "csr5g: negative vec_len");
   CSR5G_CUDA(cudaSetDevice(device));
   auto* m = new Mailbox;
   m->device = device;
   m->world = world;
   m->rank = rank;
-  cudaError_t e = cudaMalloc(&m->local, sizeof(MailboxDev));
+  m->vec_len = vec_len;
+  void* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, kVecOffset + sizeof(double) * 2 * (size_t)vec_len);
+  m->local = static_cast<MailboxDev*>(base);
   if (e == cudaSuccess) e = cudaMemset(m->local, 0, sizeof(MailboxDev));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_peer_ack, sizeof(uint32_t*) * kMaxWorld);
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_peer_xready, sizeof(uint32_t*) * kMaxWorld);
   if (e != cudaSuccess) {
     cudaFree(m->local);
+    cudaFree(m->d_peer_ack);
     delete m;
     return cuda_fail(e, "csr5g_mailbox_create");
   }
@@ -205,6 +311,13 @@ int csr5g_mailbox_create(int device, int32_t world, int32_t rank, csr5g_mailbox*
   m->peer[rank] = m->local;
   if (int rc = refresh_peer_table(m)) return rc;
   *out = new csr5g_mailbox_s{m};
+  return CSR5G_OK;
+}
+
+int csr5g_mailbox_vector(csr5g_mailbox mb, int32_t which, double** d_vec) {
+  if (!mb || !d_vec) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  if (mb->m->vec_len <= 0) return fail(CSR5G_EINVAL, "csr5g: mailbox has no x buffers");
+  *d_vec = mb->m->vec(mb->m->local, which);
   return CSR5G_OK;
 }
 
@@ -240,6 +353,8 @@ int csr5g_mailbox_link_local(csr5g_mailbox mb, int32_t peer, csr5g_mailbox peer_
   if (peer < 0 || peer >= m->world || peer == m->rank || peer_mb->m->rank != peer)
     return fail(CSR5G_EINVAL, "csr5g: peer must be another rank in [0, world)");
   if (m->peer[peer]) return fail(CSR5G_EINVAL, "csr5g: peer mailbox already linked");
+  if (peer_mb->m->vec_len != m->vec_len)
+    return fail(CSR5G_EINVAL, "csr5g: peer mailbox has another vec_len");
   if (peer_mb->m->device != m->device) {
     int ok = 0;
     CSR5G_CUDA(cudaDeviceCanAccessPeer(&ok, m->device, peer_mb->m->device));
@@ -270,6 +385,7 @@ int csr5g_mailbox_release(csr5g_mailbox mb) {
   for (int g = 0; g < m->world; ++g)
     if (m->ipc_opened[g]) cudaIpcCloseMemHandle(m->peer[g]);
   cudaFree(m->d_peer_ack);
+  cudaFree(m->d_peer_xready);
   cudaFree(m->local);
   delete m;
   delete mb;
@@ -277,18 +393,20 @@ int csr5g_mailbox_release(csr5g_mailbox mb) {
 }
 
 int csr5g_mg_bind(csr5g_matrix h, csr5g_mailbox mb, int32_t dest, int32_t sender_begin,
-                  int32_t sender_end) {
+                  int32_t sender_end, int32_t active_world) {
   if (!h || !mb) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
   Handle* hh = h->h;
   Mailbox* m = mb->m;
   if (hh->device != m->device) return fail(CSR5G_EINVAL, "csr5g: mailbox is on another device");
+  if (active_world < 1 || active_world > m->world || m->rank >= active_world)
+    return fail(CSR5G_EINVAL, "csr5g: active_world must cover this rank and not exceed world");
   const bool first_owned = hh->first_owned || hh->pcs == 0;
   if ((dest >= 0) == first_owned)
     return fail(CSR5G_EINVAL, first_owned ? "csr5g: shard owns its first row; dest must be -1"
                                           : "csr5g: shard does not own its first row; dest required");
   if (dest >= m->rank) return fail(CSR5G_EINVAL, "csr5g: dest must be an earlier rank");
   if (sender_end > sender_begin &&
-      (sender_begin != m->rank + 1 || sender_end > m->world || hh->is_last))
+      (sender_begin != m->rank + 1 || sender_end > active_world || hh->is_last))
     return fail(CSR5G_EINVAL, "csr5g: senders must be the ranks right after this one");
   for (int g = sender_begin; g < sender_end; ++g)
     if (!m->peer[g]) return fail(CSR5G_EINVAL, "csr5g: sender mailbox not linked");
@@ -298,6 +416,7 @@ int csr5g_mg_bind(csr5g_matrix h, csr5g_mailbox mb, int32_t dest, int32_t sender
   hh->mg->dest = dest;
   hh->mg->sb = sender_begin;
   hh->mg->se = std::max(sender_begin, sender_end);
+  hh->mg->active = active_world;
   return CSR5G_OK;
 }
 
@@ -317,6 +436,24 @@ int csr5g_mg_spmv(csr5g_matrix h, const double* d_x, double* d_y, void* stream, 
                   void* ev1) {
   if (int rc = csr5g_mg_spmv_post(h, d_x, d_y, stream, ev0, ev1)) return rc;
   return csr5g_mg_spmv_fixup(h, d_y, stream);
+}
+
+int csr5g_mg_iter_post(csr5g_matrix h, int64_t it, void* stream, void* ev0, void* ev1) {
+  if (!h) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
+  if (it < 0) return fail(CSR5G_EINVAL, "csr5g: negative iteration");
+  return mg_iter_post(h->h, it, static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(ev0),
+                      static_cast<cudaEvent_t>(ev1));
+}
+
+int csr5g_mg_iter_finish(csr5g_matrix h, int64_t it, void* stream) {
+  if (!h) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
+  if (it < 0) return fail(CSR5G_EINVAL, "csr5g: negative iteration");
+  return mg_iter_finish(h->h, it, static_cast<cudaStream_t>(stream));
+}
+
+int csr5g_mg_iter(csr5g_matrix h, int64_t it, void* stream, void* ev0, void* ev1) {
+  if (int rc = csr5g_mg_iter_post(h, it, stream, ev0, ev1)) return rc;
+  return csr5g_mg_iter_finish(h, it, stream);
 }
 
 }  // extern "C"

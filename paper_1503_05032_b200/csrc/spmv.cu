@@ -62,6 +62,7 @@ __device__ void rows_part(const SpmvArgs& a) {
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
     if (idx < a.lead_rows) {
       a.y[idx] = 0.0;
+      if (a.mir.n) mirror_store(a.mir, idx, 0.0);
       continue;
     }
     const int64_t r = a.tail_row_begin + (idx - a.lead_rows);
@@ -70,10 +71,12 @@ __device__ void rows_part(const SpmvArgs& a) {
     if (lo < a.tail_pos) lo = a.tail_pos;
     double s = 0.0;
     for (int64_t q = lo; q < hi; ++q) s = fma(a.val[q - a.pos0], a.x[a.col[q - a.pos0]], s);
-    if (a.has_tail_item && r == a.tail_row_begin)
+    if (a.has_tail_item && r == a.tail_row_begin) {
       put_item(a, 2 * (int64_t)a.nwarps, r, s);
-    else
+    } else {
       a.y[r] = s;
+      if (a.mir.n) mirror_store(a.mir, r, s);
+    }
   }
 }
 
@@ -105,7 +108,7 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
 // flag: value stores, system-scope fence, then the flag store with release.
 __device__ __forceinline__ void write_run(int64_t row, double v, double* y, int64_t first_row,
                                           int first_owned, csr5g_partial* send, uint32_t* flag,
-                                          uint32_t epoch) {
+                                          uint32_t epoch, const Mirrors& mir) {
   if (!first_owned && row == first_row) {
     send->row = row;
     send->value = v;
@@ -115,6 +118,7 @@ __device__ __forceinline__ void write_run(int64_t row, double v, double* y, int6
     }
   } else {
     y[row] = v;
+    if (mir.n && row != mir.skip_row) mirror_store(mir, row, v);
   }
 }
 
@@ -125,7 +129,8 @@ __device__ __forceinline__ void write_run(int64_t row, double v, double* y, int6
 __device__ void calibrate_window(const int64_t* __restrict__ item_row,
                                  const double* __restrict__ item_val, int64_t N, int64_t base,
                                  double* __restrict__ y, int64_t first_row, int first_owned,
-                                 csr5g_partial* send, uint32_t* flag, uint32_t epoch) {
+                                 csr5g_partial* send, uint32_t* flag, uint32_t epoch,
+                                 const Mirrors& mir) {
   const int lane = threadIdx.x & 31;
   if (base == 0 && lane == 0) {
     send->row = -1;
@@ -155,7 +160,7 @@ __device__ void calibrate_window(const int64_t* __restrict__ item_row,
     rk = __shfl_sync(kFull, key, ls);
     cont = (base + 32 < N) && __ldcg(item_row + base + 32) == rk;
   }
-  if (start && !(cont && lane == ls)) write_run(key, v, y, first_row, first_owned, send, flag, epoch);
+  if (start && !(cont && lane == ls)) write_run(key, v, y, first_row, first_owned, send, flag, epoch, mir);
   if (cont) {
     double total = __shfl_sync(kFull, v, ls);
     for (int64_t pos = base + 32;; pos += 32) {
@@ -168,21 +173,21 @@ __device__ void calibrate_window(const int64_t* __restrict__ item_row,
       total += s;
       if (mm != kFull) break;
     }
-    if (lane == 0) write_run(rk, total, y, first_row, first_owned, send, flag, epoch);
+    if (lane == 0) write_run(rk, total, y, first_row, first_owned, send, flag, epoch, mir);
   }
 }
 
 __global__ void k_calibrate(const int64_t* __restrict__ item_row,
                             const double* __restrict__ item_val, int64_t N, double* __restrict__ y,
                             int64_t first_row, int first_owned, csr5g_partial* send,
-                            uint32_t* flag, uint32_t epoch) {
+                            uint32_t* flag, uint32_t epoch, Mirrors mir) {
   // launched as a programmatic dependent of k_spmv: its launch overlaps the
   // SpMV; the items are read only once that grid has completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane;
   if (base >= N) return;
-  calibrate_window(item_row, item_val, N, base, y, first_row, first_owned, send, flag, epoch);
+  calibrate_window(item_row, item_val, N, base, y, first_row, first_owned, send, flag, epoch, mir);
 }
 
 }  // namespace
@@ -276,6 +281,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
         st_hint(y + r, v, pol_s);
       else
         y[r] = v;
+      if (a.mir.n) mirror_store(a.mir, r, v);
     };
     int64_t pend_row = -1;
     double pend_val = 0.0;
@@ -745,6 +751,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.stage_bytes = h->stage_bytes;
   a.bar_bytes = h->bar_bytes;
   a.atomic = atomic;
+  a.mir = h->mir;
   const int grid = std::max(h->tile_blocks, h->rows_blocks);
   const int threads = 32 * h->warps_per_block;
   // the plan's gather path; CSR5G_XMODE / CSR5G_XWINDOW override it (experiments)
@@ -831,7 +838,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     cfg.numAttrs = pdl_on ? 1 : 0;
     CSR5G_CUDA(cudaLaunchKernelEx(&cfg, k_calibrate, (const int64_t*)h->item_row,
                                   (const double*)h->item_val, items, d_y, h->first_row,
-                                  (int)h->first_owned, a.send, h->send_flag, h->send_epoch));
+                                  (int)h->first_owned, a.send, h->send_flag, h->send_epoch, h->mir));
   } else if (!atomic) {
     const csr5g_partial none{-1, 0.0};
     CSR5G_CUDA(cudaMemcpyAsync(a.send, &none, sizeof none, cudaMemcpyHostToDevice, stream));

@@ -77,6 +77,19 @@ def owned_ranges(infos) -> list[tuple[int, int]]:
     return [(int(i.own_row_begin), int(i.own_row_end)) for i in infos]
 
 
+class _CudaArray:
+    """__cuda_array_interface__ over library-owned device memory."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _device_view(ptr: int, n: int, device: int):
+    import torch
+    return torch.as_tensor(_CudaArray(ptr, n), device=f"cuda:{device}")
+
+
 def plan_exchange(firsts, owns):
     """Static routing of the boundary partials (host logic, shared with the
     gloo tests).
@@ -142,7 +155,7 @@ class Csr5Sharded:
     """Rank-local shard of a CSR5 matrix plus the exchange (torch.distributed)."""
 
     def __init__(self, row_ptr, col_slice, val_slice, m: int, n: int, nnz: int, sigma: int,
-                 rank: int, world: int, group=None):
+                 rank: int, world: int, group=None, iterative: bool = False):
         import torch
         import torch.distributed as dist
 
@@ -177,6 +190,9 @@ class Csr5Sharded:
         self.ranges = [(t[4 * g], t[4 * g + 1]) for g in range(world)]
         self.exchange = os.environ.get("CSR5G_EXCHANGE", "p2p")
         self.mailbox = None
+        self.iterative = iterative and self.exchange == "p2p"
+        if self.iterative and m != n:
+            raise ValueError("iterative mode needs a square matrix")
         if self.exchange == "p2p":
             w = self.world_eff
             firsts = [(t[4 * g + 2], t[4 * g + 3]) for g in range(w)]
@@ -191,7 +207,8 @@ class Csr5Sharded:
         torch, dist = self.torch, self.dist
         L = lib()
         mb = C.c_void_p()
-        check(L.csr5g_mailbox_create(dev.index or 0, self.world, self.rank, C.byref(mb)))
+        check(L.csr5g_mailbox_create(dev.index or 0, self.world, self.rank,
+                                     self.m if self.iterative else 0, C.byref(mb)))
         self.mailbox = mb
         hbuf = (C.c_uint8 * IPC_HANDLE_BYTES)()
         check(L.csr5g_mailbox_ipc_handle(mb, hbuf))
@@ -211,10 +228,14 @@ class Csr5Sharded:
             return
         d = self.dest[self.rank]
         sb, se = self.senders[self.rank]
-        for peer in sorted(set(([d] if d >= 0 else []) + list(range(sb, se)))):
+        peers = set(([d] if d >= 0 else []) + list(range(sb, se)))
+        if self.iterative:  # every active rank stores its rows of the next x here
+            peers |= set(range(self.world_eff))
+        peers.discard(self.rank)
+        for peer in sorted(peers):
             h = allh[IPC_HANDLE_BYTES * peer:IPC_HANDLE_BYTES * (peer + 1)]
             check(L.csr5g_mailbox_open_peer(mb, peer, (C.c_uint8 * IPC_HANDLE_BYTES)(*h.tolist())))
-        check(L.csr5g_mg_bind(self.a5.handle, mb, d, sb, se))
+        check(L.csr5g_mg_bind(self.a5.handle, mb, d, sb, se, self.world_eff))
 
     def mailbox_errors(self) -> int:
         """Protocol violations seen by this rank's fix-ups (synchronous)."""
@@ -279,6 +300,34 @@ class Csr5Sharded:
         torch.cuda.current_stream().synchronize()
         self.dist.barrier(group=self.group)
         return y
+
+    def x_buffer(self, which: int):
+        """Iterative mode: this rank's x buffer `which` (x_k = x_buffer(k & 1)) as
+        a torch view of the mailbox memory (no copy)."""
+        p = C.c_void_p()
+        check(lib().csr5g_mailbox_vector(self.mailbox, which, C.byref(p)))
+        return _device_view(p.value, self.m, self.torch.cuda.current_device())
+
+    def spmv_iter(self, it: int, events=None):
+        """Fused iterative step: x_{it+1} = A x_it in the mailbox buffers, every
+        rank's owned rows stored into every peer's buffer by the SpMV kernels
+        themselves (csr5g_mg_iter).  Returns this rank's x_{it+1} view."""
+        torch, L = self.torch, lib()
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        ev = (events[0].p, events[1].p) if events is not None else (None, None)
+        if not self.shared_gpu:
+            if self.active:
+                check(L.csr5g_mg_iter(self.a5.handle, it, stream, ev[0], ev[1]))
+            return self.x_buffer(it + 1)
+        if self.active:
+            check(L.csr5g_mg_iter_post(self.a5.handle, it, stream, ev[0], ev[1]))
+        torch.cuda.current_stream().synchronize()
+        self.dist.barrier(group=self.group)
+        if self.active:
+            check(L.csr5g_mg_iter_finish(self.a5.handle, it, stream))
+        torch.cuda.current_stream().synchronize()
+        self.dist.barrier(group=self.group)
+        return self.x_buffer(it + 1)
 
     def gather_y_into_x(self, y, x):
         """Iterative mode (square A): every rank's x <- the owned ranges of y,
@@ -383,14 +432,14 @@ def emulate_p2p_on_one_device(a, xs, sigma: int, world: int):
     boxes = []
     for g in range(w):
         mb = C.c_void_p()
-        check(L.csr5g_mailbox_create(torch.cuda.current_device(), w, g, C.byref(mb)))
+        check(L.csr5g_mailbox_create(torch.cuda.current_device(), w, g, 0, C.byref(mb)))
         boxes.append(mb)
     try:
         for g in range(w):
             peers = set(([dest[g]] if dest[g] >= 0 else []) + list(range(*senders[g])))
             for p in sorted(peers):
                 check(L.csr5g_mailbox_link_local(boxes[g], p, boxes[p]))
-            check(L.csr5g_mg_bind(shards[g].handle, boxes[g], dest[g], *senders[g]))
+            check(L.csr5g_mg_bind(shards[g].handle, boxes[g], dest[g], *senders[g], w))
         stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         outs = []
         for x in xs:
@@ -413,6 +462,67 @@ def emulate_p2p_on_one_device(a, xs, sigma: int, world: int):
             errs.append(e.value)
         return outs, errs, dest, senders
     finally:
+        for s in shards:
+            s.release()
+        for mb in boxes:
+            L.csr5g_mailbox_release(mb)
+
+
+def emulate_p2p_iterative_on_one_device(a, x0, sigma: int, world: int, iters: int):
+    """The fused iterative mode (csr5g_mg_iter) with every shard in this
+    process on one device: per iteration all posts, then all finishes, on one
+    stream (each stream wait already satisfied).  Returns, per iteration, the
+    x_{k+1} buffer of every shard (they must agree bit for bit), and the
+    mailbox errors."""
+    import torch
+
+    L = lib()
+    assert a.m == a.n
+    shards = _shards_on_device(a, sigma, world)
+    w = len(shards)
+    infos = [s.info for s in shards]
+    owns = [(i.own_row_begin, i.own_row_end) for i in infos]
+    firsts = [(i.first_row, int(g == 0 or i.own_row_begin == i.first_row))
+              for g, i in enumerate(infos)]
+    dest, senders = plan_exchange(firsts, owns)
+    dev = torch.cuda.current_device()
+    boxes = []
+    for g in range(w):
+        mb = C.c_void_p()
+        check(L.csr5g_mailbox_create(dev, w, g, a.m, C.byref(mb)))
+        boxes.append(mb)
+    try:
+        for g in range(w):
+            for p in range(w):
+                if p != g:
+                    check(L.csr5g_mailbox_link_local(boxes[g], p, boxes[p]))
+            check(L.csr5g_mg_bind(shards[g].handle, boxes[g], dest[g], *senders[g], w))
+
+        def buf(g, which):
+            p = C.c_void_p()
+            check(L.csr5g_mailbox_vector(boxes[g], which, C.byref(p)))
+            return _device_view(p.value, a.m, dev)
+
+        xd = torch.as_tensor(np.ascontiguousarray(x0, np.float64)).cuda()
+        for g in range(w):
+            buf(g, 0).copy_(xd)
+            buf(g, 1).fill_(float("nan"))
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        outs = []
+        for it in range(iters):
+            for g in reversed(range(w)):
+                check(L.csr5g_mg_iter_post(shards[g].handle, it, stream, None, None))
+            for g in range(w):
+                check(L.csr5g_mg_iter_finish(shards[g].handle, it, stream))
+            outs.append([buf(g, it + 1).cpu().numpy() for g in range(w)])
+        errs = []
+        for mb in boxes:
+            e = C.c_uint32()
+            check(L.csr5g_mailbox_errors(mb, C.byref(e)))
+            errs.append(e.value)
+        return outs, errs
+    finally:
+        torch.cuda.synchronize()
         for s in shards:
             s.release()
         for mb in boxes:

@@ -259,6 +259,32 @@ def test_p2p_exchange_on_one_device(g, orc):
             assert max(se - sb for sb, se in senders) >= 2, senders
 
 
+def test_p2p_fused_iterative_on_one_device(g, orc):
+    """Fused iterative mode (csr5g_mg_iter): every final y value also stored
+    into each peer's next-x buffer by the kernels producing it.  After every
+    iteration all shards hold the same x_{k+1} bit for bit, equal to the
+    sharded SpMV of x_k (collective form) and within tolerance of the oracle."""
+    from paper_1503_05032_b200 import mg
+    rng = orc.rng(11)
+    cases = [orc.generate_synthetic(1, 30000, 30000, 60000, 3, 0.3),  # a long row spans shards
+             orc.generate_synthetic(2, 5000, 5000, 120000, 4),
+             orc.generate_synthetic(0, 2000, 2000, 54000, 5)]
+    for a in cases:
+        sigma = orc.select_sigma(a.nnz / a.m)
+        x0 = rng.random_x(a.n) / 32.0
+        for world in (2, 3, 8):
+            outs, errs = mg.emulate_p2p_iterative_on_one_device(a, x0, sigma, world, 3)
+            assert errs == [0] * len(errs), (world, errs)
+            x = x0
+            for it, bufs in enumerate(outs):
+                for b in bufs[1:]:
+                    assert np.array_equal(b, bufs[0]), f"world={world} it={it}: shards disagree"
+                y_coll = mg.emulate_shards_on_one_device(a, x, sigma, world)
+                assert np.array_equal(bufs[0], y_coll), f"world={world} it={it}: != sharded SpMV"
+                assert_y_close(bufs[0], orc.spmv(a, x, 32, sigma), a, x, f"iter {it} world={world}")
+                x = bufs[0]
+
+
 def test_host_vector_paths(g, orc):
     """csr5g_spmv_host and the pipelined csr5g_spmv_host_batch (pinned and
     pageable host vectors, batches longer than the two buffer pairs, a second
