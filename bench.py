@@ -141,7 +141,8 @@ def workload_n(workload: dict) -> int:
     return 1 << (workload["scale"] if workload["gen"] == "rmat" else workload["log2_m"])
 
 
-def reference_cpu(workload: dict, x, budget_s: float, omega=4, sigma=16, steps=None, warmup=0):
+def reference_cpu(workload: dict, x, budget_s: float, omega=4, sigma=16, steps=None, warmup=0,
+                  also_w32=False):
     """Time the reference csr5::spmv_csr5 (deterministic) on the host cores.
 
     steps=None: the bench.cpp:147-160 protocol (samples of `inner` back-to-back
@@ -176,11 +177,23 @@ def reference_cpu(workload: dict, x, budget_s: float, omega=4, sigma=16, steps=N
     scalar = ref.L.ref_time_csr_scalar(h, xv, yp, 3)
     ref.L.ref_time_spmv(h, xv, yp, 0, 1)  # leave y = the csr5 result
     threads = ref.max_threads()
+    w32 = None
+    if also_w32:  # the GPU's own omega = 32, sigma = auto on the CPU too
+        from oracle.oracle import Oracle
+        s32 = Oracle().select_sigma(a.nnz / max(a.m, 1))
+        h32, conv32 = ref.build_handle(a, 32, s32)
+        y32 = np.zeros(a.m)
+        p32 = y32.ctypes.data_as(dp)
+        one = ref.L.ref_time_spmv(h32, xv, p32, 0, 1)
+        inner32 = max(1, int(0.5 / max(one / 1e3, 1e-6)))
+        best = min(ref.L.ref_time_spmv(h32, xv, p32, 0, inner32) for _ in range(3))
+        ref.L.ref_free(h32)
+        w32 = dict(omega=32, sigma=s32, best_ms=best, conv_ms=conv32, inner=inner32)
     ref.L.ref_vec_free(xv)
     ref.L.ref_free(h)
     return dict(nnz=a.nnz, m=a.m, best_ms=min(samples), mean_ms=sum(samples) / len(samples),
                 samples=samples, inner=inner, conv_ms=conv_ms, gen_s=gen_s, threads=threads,
-                csr_scalar_ms=scalar, omega=omega, sigma=sigma, y=y)
+                csr_scalar_ms=scalar, omega=omega, sigma=sigma, y=y, w32=w32)
 
 
 def est_nnz(wl: dict) -> int:
@@ -599,9 +612,10 @@ def run_ours(args, workload_name, workload):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                r = reference_cpu(workload, x_host, budget_s=args.cpu_seconds)
+                r = reference_cpu(workload, x_host, budget_s=args.cpu_seconds, also_w32=True)
                 model, ncpu = cpu_info()
                 yr = r.pop("y")
+                w32 = r.pop("w32")
                 cpu = {"value": 2.0 * r["nnz"] / (r["best_ms"] * 1e6), "unit": UNIT,
                        "cores": r["threads"], "kind": "reference",
                        "sample": (f"full {workload_name} matrix, reference csr5::spmv_csr5 "
@@ -611,7 +625,11 @@ def run_ours(args, workload_name, workload):
                        "conv_spmv_equiv": r["conv_ms"] / r["best_ms"],
                        "csr_scalar_gflops": 2.0 * r["nnz"] / (r["csr_scalar_ms"] * 1e6),
                        "y_max_rel_err_vs_gpu": float(np.max(np.abs(yr - y.cpu().numpy()) /
-                                                            np.maximum(1.0, np.abs(yr))))}
+                                                            np.maximum(1.0, np.abs(yr)))),
+                       "omega32": {"sigma": w32["sigma"],
+                                   "gflops": 2.0 * r["nnz"] / (w32["best_ms"] * 1e6),
+                                   "conv_ms": w32["conv_ms"],
+                                   "sample": f"best of 3 samples x {w32['inner']} calls"}}
             except Exception as e:  # the CPU number is reported, never gating
                 cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                        "sample": f"failed: {e}"}
