@@ -55,6 +55,15 @@ def test_no_cpu_fallback_without_gpu():
     rc = L.csr5g_build(0, 0, 0, 0, None, None, None, C.byref(p), None, C.byref(h))
     assert rc == _lib.ECUDA
     assert "CUDA" in L.csr5g_last_error().decode() or "device" in L.csr5g_last_error().decode()
+    # the multi-GPU exchange: argument errors first (reference-style EINVAL),
+    # then no device -> ECUDA, never a host stand-in
+    mb = C.c_void_p()
+    assert L.csr5g_mailbox_create(0, 0, 0, 0, C.byref(mb)) == _lib.EINVAL
+    assert L.csr5g_mailbox_create(0, 2, 2, 0, C.byref(mb)) == _lib.EINVAL
+    assert L.csr5g_mailbox_create(0, 2, 0, -1, C.byref(mb)) == _lib.EINVAL
+    assert L.csr5g_mailbox_create(0, 2, 0, 16, C.byref(mb)) == _lib.ECUDA
+    assert L.csr5g_mg_spmv(None, None, None, None, None, None) == _lib.EINVAL
+    assert L.csr5g_mg_iter(None, 0, None, None, None) == _lib.EINVAL
 
 
 def test_stencil_box_sizes_and_weak_scaling():
