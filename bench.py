@@ -622,6 +622,9 @@ def run_ours(args, workload_name, workload):
                                   f"omega={r['omega']} sigma={r['sigma']} deterministic; best of "
                                   f"{len(r['samples'])} samples x {r['inner']} calls"),
                        "cpu_model": model, "nproc": ncpu, "conv_ms": r["conv_ms"],
+                       # the reference's own widths (8 B val + 8 B
+                       # col_idx), x and y once; its small metadata excluded
+                       "gbs_ref_widths": (16 * r["nnz"] + 8 * (m + n)) / (r["best_ms"] * 1e6),
                        "conv_spmv_equiv": r["conv_ms"] / r["best_ms"],
                        "csr_scalar_gflops": 2.0 * r["nnz"] / (r["csr_scalar_ms"] * 1e6),
                        "y_max_rel_err_vs_gpu": float(np.max(np.abs(yr - y.cpu().numpy()) /
