@@ -282,6 +282,19 @@ def run_ours(args, workload_name, workload):
     from paper_1503_05032_b200 import csr5, mg
     from paper_1503_05032_b200.synthetic import bench_x
     rank, world, local = dist_env()
+    if world > 1:
+        # a rank that never sees a peer's flag would block its stream forever:
+        # turn such a hang into a loud failure (the whole run takes minutes)
+        limit = float(os.environ.get("CSR5G_WATCHDOG_S", "900"))
+
+        def _watchdog():
+            time.sleep(limit)
+            sys.stderr.write(f"bench.py rank {rank}: no completion after {limit:.0f} s "
+                             "(multi-GPU exchange stalled?); aborting\n")
+            sys.stderr.flush()
+            os._exit(3)
+
+        threading.Thread(target=_watchdog, daemon=True).start()
     if os.environ.get("CSR5G_SHARE_GPU") == "1":  # functional multi-rank check on one GPU
         local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
