@@ -480,11 +480,16 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       auto write_back = [&](auto eo_at, auto slot_at) {
         c0 = slot_at(1);
         cL = slot_at(H);
-        const int nch = (H + 31) >> 5;
+        // an unflagged tile has no empty row in [tile_row, next_row]: its last
+        // head is row tile_row + H - 1 and nothing after it needs zeroing, so
+        // the loop stops before it (H = 33, common at sigma * 32 = rows * nnz/row
+        // plus one partial row, then takes one trip instead of two)
+        const int hend = flagged ? H : H - 1;
+        const int nch = (hend + 31) >> 5;
   #pragma unroll 1
         for (int c = 0; c < nch; ++c) {  // warp-uniform trip count
           const int h = lane + 32 * c;
-          if (h >= H) break;
+          if (h >= hend) break;
           const int64_t r = tile_row + (flagged ? (int64_t)eo_at(h) : (int64_t)h);
           if (h == H - 1) rL = r;
           if (h != 0 && h != H - 1) put_y(r, slot_at(h + 1));
@@ -505,8 +510,8 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
         write_back([&](int i) { return eos[i]; }, [&](int i) { return closed[i]; });
       else
         write_back([&](int i) { return eo[i]; }, [&](int i) { return spill[i]; });
-      rL = __shfl_sync(kFull, rL, (H - 1) & 31);
-      uint32_t dm = __ballot_sync(kFull, defer_hi > defer_lo);
+      rL = flagged ? __shfl_sync(kFull, rL, (H - 1) & 31) : tile_row + H - 1;
+      uint32_t dm = flagged ? __ballot_sync(kFull, defer_hi > defer_lo) : 0u;
       while (dm) {  // long empty-row runs: zero cooperatively
         const int src = __ffs(dm) - 1;
         dm &= dm - 1;
