@@ -506,6 +506,7 @@ def run_ours(args, workload_name, workload):
     e2e_serial_ms = e2e_timed(lambda: [e2e_serial(k) for k in range(args.steps)])
     e2e_path = "serial: pinned x H2D + spmv + y D2H per step, one stream, CUDA events"
     e2e_ms = e2e_serial_ms
+    pcie_ms = None
     if world == 1:
         xs = [xh[k % ring] for k in range(args.steps)]
         ys = [yh[k % ring] for k in range(args.steps)]
@@ -517,6 +518,25 @@ def run_ours(args, workload_name, workload):
         err_h = float(np.max(np.abs(yh[(args.steps - 1) % ring].numpy() - y.cpu().numpy())))
         if err_h != 0.0:
             raise SystemExit(f"host-batch path differs from the device path by {err_h}")
+        # the PCIe ceiling of this e2e: the same per-step copies (x in, y out,
+        # concurrently on two streams) with no SpMV at all
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        xd2, yd2 = torch.empty_like(x), y.clone()
+
+        def duplex():
+            cur = torch.cuda.current_stream()
+            s_in.wait_stream(cur)
+            s_out.wait_stream(cur)
+            for k in range(args.steps):
+                with torch.cuda.stream(s_in):
+                    xd2.copy_(xh[k % ring], non_blocking=True)
+                with torch.cuda.stream(s_out):
+                    yh[k % ring].copy_(yd2, non_blocking=True)
+            cur.wait_stream(s_in)
+            cur.wait_stream(s_out)
+
+        duplex()
+        pcie_ms = e2e_timed(duplex)
 
     # -- iteration scenario (bench.cpp:86-90, 164-175): the GPU plain-CSR
     # baseline beside CSR5, conversion amortised over n solver iterations ----
@@ -682,6 +702,8 @@ def run_ours(args, workload_name, workload):
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * m,
                     "ms_per_step": e2e_ms, "path": e2e_path,
                     "serial_value": flops / (e2e_serial_ms * 1e6),
+                    "pcie_duplex_ms_per_step": pcie_ms if world == 1 else None,
+                    "frac_of_pcie_duplex": (pcie_ms / e2e_ms) if world == 1 else None,
                     "serial_ms_per_step": e2e_serial_ms},
             "gpu_launches": args.steps * (2 if world == 1 else 3),
             "clocks": clk,
