@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <climits>
 #include <chrono>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(128) k_desc_transpose(
   const uint64_t flags = __brevll(bits) >> (64 - sigma);  // depth j at bit sigma-1-j
   desc[k * 32 + lane] =
       (W)(((uint64_t)yoff << (kSegBits + sigma)) | ((uint64_t)seg << sigma) | flags);
-  if (lane == 0) eo_cnt[k] = (tile_ptr[k] >> 31) ? H : 0;
+  if (eo_cnt && lane == 0) eo_cnt[k] = (tile_ptr[k] >> 31) ? H : 0;
 
   // ---- transpose: logical i*sigma+j -> physical j*32+i (format.hpp:76-88) ----
   const uint64_t pol = policy_evict_first();
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(512) k_desc_transpose_tma(
     const uint64_t flags = __brevll(bits) >> (64 - sigma);
     desc[k * 32 + lane] =
         (W)(((uint64_t)yoff << (kSegBits + sigma)) | ((uint64_t)seg << sigma) | flags);
-    if (lane == 0) eo_cnt[k] = (tile_ptr[k] >> 31) ? H : 0;
+    if (eo_cnt && lane == 0) eo_cnt[k] = (tile_ptr[k] >> 31) ? H : 0;
 
     // ---- transpose: logical i*sigma+j -> physical j*32+i (format.hpp:76-88) ----
     mbar_wait(bars + st, phase);
@@ -308,14 +309,17 @@ __global__ void k_eo(const uint32_t* __restrict__ head_bits, const uint32_t* __r
 // 3.90, (0,1) 1.91, (1,1) 1.87, (4,2) 1.79 ms.
 __global__ void k_tile_work(const uint32_t* __restrict__ head_bits,
                             const uint32_t* __restrict__ tile_ptr, int64_t pcs, int sigma,
-                            int w_head, int w_row, int64_t* __restrict__ work) {
+                            int w_head, int w_row, int64_t* __restrict__ work,
+                            int64_t* __restrict__ eo_cnt) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= pcs) return;
   const uint32_t* wd = head_bits + t * sigma;  // a tile is sigma 32-bit words
   int heads = (wd[0] & 1u) ? 0 : 1;           // bf[0] is forced
   for (int i = 0; i < sigma; ++i) heads += __popc(wd[i]);
-  const int64_t rows = (int64_t)(tile_ptr[t + 1] & 0x7fffffffu) - (tile_ptr[t] & 0x7fffffffu) + 1;
+  const uint32_t tp = tile_ptr[t];
+  const int64_t rows = (int64_t)(tile_ptr[t + 1] & 0x7fffffffu) - (tp & 0x7fffffffu) + 1;
   work[t] = 32ll * sigma + (int64_t)w_head * heads + (int64_t)w_row * rows;
+  eo_cnt[t] = (tp >> 31) ? heads : 0;  // empty_offset entries: heads of flagged tiles
 }
 
 // Largest per-warp work of the equal-tile split (atomicMax into *out).
@@ -457,6 +461,18 @@ __global__ void k_untranspose(const int32_t* __restrict__ col_in, const double* 
 // paying cudaMalloc's page mapping again (allocation is reported separately,
 // as the paper separates it from conversion).
 thread_local cudaStream_t t_alloc_stream = nullptr;
+
+// Per-device side stream of the converter: the empty_offset / plan chain runs
+// on it while the transposition streams the matrix on the caller's stream.
+int side_stream(int device, cudaStream_t* out) {
+  static std::mutex mu;
+  static cudaStream_t side[64] = {};
+  if (device < 0 || device >= 64) return fail(CSR5G_EINVAL, "csr5g: device id out of range");
+  std::lock_guard<std::mutex> lock(mu);
+  if (!side[device]) CSR5G_CUDA(cudaStreamCreateWithFlags(&side[device], cudaStreamNonBlocking));
+  *out = side[device];
+  return CSR5G_OK;
+}
 
 int ensure_pool(int device) {
   static bool done[64] = {};
@@ -622,10 +638,16 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   void* cub_tmp = nullptr;
   void* cub_tmp2 = nullptr;
   int64_t* work_prefix = nullptr;
+  int64_t* work = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   auto cleanup = [&](int code) {
+    if (side && code) cudaStreamSynchronize(side);  // error path: side work may be in flight
     for (void* p : {(void*)head_bits, (void*)empty_bits, (void*)eo_cnt, (void*)scal, cub_tmp,
-                    cub_tmp2, (void*)work_prefix})
+                    cub_tmp2, (void*)work_prefix, (void*)work})
       if (p) cudaFreeAsync(p, stream);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (code) free_handle(h);
     return code;
   };
@@ -679,6 +701,14 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     TRYC(cudaMemsetAsync(h->tile_ptr, 0, sizeof(uint32_t), stream));  // encode_tile_ptr(0)
   }
   trace.mark("tile_ptr");
+  // ---- fork: the transposition streams the matrix on `stream` while the
+  // empty_offset chain (head counts, scans, host scalars, k_eo) and the warp
+  // plan's work prefix run on the side stream ----
+  TRY(side_stream(device, &side));
+  TRYC(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  TRYC(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  TRYC(cudaEventRecord(ev_fork, stream));
+  TRYC(cudaStreamWaitEvent(side, ev_fork, 0));
   if (pcs > 0) {
     // TMA-fed kernel when the input tiles are 16-byte aligned (B*8 and B*4 are
     // multiples of 16 for every sigma); the register-load kernel otherwise
@@ -697,13 +727,13 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
         TRYC(cudaFuncSetAttribute(k_desc_transpose_tma<uint64_t>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_desc_transpose_tma<uint64_t><<<grid, 32 * nw, smem, stream>>>(
-            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint64_t*)h->desc, eo_cnt,
+            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint64_t*)h->desc, nullptr,
             pcs, (int)sigma, stage_bytes);
       } else {
         TRYC(cudaFuncSetAttribute(k_desc_transpose_tma<uint32_t>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_desc_transpose_tma<uint32_t><<<grid, 32 * nw, smem, stream>>>(
-            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint32_t*)h->desc, eo_cnt,
+            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint32_t*)h->desc, nullptr,
             pcs, (int)sigma, stage_bytes);
       }
     } else {
@@ -713,13 +743,13 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
         TRYC(cudaFuncSetAttribute(k_desc_transpose<uint64_t>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_desc_transpose<uint64_t><<<grid, 128, smem, stream>>>(
-            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint64_t*)h->desc, eo_cnt,
+            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint64_t*)h->desc, nullptr,
             pcs, (int)sigma);
       } else {
         TRYC(cudaFuncSetAttribute(k_desc_transpose<uint32_t>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_desc_transpose<uint32_t><<<grid, 128, smem, stream>>>(
-            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint32_t*)h->desc, eo_cnt,
+            head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint32_t*)h->desc, nullptr,
             pcs, (int)sigma);
       }
     }
@@ -732,45 +762,49 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
                          cudaMemcpyDeviceToDevice, stream));
   }
   trace.mark("desc_transpose");
-  // empty_offset_ptr: exclusive scan of per-tile head counts (format.cpp:213-217)
-  size_t cub_bytes = 0;
-  TRYC(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, eo_cnt, h->eo_ptr, (int)(pcs + 1), stream));
-  TRY(dev_alloc(reinterpret_cast<char**>(&cub_tmp), cub_bytes, &alloc_ms, &tmp_bytes));
-  TRYC(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, eo_cnt, h->eo_ptr, (int)(pcs + 1), stream));
 
-  // Work prefix for the warps' tile ranges (eo_cnt is free after its scan).
+  // ---- side stream: per-tile head counts and work, empty_offset_ptr
+  // (exclusive scan, format.cpp:213-217), the work prefix, host scalars ----
+  t_alloc_stream = side;
+  static const int w_head = [] {
+    const char* e = std::getenv("CSR5G_WHEAD");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int w_row = [] {
+    const char* e = std::getenv("CSR5G_WROW");
+    return e ? std::atoi(e) : 1;
+  }();
   if (pcs > 0) {
-    static const int w_head = [] {
-      const char* e = std::getenv("CSR5G_WHEAD");
-      return e ? std::atoi(e) : 0;
-    }();
-    static const int w_row = [] {
-      const char* e = std::getenv("CSR5G_WROW");
-      return e ? std::atoi(e) : 1;
-    }();
-    k_tile_work<<<(unsigned)((pcs + 255) / 256), 256, 0, stream>>>(head_bits, h->tile_ptr, pcs,
-                                                                   (int)sigma, w_head, w_row,
-                                                                   eo_cnt);
+    TRY(dev_alloc(&work, (size_t)pcs, &alloc_ms, &tmp_bytes));
+    k_tile_work<<<(unsigned)((pcs + 255) / 256), 256, 0, side>>>(head_bits, h->tile_ptr, pcs,
+                                                                 (int)sigma, w_head, w_row, work,
+                                                                 eo_cnt);
     TRYC(cudaGetLastError());
+  }
+  size_t cub_bytes = 0;
+  TRYC(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, eo_cnt, h->eo_ptr, (int)(pcs + 1), side));
+  TRY(dev_alloc(reinterpret_cast<char**>(&cub_tmp), cub_bytes, &alloc_ms, &tmp_bytes));
+  TRYC(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, eo_cnt, h->eo_ptr, (int)(pcs + 1), side));
+  if (pcs > 0) {
     TRY(dev_alloc(&work_prefix, (size_t)pcs, &alloc_ms, &tmp_bytes));
     size_t need = 0;
-    TRYC(cub::DeviceScan::InclusiveSum(nullptr, need, eo_cnt, work_prefix, (int)pcs, stream));
+    TRYC(cub::DeviceScan::InclusiveSum(nullptr, need, work, work_prefix, (int)pcs, side));
     void* t2 = cub_tmp;
     if (need > cub_bytes) {
       TRY(dev_alloc(reinterpret_cast<char**>(&cub_tmp2), need, &alloc_ms, &tmp_bytes));
       t2 = cub_tmp2;
     }
-    TRYC(cub::DeviceScan::InclusiveSum(t2, need, eo_cnt, work_prefix, (int)pcs, stream));
+    TRYC(cub::DeviceScan::InclusiveSum(t2, need, work, work_prefix, (int)pcs, side));
   }
 
   // Scalars of the held range.
   int64_t ptr_first = 0, ptr_close = 0, eo_total = 0;
-  TRYC(cudaMemcpyAsync(&eo_total, h->eo_ptr + pcs, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  TRYC(cudaMemcpyAsync(&eo_total, h->eo_ptr + pcs, sizeof(int64_t), cudaMemcpyDeviceToHost, side));
   uint32_t tp0 = 0, tpc = 0;
-  TRYC(cudaMemcpyAsync(&tp0, h->tile_ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+  TRYC(cudaMemcpyAsync(&tp0, h->tile_ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, side));
   TRYC(cudaMemcpyAsync(&tpc, h->tile_ptr + (pcs < tile_ptr_len ? pcs : tile_ptr_len - 1),
-                       sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
-  TRYC(cudaStreamSynchronize(stream));
+                       sizeof(uint32_t), cudaMemcpyDeviceToHost, side));
+  TRYC(cudaStreamSynchronize(side));  // the transposition keeps running on `stream`
   trace.mark("scan");
   ptr_first = tp0 & 0x7fffffffu;
   ptr_close = tpc & 0x7fffffffu;
@@ -779,21 +813,23 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   const int64_t g0 = pcs > 0 ? tile_end * B - 1 : -1;
   const int64_t g1 = nnz > 0 ? nnz - 1 : -1;
   if (m > 0) {
-    k_scalars<<<1, 1, 0, stream>>>(h->row_ptr, m, g0, g1, ptr_first, ptr_close, scal);
+    k_scalars<<<1, 1, 0, side>>>(h->row_ptr, m, g0, g1, ptr_first, ptr_close, scal);
     TRYC(cudaGetLastError());
   }
   int64_t sv[4] = {-1, -1, -1, -1};
-  if (m > 0) TRYC(cudaMemcpyAsync(sv, scal, sizeof sv, cudaMemcpyDeviceToHost, stream));
+  if (m > 0) TRYC(cudaMemcpyAsync(sv, scal, sizeof sv, cudaMemcpyDeviceToHost, side));
   TRY(dev_alloc(&h->eo, (size_t)eo_total, &alloc_ms, &bytes));
   if (pcs > 0 && eo_total > 0) {
     const int64_t threads = pcs * 32;
-    k_eo<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(
+    k_eo<<<(unsigned)((threads + 255) / 256), 256, 0, side>>>(
         head_bits, h->tile_ptr, h->row_ptr, m, pcs, (int)sigma, pos0, h->eo_ptr, h->eo);
     TRYC(cudaGetLastError());
   }
+  TRYC(cudaEventRecord(ev_join, side));
+  t_alloc_stream = stream;
   trace.mark("eo");
-  // gather locality over up to 4096 sampled tiles (drives the SpMV plan); its
-  // counter sits after the four scalars, read back with them in one sync
+  // gather locality over up to 4096 sampled tiles (drives the SpMV plan), on
+  // `stream` after the transposition; its counter sits after the four scalars
   h->lines_per_gather = 1.0;
   unsigned long long lines = 0;
   const int64_t samples = std::min<int64_t>(pcs, 4096);
@@ -805,6 +841,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     TRYC(cudaGetLastError());
     TRYC(cudaMemcpyAsync(&lines, ctr, sizeof lines, cudaMemcpyDeviceToHost, stream));
   }
+  TRYC(cudaStreamWaitEvent(stream, ev_join, 0));  // join: eo, eo_ptr, scalars, work prefix
   TRYC(cudaStreamSynchronize(stream));
   if (pcs > 0) h->lines_per_gather = (double)lines / (double)(samples * sigma);
   trace.mark("locality");
