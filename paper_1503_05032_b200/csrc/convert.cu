@@ -684,8 +684,8 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRYC(cudaMemsetAsync(head_bits, 0, sizeof(uint32_t) * head_words, stream));
   TRYC(cudaMemsetAsync(empty_bits, 0, sizeof(uint32_t) * empty_words, stream));
   TRYC(cudaMemsetAsync(eo_cnt, 0, sizeof(int64_t) * (pcs + 1), stream));
-  const csr5g_partial none{-1, 0.0};
-  TRYC(cudaMemcpyAsync(h->send, &none, sizeof none, cudaMemcpyHostToDevice, stream));
+  TRYC(cudaMemsetAsync(&h->send->row, 0xff, sizeof(int64_t), stream));  // no record: row -1
+  TRYC(cudaMemsetAsync(&h->send->value, 0, sizeof(double), stream));
 
   const int64_t pos0 = tile_begin * B;
   trace.mark("init");
@@ -724,14 +724,12 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
       TRYC(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
       const unsigned grid = (unsigned)std::min<int64_t>((warps_needed + nw - 1) / nw, sms);
       if (h->wide) {
-        TRYC(cudaFuncSetAttribute(k_desc_transpose_tma<uint64_t>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TRY(func_attrs((const void*)k_desc_transpose_tma<uint64_t>, device, (int)smem, -1));
         k_desc_transpose_tma<uint64_t><<<grid, 32 * nw, smem, stream>>>(
             head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint64_t*)h->desc, nullptr,
             pcs, (int)sigma, stage_bytes);
       } else {
-        TRYC(cudaFuncSetAttribute(k_desc_transpose_tma<uint32_t>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TRY(func_attrs((const void*)k_desc_transpose_tma<uint32_t>, device, (int)smem, -1));
         k_desc_transpose_tma<uint32_t><<<grid, 32 * nw, smem, stream>>>(
             head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint32_t*)h->desc, nullptr,
             pcs, (int)sigma, stage_bytes);
@@ -740,14 +738,12 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
       const size_t smem = (size_t)4 * sigma * 33 * sizeof(double);
       const unsigned grid = (unsigned)((pcs + 3) / 4);
       if (h->wide) {
-        TRYC(cudaFuncSetAttribute(k_desc_transpose<uint64_t>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TRY(func_attrs((const void*)k_desc_transpose<uint64_t>, device, (int)smem, -1));
         k_desc_transpose<uint64_t><<<grid, 128, smem, stream>>>(
             head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint64_t*)h->desc, nullptr,
             pcs, (int)sigma);
       } else {
-        TRYC(cudaFuncSetAttribute(k_desc_transpose<uint32_t>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TRY(func_attrs((const void*)k_desc_transpose<uint32_t>, device, (int)smem, -1));
         k_desc_transpose<uint32_t><<<grid, 128, smem, stream>>>(
             head_bits, h->tile_ptr, d_col_idx, d_val, h->col, h->val, (uint32_t*)h->desc, nullptr,
             pcs, (int)sigma);

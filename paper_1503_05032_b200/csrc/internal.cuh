@@ -121,6 +121,7 @@ struct Handle {
   bool x_window = false;          // L2 persisting window on x
   bool vr = false;                // values outside the TMA ring (k_spmv<SIG, true>)
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
+  int carveout_pct = -1;  // preferred shared-memory carveout of the SpMV kernel
   Pipeline* pipe = nullptr;  // created by the first host-vector SpMV
 };
 
@@ -147,6 +148,7 @@ int launch_fixup(Handle* h, const csr5g_partial* d_all, int world, int rank, dou
                  cudaStream_t stream);
 int launch_to_csr(Handle* h, int32_t* d_col, double* d_val, cudaStream_t stream);
 int spmv_plan(Handle* h, int sms);
+int func_attrs(const void* fn, int device, int smem, int carve);
 int spmv_host_batch(Handle* h, const double* const* xs, double* const* ys, int64_t count,
                     int mode, cudaStream_t stream);
 void free_pipeline(Pipeline* p);

@@ -30,6 +30,9 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <type_traits>
 
 #include "internal.cuh"
@@ -682,25 +685,38 @@ int spmv_plan(Handle* h, int sms) {
   h->stage_bytes = stage_bytes;
   h->bar_bytes = bars(nw, stages);
   h->smem_bytes = need(nw, stages);
-  CSR5G_CUDA(cudaFuncSetAttribute(spmv_fn((int)h->info.sigma, h->vr),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
   // Ask for the smallest shared-memory carveout that holds the ring: the rest
   // of the SM's 256 KB stays L1, which is where outstanding gather misses land
   // (measured: a 233 KB carveout halves R-MAT throughput through mio/lg
-  // throttling).
+  // throttling).  The attributes are set per launch (func_attrs): handles of
+  // one sigma can carry different plans.
   {
     int max_smem = 0;
     CSR5G_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
                                       h->device));
     const int need_bytes = h->smem_bytes + 1024;  // + the per-CTA reserved 1 KB
     int pct = (int)((100LL * need_bytes + max_smem - 1) / max_smem);
-    pct = std::min(100, std::max(0, pct));
-    CSR5G_CUDA(cudaFuncSetAttribute(spmv_fn((int)h->info.sigma, h->vr),
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    h->carveout_pct = std::min(100, std::max(0, pct));
   }
   const int64_t max_warps = (int64_t)sms * nw;
   h->nwarps = (int)std::min<int64_t>(max_warps, h->pcs);
   h->tile_blocks = (h->nwarps + nw - 1) / nw;
+  return CSR5G_OK;
+}
+
+// Kernel attributes (dynamic shared memory, carveout) as the handle's plan
+// needs them, set only when they differ from the last values set on that
+// device (a host-side map lookup per launch).
+int func_attrs(const void* fn, int device, int smem, int carve) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, std::pair<int, int>> cur;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cur.find({fn, device});
+  if (it != cur.end() && it->second == std::make_pair(smem, carve)) return CSR5G_OK;
+  CSR5G_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (carve >= 0)
+    CSR5G_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+  cur[{fn, device}] = {smem, carve};
   return CSR5G_OK;
 }
 
@@ -827,6 +843,9 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
       cfg.attrs = attr;
       cfg.numAttrs = 1;
     }
+    if (int rc = func_attrs((const void*)spmv_fn(a.sigma, h->vr), h->device, h->smem_bytes,
+                            h->carveout_pct))
+      return rc;
     CSR5G_CUDA(cudaLaunchKernelEx(&cfg, spmv_fn(a.sigma, h->vr), a));
   }
   if (ev1) CSR5G_CUDA(cudaEventRecord(ev1, stream));
@@ -844,9 +863,9 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     CSR5G_CUDA(cudaLaunchKernelEx(&cfg, k_calibrate, (const int64_t*)h->item_row,
                                   (const double*)h->item_val, items, d_y, h->first_row,
                                   (int)h->first_owned, a.send, h->send_flag, h->send_epoch, h->mir));
-  } else if (!atomic) {
-    const csr5g_partial none{-1, 0.0};
-    CSR5G_CUDA(cudaMemcpyAsync(a.send, &none, sizeof none, cudaMemcpyHostToDevice, stream));
+  } else if (!atomic) {  // no record: row -1 (all ones), value 0.0
+    CSR5G_CUDA(cudaMemsetAsync(&a.send->row, 0xff, sizeof(int64_t), stream));
+    CSR5G_CUDA(cudaMemsetAsync(&a.send->value, 0, sizeof(double), stream));
   }
   return CSR5G_OK;
 }

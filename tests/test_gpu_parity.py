@@ -285,6 +285,30 @@ def test_p2p_fused_iterative_on_one_device(g, orc):
                 x = bufs[0]
 
 
+def test_two_plans_of_one_kernel(g, orc):
+    """Two live handles whose plans differ for the same sigma-specialised
+    kernel (banded: local gathers, large shared-memory ring; random columns:
+    random plan, smaller ring): each SpMV launches with its own plan, in any
+    order (kernel attributes follow the launch, not the last build)."""
+    rng = np.random.default_rng(3)
+    m = n = 20000
+    rows = np.repeat(np.arange(m), 27)
+    band = (rows + np.tile(np.arange(27), m)) % n
+    rnd = rng.integers(0, n, rows.size)
+    mats = []
+    for cols in (band, rnd):
+        a = orc.coo_to_csr(rows.tolist(), cols.tolist(), np.linspace(0.5, 1.5, rows.size), m, n)
+        mats.append(a)
+    hs = [gpu_build(g, a, 27) for a in mats]
+    assert hs[0].info.smem_bytes != hs[1].info.smem_bytes, "plans should differ"
+    x = orc.rng(4).random_x(n)
+    for order in ((0, 1), (1, 0), (0, 0, 1, 1, 0)):
+        for i in order:
+            assert_y_close(gpu_y(g, hs[i], x), orc.spmv(mats[i], x, 32, 27), mats[i], x, f"plan {i}")
+    for h in hs:
+        h.release()
+
+
 def test_host_vector_paths(g, orc):
     """csr5g_spmv_host and the pipelined csr5g_spmv_host_batch (pinned and
     pageable host vectors, batches longer than the two buffer pairs, a second
