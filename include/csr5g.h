@@ -117,7 +117,9 @@ CSR5G_API int csr5g_export(csr5g_matrix h, uint64_t *h_tile_ptr, uint64_t *h_til
 
 /* spmv.cpp:224-298 spmv_csr5 (spmv.hpp:58): y = A x, y fully overwritten
  * (rows own_row_begin..own_row_end for a shard).  Stream-ordered, no sync.
- * Not re-entrant on one handle across concurrent streams (one scratch). */
+ * Concurrent calls on one handle from distinct streams are safe: every
+ * stream gets its own scratch (the reference's per-worker workspaces,
+ * spmv.hpp:27-38). */
 CSR5G_API int csr5g_spmv(csr5g_matrix h, const double *d_x, double *d_y, int32_t mode, void *stream);
 
 /* Same, recording ev_tiles_begin / ev_tiles_end (from csr5g_event_create)

@@ -568,6 +568,8 @@ void free_handle(Handle* h) {
                   (void*)h->col, (void*)h->val, (void*)h->item_row, (void*)h->item_val,
                   (void*)h->send, (void*)h->spill, (void*)h->warp_begin})
     if (p) cudaFreeAsync(p, 0);
+  for (const StreamScratch& x : h->extra_scratch)
+    for (void* p : {(void*)x.item_row, (void*)x.item_val, (void*)x.spill}) cudaFreeAsync(p, 0);
   cudaDeviceSynchronize();
   cudaSetDevice(prev);
   delete h;

@@ -15,7 +15,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/csr5g.h"
 
@@ -88,6 +90,16 @@ struct SpmvArgs {
 };
 
 struct Pipeline;  // pipeline.cu: host-vector copy/compute pipeline
+
+// Per-stream SpMV scratch (the reference's per-worker workspaces,
+// spmv.hpp:27-38): concurrent spmv calls on one handle from distinct streams
+// each get their own run items and closed-segment spill area.
+struct StreamScratch {
+  cudaStream_t stream;
+  int64_t* item_row;
+  double* item_val;
+  double* spill;
+};
 struct Binding;   // p2p.cu: a shard's NVLink boundary exchange
 
 struct Handle {
@@ -122,6 +134,12 @@ struct Handle {
   bool vr = false;                // values outside the TMA ring (k_spmv<SIG, true>)
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
   int carveout_pct = -1;  // preferred shared-memory carveout of the SpMV kernel
+  // scratch of streams other than the first one that ran an SpMV (which uses
+  // item_row / item_val / spill above); guarded by scratch_mu
+  bool scratch_claimed = false;
+  cudaStream_t scratch_stream = nullptr;
+  std::vector<StreamScratch> extra_scratch;
+  std::mutex scratch_mu;
   Pipeline* pipe = nullptr;  // created by the first host-vector SpMV
 };
 

@@ -720,6 +720,45 @@ int func_attrs(const void* fn, int device, int smem, int carve) {
   return CSR5G_OK;
 }
 
+// The scratch of `stream`: the handle's own arrays for the first stream that
+// runs an SpMV on it, arrays allocated (stream-ordered) for every other one.
+int scratch_for(Handle* h, cudaStream_t stream, int64_t** ir, double** iv, double** sp) {
+  std::lock_guard<std::mutex> lock(h->scratch_mu);
+  if (!h->scratch_claimed) {
+    h->scratch_claimed = true;
+    h->scratch_stream = stream;
+  }
+  if (stream == h->scratch_stream) {
+    *ir = h->item_row;
+    *iv = h->item_val;
+    *sp = h->spill;
+    return CSR5G_OK;
+  }
+  for (const StreamScratch& x : h->extra_scratch)
+    if (x.stream == stream) {
+      *ir = x.item_row;
+      *iv = x.item_val;
+      *sp = x.spill;
+      return CSR5G_OK;
+    }
+  const size_t items = 2 * (size_t)h->nwarps + 1;
+  const size_t spill = (size_t)std::max(h->nwarps, 1) * (size_t)(h->B + 1);
+  StreamScratch x{stream, nullptr, nullptr, nullptr};
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&x.item_row), items * 8, stream);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&x.item_val), items * 8, stream);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&x.spill), spill * 8, stream);
+  if (e != cudaSuccess) {
+    for (void* p : {(void*)x.item_row, (void*)x.item_val, (void*)x.spill})
+      if (p) cudaFreeAsync(p, stream);
+    return cuda_fail(e, "per-stream SpMV scratch");
+  }
+  h->extra_scratch.push_back(x);
+  *ir = x.item_row;
+  *iv = x.item_val;
+  *sp = x.spill;
+  return CSR5G_OK;
+}
+
 int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_t stream,
                 cudaEvent_t ev0, cudaEvent_t ev1) {
   CSR5G_CUDA(cudaSetDevice(h->device));
@@ -745,10 +784,8 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.val = h->val;
   a.x = d_x;
   a.y = d_y;
-  a.item_row = h->item_row;
-  a.item_val = h->item_val;
+  if (int rc = scratch_for(h, stream, &a.item_row, &a.item_val, &a.spill)) return rc;
   a.send = h->send_ext ? h->send_ext : h->send;
-  a.spill = h->spill;
   static const bool equal_split = [] {  // A/B: equal tile counts per warp
     const char* e = std::getenv("CSR5G_EQUAL_SPLIT");
     return e && std::atoi(e) != 0;
@@ -860,8 +897,8 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = pdl;
     cfg.numAttrs = pdl_on ? 1 : 0;
-    CSR5G_CUDA(cudaLaunchKernelEx(&cfg, k_calibrate, (const int64_t*)h->item_row,
-                                  (const double*)h->item_val, items, d_y, h->first_row,
+    CSR5G_CUDA(cudaLaunchKernelEx(&cfg, k_calibrate, (const int64_t*)a.item_row,
+                                  (const double*)a.item_val, items, d_y, h->first_row,
                                   (int)h->first_owned, a.send, h->send_flag, h->send_epoch, h->mir));
   } else if (!atomic) {  // no record: row -1 (all ones), value 0.0
     CSR5G_CUDA(cudaMemsetAsync(&a.send->row, 0xff, sizeof(int64_t), stream));
