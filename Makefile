@@ -30,7 +30,7 @@ CXX_SYS  := $(if $(wildcard /usr/bin/g++),/usr/bin/g++,g++)
 shim: build/shim_test
 build/shim_test: tests/cpp/shim_test.cpp include/csr5g.hpp include/csr5g.h $(PKG)/libcsr5g.so
 	@mkdir -p build
-	$(CXX_SYS) -std=c++20 -O2 -Wall -Iinclude $< -L$(PKG) -lcsr5g \
+	$(CXX_SYS) -std=c++20 -O2 -Wall -pthread -Iinclude $< -L$(PKG) -lcsr5g \
 	  -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
 
 # measurement tool (random-gather ceiling), not part of the product

@@ -141,6 +141,7 @@ struct Handle {
   std::vector<StreamScratch> extra_scratch;
   std::mutex scratch_mu;
   Pipeline* pipe = nullptr;  // created by the first host-vector SpMV
+  std::mutex pipe_mu;        // host-vector calls from several threads enqueue one at a time
 };
 
 // ---- errors --------------------------------------------------------------

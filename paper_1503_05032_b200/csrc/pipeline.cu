@@ -82,6 +82,10 @@ int make_pipeline(Handle* h, Pipeline** out) {
 int spmv_host_batch(Handle* h, const double* const* xs, double* const* ys, int64_t count,
                     int mode, cudaStream_t stream) {
   CSR5G_CUDA(cudaSetDevice(h->device));
+  // concurrent host-vector calls on one handle (reference: spmv_csr5 from
+  // several threads) share its pipeline; their enqueues are serialised and the
+  // buffer-reuse events order the GPU work
+  std::lock_guard<std::mutex> lock(h->pipe_mu);
   Pipeline* p = nullptr;
   int rc = make_pipeline(h, &p);
   if (rc) return rc;

@@ -10,6 +10,8 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "csr5g.hpp"
 
@@ -143,6 +145,26 @@ int main() {
     }
     spmv_csr5_batch(a5, px, py);
     for (std::size_t k = 0; k < xs.size(); ++k) CHECK(ys[k] == spmv_csr5(a5, xs[k]));
+  }
+  // one matrix, spmv_csr5 from several host threads at once (the reference's
+  // types are shareable read-only): every result equals the
+  // single-threaded one bit for bit (deterministic mode)
+  {
+    const CsrMatrix a = random_csr(77, 900, 700, 0.05);
+    const Csr5Matrix a5 = csr_to_csr5(a);
+    const int T = 6;
+    std::vector<DenseVector> xs(T, DenseVector((std::size_t)a.n)), ref(T), got(T);
+    for (int t = 0; t < T; ++t) {
+      for (std::size_t i = 0; i < xs[t].size(); ++i) xs[t][i] = 0.5 + 0.003 * (double)((7 * i + t) % 331);
+      ref[t] = spmv_csr5(a5, xs[t]);
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([&, t] {
+        for (int r = 0; r < 20; ++r) got[t] = spmv_csr5(a5, xs[t]);
+      });
+    for (auto& x : th) x.join();
+    for (int t = 0; t < T; ++t) CHECK(got[t] == ref[t]);
   }
   // Matrix Market -> coo_to_csr on the device -> CSR5
   {
