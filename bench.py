@@ -669,6 +669,13 @@ def run_ours(args, workload_name, workload):
             except Exception as e:  # the CPU number is reported, never gating
                 cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                        "sample": f"failed: {e}"}
+        launches_per_step = 1
+        if world > 1 and sh.active:
+            if sh.exchange == "p2p":
+                sb, se = sh.senders[sh.rank]
+                launches_per_step += int(se > sb) + int(bool(args.iterative and sh.iterative))
+            else:
+                launches_per_step += 1
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -705,7 +712,10 @@ def run_ours(args, workload_name, workload):
                     "pcie_duplex_ms_per_step": pcie_ms if world == 1 else None,
                     "frac_of_pcie_duplex": (pcie_ms / e2e_ms) if world == 1 else None,
                     "serial_ms_per_step": e2e_serial_ms},
-            "gpu_launches": args.steps * (2 if world == 1 else 3),
+            # our kernels per step: the SpMV (calibration inside it); at N>1 plus
+            # the P2P fix-up on an owner with senders and, fused iterative, the
+            # ready signal (collective exchange: plus k_fixup)
+            "gpu_launches": args.steps * launches_per_step,
             "clocks": clk,
             "correctness_max_rel_err": err,
         }

@@ -412,6 +412,70 @@ __global__ void __launch_bounds__(kFixThreads) k_warp_bounds_fix(int64_t* __rest
   }
 }
 
+// Item rows of the in-kernel calibration (spmv.cu resolve_item): item 2w is
+// the row of warp w's first tile start, item 2w+1 the row holding the warp's
+// last nonzero, item 2*nwarps (tail) the tail's first row.
+__global__ void k_item_keys(const int64_t* __restrict__ warp_begin,
+                            const uint32_t* __restrict__ tile_ptr, const int64_t* __restrict__ rp,
+                            int64_t m, int nwarps, int64_t B, int64_t pos0, int has_tail_item,
+                            int64_t tail_row_begin, int64_t* __restrict__ key) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = 2 * nwarps + (has_tail_item ? 1 : 0);
+  if (i >= n) return;
+  if (i == 2 * nwarps) {
+    key[i] = tail_row_begin;
+  } else if ((i & 1) == 0) {
+    key[i] = tile_ptr[warp_begin[i >> 1]] & 0x7fffffffu;
+  } else {
+    key[i] = row_of_nonzero_dev(rp, m, pos0 + warp_begin[(i >> 1) + 1] * B - 1);
+  }
+}
+
+// Runs of equal keys (keys are non-decreasing): run_first[i] = prefix max of
+// the run starts, run_last[i] = suffix min of the run ends -- one CTA, the
+// scans of k_warp_bounds_fix.
+__global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __restrict__ key, int n,
+                                                           int32_t* __restrict__ run_first,
+                                                           int32_t* __restrict__ run_last) {
+  __shared__ int part[kFixThreads];
+  const int t = threadIdx.x;
+  const int per = (n + kFixThreads - 1) / kFixThreads;
+  const int lo = min(n, t * per), hi = min(n, lo + per);
+  int m = -1;
+  for (int i = lo; i < hi; ++i)
+    if (i == 0 || key[i] != key[i - 1]) m = i;
+  part[t] = m;
+  __syncthreads();
+  for (int d = 1; d < kFixThreads; d <<= 1) {
+    const int o = t >= d ? part[t - d] : -1;
+    __syncthreads();
+    part[t] = max(part[t], o);
+    __syncthreads();
+  }
+  int run = t > 0 ? part[t - 1] : -1;
+  for (int i = lo; i < hi; ++i) {
+    if (i == 0 || key[i] != key[i - 1]) run = i;
+    run_first[i] = run;
+  }
+  __syncthreads();
+  m = INT_MAX;
+  for (int i = hi - 1; i >= lo; --i)
+    if (i == n - 1 || key[i] != key[i + 1]) m = i;
+  part[t] = m;
+  __syncthreads();
+  for (int d = 1; d < kFixThreads; d <<= 1) {
+    const int o = t + d < kFixThreads ? part[t + d] : INT_MAX;
+    __syncthreads();
+    part[t] = min(part[t], o);
+    __syncthreads();
+  }
+  run = t + 1 < kFixThreads ? part[t + 1] : INT_MAX;
+  for (int i = hi - 1; i >= lo; --i) {
+    if (i == n - 1 || key[i] != key[i + 1]) run = i;
+    run_last[i] = run;
+  }
+}
+
 // A few scalars of the held range, one thread: row_of_nonzero at two positions
 // and row_ptr at two rows (negative query = skip).
 __global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0, int64_t g1,
@@ -565,11 +629,12 @@ void free_handle(Handle* h) {
   free_pipeline(h->pipe);
   free_binding(h->mg);
   for (void* p : {(void*)h->row_ptr, (void*)h->tile_ptr, h->desc, (void*)h->eo_ptr, (void*)h->eo,
-                  (void*)h->col, (void*)h->val, (void*)h->item_row, (void*)h->item_val,
-                  (void*)h->send, (void*)h->spill, (void*)h->warp_begin})
+                  (void*)h->col, (void*)h->val, (void*)h->item_val, (void*)h->run_first,
+                  (void*)h->run_last, (void*)h->run_cnt, (void*)h->send, (void*)h->spill,
+                  (void*)h->warp_begin})
     if (p) cudaFreeAsync(p, 0);
   for (const StreamScratch& x : h->extra_scratch)
-    for (void* p : {(void*)x.item_row, (void*)x.item_val, (void*)x.spill}) cudaFreeAsync(p, 0);
+    for (void* p : {(void*)x.item_val, (void*)x.run_cnt, (void*)x.spill}) cudaFreeAsync(p, 0);
   cudaDeviceSynchronize();
   cudaSetDevice(prev);
   delete h;
@@ -641,12 +706,13 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   void* cub_tmp2 = nullptr;
   int64_t* work_prefix = nullptr;
   int64_t* work = nullptr;
+  int64_t* item_key = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   auto cleanup = [&](int code) {
     if (side && code) cudaStreamSynchronize(side);  // error path: side work may be in flight
     for (void* p : {(void*)head_bits, (void*)empty_bits, (void*)eo_cnt, (void*)scal, cub_tmp,
-                    cub_tmp2, (void*)work_prefix, (void*)work})
+                    cub_tmp2, (void*)work_prefix, (void*)work, (void*)item_key})
       if (p) cudaFreeAsync(p, stream);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -867,8 +933,12 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   const int64_t rows_total = h->lead_rows + (m - h->tail_row_begin);
   h->rows_blocks = rows_total > 0 ? (int)std::min<int64_t>((rows_total + 255) / 256, 2 * sms) : 0;
   const int64_t items = 2 * (int64_t)h->nwarps + 1;
-  TRY(dev_alloc(&h->item_row, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->item_val, (size_t)items, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->run_first, (size_t)items, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->run_last, (size_t)items, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->run_cnt, (size_t)items, &alloc_ms, &bytes));
+  TRYC(cudaMemsetAsync(h->run_cnt, 0, sizeof(int32_t) * items, stream));
+  TRYC(cudaMemsetAsync(h->item_val, 0xff, sizeof(double) * items, stream));  // idle pair slots
   TRY(dev_alloc(&h->spill, (size_t)std::max(h->nwarps, 1) * (B + 1), &alloc_ms, &bytes));
   if (pcs > 0 && h->nwarps > 0) {
     TRY(dev_alloc(&h->warp_begin, (size_t)h->nwarps + 1, &alloc_ms, &bytes));
@@ -882,6 +952,19 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     TRYC(cudaGetLastError());
     k_warp_bounds_fix<<<1, kFixThreads, 0, stream>>>(h->warp_begin, h->nwarps);
     TRYC(cudaGetLastError());
+  }
+  // runs of the calibration items (the rows warps / the tail share)
+  {
+    const int n_items = 2 * h->nwarps + (h->has_tail_item ? 1 : 0);
+    if (n_items > 0) {
+      TRY(dev_alloc(&item_key, (size_t)n_items, &alloc_ms, &tmp_bytes));
+      k_item_keys<<<(unsigned)((n_items + 255) / 256), 256, 0, stream>>>(
+          h->warp_begin, h->tile_ptr, h->row_ptr, m, h->nwarps, B, pos0, h->has_tail_item ? 1 : 0,
+          h->tail_row_begin, item_key);
+      TRYC(cudaGetLastError());
+      k_item_runs<<<1, kFixThreads, 0, stream>>>(item_key, n_items, h->run_first, h->run_last);
+      TRYC(cudaGetLastError());
+    }
   }
   trace.mark("plan");
 

@@ -57,9 +57,13 @@ struct SpmvArgs {
   const double* val;
   const double* x;
   double* y;
-  int64_t* item_row;
-  double* item_val;
+  double* item_val;        // run partials (deterministic mode), per stream
+  const int32_t* run_first;  // item i's run of equal rows is items [run_first[i], run_last[i]]
+  const int32_t* run_last;
+  int32_t* run_cnt;        // arrivals per run (indexed by its first item), per stream
   csr5g_partial* send;
+  uint32_t* send_flag;     // p2p.cu: owner's ready flag for the send record (or null)
+  uint32_t send_epoch;
   double* spill;           // per-warp overflow slots for closed segment sums
   const int64_t* warp_begin;  // warp w holds tiles [warp_begin[w], warp_begin[w+1])
   int64_t pcs;             // complete tiles held
@@ -81,7 +85,6 @@ struct SpmvArgs {
   int32_t bar_bytes;       // mbarrier area at the start of shared memory
   int32_t atomic;          // SpmvMode::atomic
   int32_t x_mode;          // x gather path: 0 L1+evict_last, 1 L1 no-allocate+evict_last
-  int32_t jitter;          // hashed tile-range boundaries
   int32_t stream_only;     // profiling: run the TMA ring without gathers/math
   int32_t early_gather;    // random gathers: issue tile k+1's gathers before tile k's depth loop
   float x_frac;            // share of x lines given evict_last (the rest evict_first)
@@ -96,8 +99,8 @@ struct Pipeline;  // pipeline.cu: host-vector copy/compute pipeline
 // each get their own run items and closed-segment spill area.
 struct StreamScratch {
   cudaStream_t stream;
-  int64_t* item_row;
   double* item_val;
+  int32_t* run_cnt;
   double* spill;
 };
 struct Binding;   // p2p.cu: a shard's NVLink boundary exchange
@@ -114,8 +117,10 @@ struct Handle {
   int32_t* eo = nullptr;
   int32_t* col = nullptr;
   double* val = nullptr;
-  int64_t* item_row = nullptr;
   double* item_val = nullptr;
+  int32_t* run_first = nullptr;  // static run structure of the items (built once)
+  int32_t* run_last = nullptr;
+  int32_t* run_cnt = nullptr;    // zeroed; every launch leaves it zeroed
   csr5g_partial* send = nullptr;
   csr5g_partial* send_ext = nullptr;  // caller-provided record slot
   uint32_t* send_flag = nullptr;      // p2p.cu: owner's ready flag for this shard's record

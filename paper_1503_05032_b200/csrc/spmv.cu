@@ -23,10 +23,11 @@
 //     (row, partial) items.
 //   * Before its tiles every thread takes a grid-stride share of the "rows
 //     part": CSR tail rows (spmv.cpp:110-124), leading/trailing empty rows.
-// k_calibrate: deterministic merge of the 2*warps+1 items (keys are
-//   non-decreasing rows): segmented reduction per warp window, forward walk
-//   for runs crossing windows; y[row] = run total.  Atomic mode instead adds
-//   items with fp64 atomics into a zeroed y (spmv.cpp:273-295).
+// Calibration (spmv.cpp:224-298) happens inside the same kernel: the items of
+//   a row shared between warps (or with the tail) form a run known at build
+//   time (k_item_runs); the last writer of a run sums its partials in item
+//   order and writes the row (resolve_item).  Atomic mode instead adds items
+//   with fp64 atomics into a zeroed y (spmv.cpp:273-295).
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -48,14 +49,7 @@ __device__ __forceinline__ void sts_if(int32_t* p, int32_t v, bool pred) {
       : "memory");
 }
 
-__device__ __forceinline__ void put_item(const SpmvArgs& a, int64_t idx, int64_t row, double v) {
-  if (a.atomic) {
-    if (v != 0.0) atomicAdd(a.y + row, v);
-  } else {
-    a.item_row[idx] = row;
-    a.item_val[idx] = v;
-  }
-}
+__device__ void resolve_item(const SpmvArgs& a, int64_t idx, int64_t row, double v);
 
 // Tail rows and leading/trailing empty rows, grid-stride over all threads.
 __device__ void rows_part(const SpmvArgs& a) {
@@ -75,29 +69,12 @@ __device__ void rows_part(const SpmvArgs& a) {
     double s = 0.0;
     for (int64_t q = lo; q < hi; ++q) s = fma(a.val[q - a.pos0], a.x[a.col[q - a.pos0]], s);
     if (a.has_tail_item && r == a.tail_row_begin) {
-      put_item(a, 2 * (int64_t)a.nwarps, r, s);
+      resolve_item(a, 2 * (int64_t)a.nwarps, r, s);
     } else {
       a.y[r] = s;
       if (a.mir.n) mirror_store(a.mir, r, s);
     }
   }
-}
-
-// First tile of warp w's contiguous range.  With jitter, the boundaries move
-// by a hashed offset of up to a quarter range so that the warps' concurrent
-// streams do not sit on a regular address lattice.
-__device__ __forceinline__ int64_t range_begin(int w, int64_t pcs, int nwarps, int jitter) {
-  if (w <= 0) return 0;
-  if (w >= nwarps) return pcs;
-  const int64_t base = (int64_t)w * pcs / nwarps;
-  if (!jitter) return base;
-  const int64_t q = pcs / nwarps / 4;
-  if (q < 1) return base;
-  uint32_t h = (uint32_t)w * 2654435761u;
-  h ^= h >> 15;
-  h *= 2246822519u;
-  h ^= h >> 13;
-  return base + (int64_t)(h % (uint32_t)q);
 }
 
 __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
@@ -125,72 +102,79 @@ __device__ __forceinline__ void write_run(int64_t row, double v, double* y, int6
   }
 }
 
-// One full warp merges items [base, base + 32): segmented warp reduction over
-// the non-decreasing keys; a run that continues past the window is finished
-// by the warp holding its start, walking forward.  Items written by other
-// CTAs of the same launch are read through L2 (ld.cg).
-__device__ void calibrate_window(const int64_t* __restrict__ item_row,
-                                 const double* __restrict__ item_val, int64_t N, int64_t base,
-                                 double* __restrict__ y, int64_t first_row, int first_owned,
-                                 csr5g_partial* send, uint32_t* flag, uint32_t epoch,
-                                 const Mirrors& mir) {
-  const int lane = threadIdx.x & 31;
-  if (base == 0 && lane == 0) {
-    send->row = -1;
-    send->value = 0.0;
-  }
-  __syncwarp();
-  const int64_t i = base + lane;
-  const bool valid = i < N;
-  const int64_t key = valid ? __ldcg(item_row + i) : (LLONG_MAX - lane);
-  int64_t prev = __shfl_up_sync(kFull, key, 1);
-  if (lane == 0) prev = base > 0 ? __ldcg(item_row + base - 1) : LLONG_MIN;
-  const bool start = valid && key != prev;
-  const uint32_t sm = __ballot_sync(kFull, start);
-  const uint32_t vm = __ballot_sync(kFull, valid);
-  const uint64_t above = (uint64_t)sm >> (lane + 1);
-  const int end = above ? lane + __ffsll((long long)above) - 1 : 31 - __clz(vm);
-  double v = valid ? __ldcg(item_val + i) : 0.0;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const double o = __shfl_down_sync(kFull, v, d);
-    if (lane + d <= end) v += o;
-  }
-  const int ls = sm ? 31 - __clz(sm) : -1;
-  bool cont = false;
-  int64_t rk = 0;
-  if (ls >= 0) {
-    rk = __shfl_sync(kFull, key, ls);
-    cont = (base + 32 < N) && __ldcg(item_row + base + 32) == rk;
-  }
-  if (start && !(cont && lane == ls)) write_run(key, v, y, first_row, first_owned, send, flag, epoch, mir);
-  if (cont) {
-    double total = __shfl_sync(kFull, v, ls);
-    for (int64_t pos = base + 32;; pos += 32) {
-      const int64_t q = pos + lane;
-      const bool mt = q < N && __ldcg(item_row + q) == rk;
-      const uint32_t mm = __ballot_sync(kFull, mt);
-      double s = mt ? __ldcg(item_val + q) : 0.0;
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(kFull, s, d);
-      total += s;
-      if (mm != kFull) break;
-    }
-    if (lane == 0) write_run(rk, total, y, first_row, first_owned, send, flag, epoch, mir);
-  }
+// In-kernel calibration (deterministic mode).  Rows wholly inside a warp's
+// tile range are final in the warp; only its first and last row runs can be
+// shared, so it emits two items (2w, 2w+1; the tail's first row is item
+// 2*nwarps).  Their rows are fixed by the structure, so the build records for
+// every item the run of equal rows it belongs to (k_item_runs).  The writer of
+// an item stores its partial, fences and counts an arrival on the run; the
+// last arrival sums the run's partials in item order (deterministic whatever
+// the arrival order), resets the counter for the next launch and writes the
+// row (y, or the shard's send record, spmv.cpp:267-272).  No second kernel.
+// A run of two partials (the common case: a row shared by two neighbouring
+// warps) needs no fence or counter: both writers exchange their value through
+// one 64-bit atomic on the run's slot, and the second adds the two (a + b is
+// b + a bit for bit).  The slot's idle value is all ones, a NaN that no
+// arithmetic produces (results are the canonical NaN); the second writer
+// restores it for the next launch.
+constexpr unsigned long long kSlotIdle = ~0ull;
+
+__device__ __forceinline__ bool pair_exchange(const SpmvArgs& a, int s, double v, double* total) {
+  auto* slot = reinterpret_cast<unsigned long long*>(a.item_val + s);
+  const unsigned long long old = atomicExch(slot, (unsigned long long)__double_as_longlong(v));
+  if (old == kSlotIdle) return false;
+  *slot = kSlotIdle;
+  *total = __longlong_as_double((long long)old) + v;
+  return true;
 }
 
-__global__ void k_calibrate(const int64_t* __restrict__ item_row,
-                            const double* __restrict__ item_val, int64_t N, double* __restrict__ y,
-                            int64_t first_row, int first_owned, csr5g_partial* send,
-                            uint32_t* flag, uint32_t epoch, Mirrors mir) {
-  // launched as a programmatic dependent of k_spmv: its launch overlaps the
-  // SpMV; the items are read only once that grid has completed
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int lane = threadIdx.x & 31;
-  const int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane;
-  if (base >= N) return;
-  calibrate_window(item_row, item_val, N, base, y, first_row, first_owned, send, flag, epoch, mir);
+__device__ void resolve_item(const SpmvArgs& a, int64_t idx, int64_t row, double v) {
+  if (a.atomic) {  // spmv.cpp:273-295: fp64 atomics into the zeroed y
+    if (v != 0.0) atomicAdd(a.y + row, v);
+    return;
+  }
+  const int s = a.run_first[idx], e = a.run_last[idx];
+  double t = v;
+  if (e == s + 1) {
+    if (!pair_exchange(a, s, v, &t)) return;
+  } else if (e > s) {
+    __stcg(a.item_val + idx, v);
+    __threadfence();
+    if (atomicAdd(a.run_cnt + s, 1) != e - s) return;
+    __threadfence();
+    t = 0.0;
+#pragma unroll 4
+    for (int j = s; j <= e; ++j) t += __ldcg(a.item_val + j);
+    a.run_cnt[s] = 0;
+  }
+  write_run(row, t, a.y, a.first_row, a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
+}
+
+// The same, called by a whole warp (idx, row, v uniform): the last arrival's
+// warp sums a long run 32 items at a time (fixed tree, deterministic).
+__device__ __forceinline__ void resolve_item_warp(const SpmvArgs& a, int64_t idx, int64_t row,
+                                                  double v, int lane) {
+  const int s = a.atomic ? 0 : a.run_first[idx], e = a.atomic ? 0 : a.run_last[idx];
+  if (a.atomic || e <= s + 1) {  // single partial, pair exchange, or atomic mode
+    if (lane == 0) resolve_item(a, idx, row, v);
+    return;
+  }
+  int last = 0;
+  if (lane == 0) {
+    __stcg(a.item_val + idx, v);
+    __threadfence();
+    last = atomicAdd(a.run_cnt + s, 1) == e - s;
+  }
+  if (!__shfl_sync(kFull, last, 0)) return;
+  __threadfence();
+  double t = 0.0;
+  for (int j = s + lane; j <= e; j += 32) t += __ldcg(a.item_val + j);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(kFull, t, d);
+  if (lane == 0) {
+    a.run_cnt[s] = 0;
+    write_run(row, t, a.y, a.first_row, a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
+  }
 }
 
 }  // namespace
@@ -224,11 +208,12 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   constexpr uint32_t COL_OFF = VR ? 0 : B * 8, DESC_OFF = COL_OFF + B * 4;
   constexpr uint32_t TILE_BYTES = DESC_OFF + 32 * sizeof(W);
 
-  // the calibration grid may launch now; it waits (griddepcontrol.wait) for
-  // this grid to complete before reading the items
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (a.first_owned && !a.atomic && blockIdx.x == 0 && threadIdx.x == 0) {
+    a.send->row = -1;  // this handle has no partial to send
+    a.send->value = 0.0;
+  }
   const int NW = blockDim.x >> 5;
   const int S = a.stages;
   const int w = blockIdx.x * NW + wib;
@@ -250,12 +235,9 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   const W* __restrict__ desc = static_cast<const W*>(a.desc);
 
   int64_t kb = 0, ke = 0;
-  if (has_tiles && a.warp_begin && !a.jitter) {
+  if (has_tiles) {
     kb = a.warp_begin[w];
     ke = a.warp_begin[w + 1];
-  } else if (has_tiles) {
-    kb = range_begin(w, a.pcs, a.nwarps, a.jitter);
-    ke = range_begin(w + 1, a.pcs, a.nwarps, a.jitter);
   }
   auto issue = [&](int64_t k, int s) {  // lane 0 only
     unsigned char* st = ring + (size_t)s * a.stage_bytes;
@@ -289,6 +271,10 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
     int64_t pend_row = -1;
     double pend_val = 0.0;
     bool pend_first = true;
+    // the warp's first run is resolved after its loop, together with the last
+    // one (both pair exchanges in flight at once, none stalls the tile loop)
+    int64_t first_row = -1;
+    double first_val = 0.0;
     uint32_t tpv = 0, tpv_next = 0;
     int64_t eov = 0;
     int s = 0;
@@ -525,12 +511,12 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       __syncwarp();  // closed[] is rewritten by the next tile
 
       // ---- row runs across the warp's consecutive tiles ----
-      auto flush = [&]() {
-        if (lane == 0) {
-          if (pend_first)
-            put_item(a, 2 * (int64_t)w, pend_row, pend_val);
-          else
-            put_y(pend_row, pend_val);
+      auto flush = [&]() {  // warp-uniform
+        if (pend_first) {
+          first_row = pend_row;
+          first_val = pend_val;
+        } else if (lane == 0) {
+          put_y(pend_row, pend_val);
         }
       };
       if (k == kb) {
@@ -552,13 +538,45 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
         pend_first = false;
       }
     }
-    if (lane == 0) {
-      if (pend_first) {
-        put_item(a, 2 * (int64_t)w, pend_row, pend_val);
-        put_item(a, 2 * (int64_t)w + 1, pend_row, 0.0);
-      } else {
-        put_item(a, 2 * (int64_t)w + 1, pend_row, pend_val);
+    const int64_t i0 = 2 * (int64_t)w, i1 = i0 + 1;
+    const int64_t r0 = pend_first ? pend_row : first_row;
+    const double v0 = pend_first ? pend_val : first_val;
+    const double v1 = pend_first ? 0.0 : pend_val;
+    const bool short_runs = !a.atomic && a.run_last[i0] - a.run_first[i0] <= 1 &&
+                            a.run_last[i1] - a.run_first[i1] <= 1;
+    if (short_runs) {
+      // both runs hold one or two partials: lane 0 issues both exchanges, then
+      // finishes whichever it completed
+      if (lane == 0) {
+        const int s0 = a.run_first[i0], e0 = a.run_last[i0];
+        const int s1 = a.run_first[i1], e1 = a.run_last[i1];
+        unsigned long long o0 = 0, o1 = 0;
+        if (e0 > s0)
+          o0 = atomicExch(reinterpret_cast<unsigned long long*>(a.item_val + s0),
+                          (unsigned long long)__double_as_longlong(v0));
+        if (e1 > s1)
+          o1 = atomicExch(reinterpret_cast<unsigned long long*>(a.item_val + s1),
+                          (unsigned long long)__double_as_longlong(v1));
+        if (e0 == s0) {
+          write_run(r0, v0, a.y, a.first_row, a.first_owned, a.send, a.send_flag, a.send_epoch,
+                    a.mir);
+        } else if (o0 != kSlotIdle && !(s1 == s0 && e1 > s1)) {
+          a.item_val[s0] = __longlong_as_double((long long)kSlotIdle);
+          write_run(r0, __longlong_as_double((long long)o0) + v0, a.y, a.first_row,
+                    a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
+        }
+        if (e1 == s1) {
+          write_run(pend_row, v1, a.y, a.first_row, a.first_owned, a.send, a.send_flag,
+                    a.send_epoch, a.mir);
+        } else if (o1 != kSlotIdle) {
+          a.item_val[s1] = __longlong_as_double((long long)kSlotIdle);
+          write_run(pend_row, __longlong_as_double((long long)o1) + v1, a.y, a.first_row,
+                    a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
+        }
       }
+    } else {
+      resolve_item_warp(a, i0, r0, v0, lane);
+      resolve_item_warp(a, i1, pend_row, v1, lane);
     }
   }
 }
@@ -722,39 +740,41 @@ int func_attrs(const void* fn, int device, int smem, int carve) {
 
 // The scratch of `stream`: the handle's own arrays for the first stream that
 // runs an SpMV on it, arrays allocated (stream-ordered) for every other one.
-int scratch_for(Handle* h, cudaStream_t stream, int64_t** ir, double** iv, double** sp) {
+int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, double** sp) {
   std::lock_guard<std::mutex> lock(h->scratch_mu);
   if (!h->scratch_claimed) {
     h->scratch_claimed = true;
     h->scratch_stream = stream;
   }
   if (stream == h->scratch_stream) {
-    *ir = h->item_row;
     *iv = h->item_val;
+    *rc = h->run_cnt;
     *sp = h->spill;
     return CSR5G_OK;
   }
   for (const StreamScratch& x : h->extra_scratch)
     if (x.stream == stream) {
-      *ir = x.item_row;
       *iv = x.item_val;
+      *rc = x.run_cnt;
       *sp = x.spill;
       return CSR5G_OK;
     }
   const size_t items = 2 * (size_t)h->nwarps + 1;
   const size_t spill = (size_t)std::max(h->nwarps, 1) * (size_t)(h->B + 1);
   StreamScratch x{stream, nullptr, nullptr, nullptr};
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&x.item_row), items * 8, stream);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&x.item_val), items * 8, stream);
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&x.item_val), items * 8, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(x.item_val, 0xff, items * 8, stream);  // idle slots
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&x.run_cnt), items * 4, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(x.run_cnt, 0, items * 4, stream);
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&x.spill), spill * 8, stream);
   if (e != cudaSuccess) {
-    for (void* p : {(void*)x.item_row, (void*)x.item_val, (void*)x.spill})
+    for (void* p : {(void*)x.item_val, (void*)x.run_cnt, (void*)x.spill})
       if (p) cudaFreeAsync(p, stream);
     return cuda_fail(e, "per-stream SpMV scratch");
   }
   h->extra_scratch.push_back(x);
-  *ir = x.item_row;
   *iv = x.item_val;
+  *rc = x.run_cnt;
   *sp = x.spill;
   return CSR5G_OK;
 }
@@ -784,13 +804,13 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.val = h->val;
   a.x = d_x;
   a.y = d_y;
-  if (int rc = scratch_for(h, stream, &a.item_row, &a.item_val, &a.spill)) return rc;
+  if (int rc = scratch_for(h, stream, &a.item_val, &a.run_cnt, &a.spill)) return rc;
+  a.run_first = h->run_first;
+  a.run_last = h->run_last;
   a.send = h->send_ext ? h->send_ext : h->send;
-  static const bool equal_split = [] {  // A/B: equal tile counts per warp
-    const char* e = std::getenv("CSR5G_EQUAL_SPLIT");
-    return e && std::atoi(e) != 0;
-  }();
-  a.warp_begin = equal_split ? nullptr : h->warp_begin;
+  a.send_flag = h->send_flag;
+  a.send_epoch = h->send_epoch;
+  a.warp_begin = h->warp_begin;
   a.pcs = h->pcs;
   a.pos0 = h->t0 * h->B;
   a.next_row_after = h->next_row_after;
@@ -836,21 +856,12 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.x_frac = x_frac_env > 0.0f ? std::min(1.0f, x_frac_env) : 1.0f;
   a.y_hint = y_hint_env >= 0 ? y_hint_env : 0;
   if (const char* e = std::getenv("CSR5G_EARLY")) a.early_gather = std::atoi(e) != 0;
-  static const int jitter = [] {
-    const char* e = std::getenv("CSR5G_JITTER");
-    return e ? std::atoi(e) : 0;
-  }();
-  a.jitter = jitter;
   static const int stream_only = [] {  // 1: TMA ring only, 2: compute only (profiling)
     const char* e = std::getenv("CSR5G_STREAM_ONLY");
     return e ? std::atoi(e) : 0;
   }();
   a.stream_only = stream_only;
   const int64_t items = 2 * (int64_t)h->nwarps + (h->has_tail_item ? 1 : 0);
-  static const bool pdl_on = [] {  // CSR5G_PDL=0: plain stream order (A/B)
-    const char* e = std::getenv("CSR5G_PDL");
-    return !e || std::atoi(e) != 0;
-  }();
   if (ev0) CSR5G_CUDA(cudaEventRecord(ev0, stream));
   if (grid > 0) {
     cudaLaunchConfig_t cfg{};
@@ -886,21 +897,9 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     CSR5G_CUDA(cudaLaunchKernelEx(&cfg, spmv_fn(a.sigma, h->vr), a));
   }
   if (ev1) CSR5G_CUDA(cudaEventRecord(ev1, stream));
-  if (stream_only) return CSR5G_OK;  // no items were produced
-  if (!atomic && items > 0) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)((items + 255) / 256));
-    cfg.blockDim = dim3(256);
-    cfg.stream = stream;
-    cudaLaunchAttribute pdl[1];
-    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    pdl[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = pdl;
-    cfg.numAttrs = pdl_on ? 1 : 0;
-    CSR5G_CUDA(cudaLaunchKernelEx(&cfg, k_calibrate, (const int64_t*)a.item_row,
-                                  (const double*)a.item_val, items, d_y, h->first_row,
-                                  (int)h->first_owned, a.send, h->send_flag, h->send_epoch, h->mir));
-  } else if (!atomic) {  // no record: row -1 (all ones), value 0.0
+  // the rows shared between warps were merged inside the kernel
+  // (resolve_item); a handle with nothing to multiply has no record
+  if (!atomic && items == 0 && grid == 0) {  // no record: row -1 (all ones), value 0.0
     CSR5G_CUDA(cudaMemsetAsync(&a.send->row, 0xff, sizeof(int64_t), stream));
     CSR5G_CUDA(cudaMemsetAsync(&a.send->value, 0, sizeof(double), stream));
   }

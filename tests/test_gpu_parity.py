@@ -248,7 +248,7 @@ def test_p2p_exchange_on_one_device(g, orc):
     for a in cases:
         sigma = orc.select_sigma(a.nnz / a.m)
         xs = [rng.random_x(a.n) for _ in range(3)]
-        for world in (2, 3, 8):
+        for world in (2, 3, 8, 16):
             ys, errs, dest, senders = mg.emulate_p2p_on_one_device(a, xs, sigma, world)
             assert errs == [0] * len(errs), (world, errs)
             for x, y in zip(xs, ys):
