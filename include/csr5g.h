@@ -143,7 +143,7 @@ CSR5G_API int csr5g_fixup(csr5g_matrix h, const csr5g_partial *d_all, int32_t wo
  * backend).  One mailbox per rank in its own HBM, exported with a CUDA IPC
  * handle and opened by every peer.  A shard that does not own its first row
  * stores that row's partial straight into the owner's mailbox (dest) from
- * its calibration kernel, then a ready flag; an owner stream-waits on the
+ * its SpMV kernel, then a ready flag; an owner stream-waits on the
  * flags of its senders (the ranks sender_begin..sender_end-1 right after it
  * whose first row is its last row), adds their partials in shard order and
  * acknowledges.  No collective, no host sync per call.  Deterministic mode

@@ -16,7 +16,7 @@
 //   err      u32            protocol violations seen by k_fixup_p2p (tests read it)
 // Per call (epoch e, host counter, one per binding):
 //   sender r:  stream-wait ack >= e-1 (the owner consumed the previous record;
-//              single-buffered slot), then the SpMV; k_calibrate stores the
+//              single-buffered slot), then the SpMV, whose calibration stores the
 //              record into dest's slot[r], fences at system scope and stores
 //              ready[r] = e with release semantics (spmv.cu write_run).
 //   owner o:   stream-wait ready[g] >= e for every sender g (cuStreamWaitValue32

@@ -11,7 +11,7 @@ shard edge gets a partial sum from each shard.  The row's owner is the shard
 holding its first nonzero.  Each shard has at most one partial to send (its
 first row, when it does not own it), to a destination fixed by the matrix
 structure (plan_exchange).  The default exchange is NVLink P2P (p2p.cu):
-the shard's calibration kernel stores the 16-byte partial straight into the
+the shard's SpMV kernel stores the 16-byte partial straight into the
 owner's mailbox and raises a flag; the owner's stream waits on the flags of
 its senders, adds their partials in shard order (deterministic) and
 acknowledges -- no collective, no host sync.  CSR5G_EXCHANGE=collective

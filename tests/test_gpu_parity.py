@@ -237,7 +237,7 @@ def test_shards_concatenate_and_fix_up(g, orc):
 
 def test_p2p_exchange_on_one_device(g, orc):
     """The NVLink P2P boundary exchange (p2p.cu) with all shards in one process:
-    partials stored into the owners' mailboxes by the calibration kernel,
+    partials stored into the owners' mailboxes by the SpMV kernel,
     flags/acks over several calls (epochs), y equal to the collective form and
     within tolerance of the oracle, no protocol errors."""
     from paper_1503_05032_b200 import mg

@@ -3,7 +3,7 @@ run as world_size 2 and 3 process groups over gloo on CPU.
 
 Every rank plans its shard with the product's planner (mg.shard_view), builds
 the shard's partial result with a CPU emulation of the CUDA shard semantics
-(spmv.cu k_calibrate / k_fixup: rows owned by the shard holding their first
+(spmv.cu resolve_item / k_fixup: rows owned by the shard holding their first
 nonzero; a shard sends at most one partial, for a first row it does not own;
 owners add later shards' partials in shard order), exchanges the 16-byte
 records with mg.exchange_records, and assembles x for the next iteration with
