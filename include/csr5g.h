@@ -179,8 +179,9 @@ CSR5G_API int csr5g_mg_spmv(csr5g_matrix h, const double *d_x, double *d_y, void
  * from vector(it & 1) into vector((it+1) & 1), every final y value also
  * stored into each peer's vector((it+1) & 1) over NVLink by the kernels that
  * produce it, then the boundary fix-up (mirrored) and the ready signal to
- * every peer.  No all-gather.  post/finish split as above for ranks sharing
- * one GPU (host barrier between and after). */
+ * every peer.  No all-gather.  Steps run 0, 1, 2, ... on every rank (x_0 is
+ * vector(0)); anything else is EINVAL.  post/finish split as above for ranks
+ * sharing one GPU (host barrier between and after). */
 CSR5G_API int csr5g_mg_iter_post(csr5g_matrix h, int64_t it, void *stream, void *ev_tiles_begin,
                                  void *ev_tiles_end);
 CSR5G_API int csr5g_mg_iter_finish(csr5g_matrix h, int64_t it, void *stream);

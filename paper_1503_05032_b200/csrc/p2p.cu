@@ -81,6 +81,7 @@ struct Binding {
   Mailbox* mb = nullptr;
   int dest = -1, sb = 0, se = 0, active = 1;
   uint32_t epoch = 0;
+  int64_t last_iter = -1;  // iterative mode: steps run 0, 1, 2, ... on every rank
 };
 
 void free_binding(Binding* b) { delete b; }
@@ -224,6 +225,11 @@ int mg_iter_post(Handle* h, int64_t it, cudaStream_t stream, cudaEvent_t ev0, cu
   if (int rc = iter_check(h)) return rc;
   Binding* b = h->mg;
   Mailbox* m = b->mb;
+  // the xready flags and the buffer parity assume consecutive steps from 0
+  if (it != b->last_iter + 1)
+    return fail(CSR5G_EINVAL, "csr5g: iterative step " + std::to_string(it) + " after step " +
+                                  std::to_string(b->last_iter) + " (steps run 0, 1, 2, ...)");
+  b->last_iter = it;
   CSR5G_CUDA(cudaSetDevice(h->device));
   for (int g = 0; g < b->active; ++g)
     if (g != m->rank)
