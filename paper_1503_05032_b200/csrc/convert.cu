@@ -414,11 +414,15 @@ __global__ void __launch_bounds__(kFixThreads) k_warp_bounds_fix(int64_t* __rest
 
 // Item rows of the in-kernel calibration (spmv.cu resolve_item): item 2w is
 // the row of warp w's first tile start, item 2w+1 the row holding the warp's
-// last nonzero, item 2*nwarps (tail) the tail's first row.
+// last nonzero -- the last head of its last tile t: H = y_offset + popc(flags)
+// of column 31, row = tile_row + (flagged ? eo[eo_ptr[t] + H - 1] : H - 1) --
+// and item 2*nwarps (tail) the tail's first row.  O(1) loads per item.
+template <typename W>
 __global__ void k_item_keys(const int64_t* __restrict__ warp_begin,
-                            const uint32_t* __restrict__ tile_ptr, const int64_t* __restrict__ rp,
-                            int64_t m, int nwarps, int64_t B, int64_t pos0, int has_tail_item,
-                            int64_t tail_row_begin, int64_t* __restrict__ key) {
+                            const uint32_t* __restrict__ tile_ptr, const W* __restrict__ desc,
+                            const int64_t* __restrict__ eo_ptr, const int32_t* __restrict__ eo,
+                            int sigma, int nwarps, int has_tail_item, int64_t tail_row_begin,
+                            int64_t* __restrict__ key) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = 2 * nwarps + (has_tail_item ? 1 : 0);
   if (i >= n) return;
@@ -427,7 +431,11 @@ __global__ void k_item_keys(const int64_t* __restrict__ warp_begin,
   } else if ((i & 1) == 0) {
     key[i] = tile_ptr[warp_begin[i >> 1]] & 0x7fffffffu;
   } else {
-    key[i] = row_of_nonzero_dev(rp, m, pos0 + warp_begin[(i >> 1) + 1] * B - 1);
+    const int64_t t = warp_begin[(i >> 1) + 1] - 1;
+    const uint32_t tp = tile_ptr[t];
+    const uint64_t wd = (uint64_t)desc[t * 32 + 31];
+    const int H = (int)(wd >> (kSegBits + sigma)) + __popcll(wd & ((1ull << sigma) - 1));
+    key[i] = (int64_t)(tp & 0x7fffffffu) + ((tp >> 31) ? (int64_t)eo[eo_ptr[t] + H - 1] : H - 1);
   }
 }
 
@@ -958,9 +966,15 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     const int n_items = 2 * h->nwarps + (h->has_tail_item ? 1 : 0);
     if (n_items > 0) {
       TRY(dev_alloc(&item_key, (size_t)n_items, &alloc_ms, &tmp_bytes));
-      k_item_keys<<<(unsigned)((n_items + 255) / 256), 256, 0, stream>>>(
-          h->warp_begin, h->tile_ptr, h->row_ptr, m, h->nwarps, B, pos0, h->has_tail_item ? 1 : 0,
-          h->tail_row_begin, item_key);
+      const unsigned kb = (unsigned)((n_items + 255) / 256);
+      if (h->wide)
+        k_item_keys<uint64_t><<<kb, 256, 0, stream>>>(
+            h->warp_begin, h->tile_ptr, (const uint64_t*)h->desc, h->eo_ptr, h->eo, (int)sigma,
+            h->nwarps, h->has_tail_item ? 1 : 0, h->tail_row_begin, item_key);
+      else
+        k_item_keys<uint32_t><<<kb, 256, 0, stream>>>(
+            h->warp_begin, h->tile_ptr, (const uint32_t*)h->desc, h->eo_ptr, h->eo, (int)sigma,
+            h->nwarps, h->has_tail_item ? 1 : 0, h->tail_row_begin, item_key);
       TRYC(cudaGetLastError());
       k_item_runs<<<1, kFixThreads, 0, stream>>>(item_key, n_items, h->run_first, h->run_last);
       TRYC(cudaGetLastError());
