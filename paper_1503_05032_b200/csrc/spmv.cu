@@ -540,6 +540,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
         pend_first = false;
       }
     }
+    if (a.stream_only) return;  // profiling knobs: no rows were produced
     const int64_t i0 = 2 * (int64_t)w, i1 = i0 + 1;
     const int64_t r0 = pend_first ? pend_row : first_row;
     const double v0 = pend_first ? pend_val : first_val;
