@@ -285,7 +285,7 @@ def run_ours(args, workload_name, workload):
     if world > 1:
         # a rank that never sees a peer's flag would block its stream forever:
         # turn such a hang into a loud failure (the whole run takes minutes)
-        limit = float(os.environ.get("CSR5G_WATCHDOG_S", "900"))
+        limit = float(os.environ.get("CSR5G_WATCHDOG_S", "300"))
 
         def _watchdog():
             time.sleep(limit)
