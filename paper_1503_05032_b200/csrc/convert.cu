@@ -310,16 +310,23 @@ __global__ void k_eo(const uint32_t* __restrict__ head_bits, const uint32_t* __r
 __global__ void k_tile_work(const uint32_t* __restrict__ head_bits,
                             const uint32_t* __restrict__ tile_ptr, int64_t pcs, int sigma,
                             int w_head, int w_row, int64_t* __restrict__ work,
-                            int64_t* __restrict__ eo_cnt) {
+                            int64_t* __restrict__ eo_cnt, int* __restrict__ max_heads) {
+  __shared__ int bmax;
+  if (threadIdx.x == 0) bmax = 0;
+  __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= pcs) return;
-  const uint32_t* wd = head_bits + t * sigma;  // a tile is sigma 32-bit words
-  int heads = (wd[0] & 1u) ? 0 : 1;           // bf[0] is forced
-  for (int i = 0; i < sigma; ++i) heads += __popc(wd[i]);
-  const uint32_t tp = tile_ptr[t];
-  const int64_t rows = (int64_t)(tile_ptr[t + 1] & 0x7fffffffu) - (tp & 0x7fffffffu) + 1;
-  work[t] = 32ll * sigma + (int64_t)w_head * heads + (int64_t)w_row * rows;
-  eo_cnt[t] = (tp >> 31) ? heads : 0;  // empty_offset entries: heads of flagged tiles
+  if (t < pcs) {
+    const uint32_t* wd = head_bits + t * sigma;  // a tile is sigma 32-bit words
+    int heads = (wd[0] & 1u) ? 0 : 1;           // bf[0] is forced
+    for (int i = 0; i < sigma; ++i) heads += __popc(wd[i]);
+    const uint32_t tp = tile_ptr[t];
+    const int64_t rows = (int64_t)(tile_ptr[t + 1] & 0x7fffffffu) - (tp & 0x7fffffffu) + 1;
+    work[t] = 32ll * sigma + (int64_t)w_head * heads + (int64_t)w_row * rows;
+    eo_cnt[t] = (tp >> 31) ? heads : 0;  // empty_offset entries: heads of flagged tiles
+    atomicMax(&bmax, heads);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bmax > 0) atomicMax(max_heads, bmax);
 }
 
 // Largest per-warp work of the equal-tile split (atomicMax into *out).
@@ -752,7 +759,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRY(dev_alloc(&head_bits, (size_t)head_words, &alloc_ms, &tmp_bytes));
   TRY(dev_alloc(&empty_bits, (size_t)empty_words, &alloc_ms, &tmp_bytes));
   TRY(dev_alloc(&eo_cnt, (size_t)pcs + 1, &alloc_ms, &tmp_bytes));
-  TRY(dev_alloc(&scal, 8, &alloc_ms, &tmp_bytes));
+  TRY(dev_alloc(&scal, 10, &alloc_ms, &tmp_bytes));  // 0-3 scalars, 4 lines, 6 emax, 8 max heads
 
   trace.mark("alloc");
   if (m > 0) TRYC(cudaMemcpyAsync(h->row_ptr, d_row_ptr, sizeof(int64_t) * (m + 1),
@@ -846,11 +853,13 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     const char* e = std::getenv("CSR5G_WROW");
     return e ? std::atoi(e) : 1;
   }();
+  int* max_heads_d = reinterpret_cast<int*>(scal + 8);
+  TRYC(cudaMemsetAsync(max_heads_d, 0, sizeof(int), side));
   if (pcs > 0) {
     TRY(dev_alloc(&work, (size_t)pcs, &alloc_ms, &tmp_bytes));
     k_tile_work<<<(unsigned)((pcs + 255) / 256), 256, 0, side>>>(head_bits, h->tile_ptr, pcs,
                                                                  (int)sigma, w_head, w_row, work,
-                                                                 eo_cnt);
+                                                                 eo_cnt, max_heads_d);
     TRYC(cudaGetLastError());
   }
   size_t cub_bytes = 0;
@@ -873,6 +882,8 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   int64_t ptr_first = 0, ptr_close = 0, eo_total = 0;
   TRYC(cudaMemcpyAsync(&eo_total, h->eo_ptr + pcs, sizeof(int64_t), cudaMemcpyDeviceToHost, side));
   uint32_t tp0 = 0, tpc = 0;
+  int max_heads = 0;
+  TRYC(cudaMemcpyAsync(&max_heads, max_heads_d, sizeof(int), cudaMemcpyDeviceToHost, side));
   TRYC(cudaMemcpyAsync(&tp0, h->tile_ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, side));
   TRYC(cudaMemcpyAsync(&tpc, h->tile_ptr + (pcs < tile_ptr_len ? pcs : tile_ptr_len - 1),
                        sizeof(uint32_t), cudaMemcpyDeviceToHost, side));
@@ -935,6 +946,8 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   h->has_tail_item = is_last && tail > 0;
   int sms = 0;
   TRYC(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  h->max_heads = max_heads;  // with eo_total: may the plan drop the flag paths (NF)?
+  h->eo_entries = eo_total;
   h->info.sigma = sigma;  // spmv_plan picks the sigma-specialised kernel
   h->info.n = n;          // ... and sizes its shared memory by x
   TRY(spmv_plan(h, sms));

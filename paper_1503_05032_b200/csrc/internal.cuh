@@ -137,6 +137,9 @@ struct Handle {
   int x_mode = 0;                 // gather path chosen by the plan
   bool x_window = false;          // L2 persisting window on x
   bool vr = false;                // values outside the TMA ring (k_spmv<SIG, true>)
+  bool nf = false;                // no flagged tile, heads fit the slots (k_spmv<SIG, false, true>)
+  int max_heads = 0;              // most segment heads in one tile
+  int64_t eo_entries = 0;         // empty_offset entries
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
   int carveout_pct = -1;  // preferred shared-memory carveout of the SpMV kernel
   // scratch of streams other than the first one that ran an SpMV (which uses

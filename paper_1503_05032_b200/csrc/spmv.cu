@@ -198,7 +198,10 @@ constexpr int kVrMaxSigma = 24;  // VR variants are instantiated up to this sigm
 // loaded coalesced straight into registers together with its x gathers, so a
 // warp's ring is a third of the size and more of the SM's L1 stays free for
 // outstanding gather misses.
-template <int SIG, bool VR>
+// NF ("no flags"): the plan proved that no tile is flagged and every tile's
+// heads fit the shared-memory slots (Laplacian-like matrices), so the
+// empty_offset staging, the spill path and the empty-row zeroing compile out.
+template <int SIG, bool VR, bool NF = false>
 __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
   using W = typename std::conditional<(SIG <= 17), uint32_t, uint64_t>::type;
   constexpr int B = 32 * SIG;
@@ -320,14 +323,14 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
         const int64_t last = a.tile_ptr_len - 1;
         tpv = a.tile_ptr[k + lane < last ? k + lane : last];
         tpv_next = a.tile_ptr[k + 32 < last ? k + 32 : last];
-        eov = a.eo_ptr[k + lane < a.pcs ? k + lane : a.pcs];
+        if (!NF) eov = a.eo_ptr[k + lane < a.pcs ? k + lane : a.pcs];
       }
       const uint32_t tp = __shfl_sync(kFull, tpv, slot);
       const uint32_t tpn_s = __shfl_sync(kFull, tpv, (slot + 1) & 31);
       const uint32_t tpn = slot == 31 ? tpv_next : tpn_s;
       const int64_t eo_base = __shfl_sync(kFull, eov, slot);
       const int64_t tile_row = tp & 0x7fffffffu;
-      const bool flagged = (tp >> 31) != 0;
+      const bool flagged = !NF && (tp >> 31) != 0;
       const int64_t next_row = (k + 1 == a.pcs) ? a.next_row_after : (int64_t)(tpn & 0x7fffffffu);
       const int32_t* __restrict__ eo = a.eo + eo_base;
 
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       const int yoff = (int)(wd >> (kSegBits + SIG));
       const int cnt = __popcll(fr);
       const int H = __shfl_sync(kFull, yoff + cnt, 31);
-      const bool fast = H < CAPC;
+      const bool fast = NF || H < CAPC;
       // a flagged shared-slot tile's empty_offset entries (H < 128: at most 4
       // per lane) are in flight during the depth loop
       int32_t eov4[4] = {0, 0, 0, 0};
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
       // leave a possibly-outstanding load whose scoreboard the gathers reuse)
   #pragma unroll
       for (int q = 0; q < 4; ++q)
-        sts_if(eos + lane + 32 * q, eov4[q], flagged && fast && lane + 32 * q < H);
+        if (!NF) sts_if(eos + lane + 32 * q, eov4[q], flagged && fast && lane + 32 * q < H);
       __syncwarp();
       if (lane == 0 && k + S < ke && !compute_only) issue(k + S, s);  // refill this stage
       // gathers for tile k+1 land in the registers the depth loop just drained;
@@ -599,7 +602,21 @@ __global__ void k_fixup(const csr5g_partial* __restrict__ all, int world, int ra
 using SpmvFn = void (*)(SpmvArgs);
 
 // sigma is 1..48 at omega = 32 (the 64-bit descriptor limit, descriptor.cpp:22-36)
-SpmvFn spmv_fn(int sigma, bool vr) {
+constexpr int kNfMaxSigma = 8;  // NF variants are instantiated up to this sigma
+
+SpmvFn spmv_fn(int sigma, bool vr, bool nf = false) {
+  if (nf && !vr && sigma <= kNfMaxSigma) {
+    switch (sigma) {
+#define CSR5G_KN(S) \
+  case S:           \
+    return k_spmv<S, false, true>;
+      CSR5G_KN(1) CSR5G_KN(2) CSR5G_KN(3) CSR5G_KN(4) CSR5G_KN(5) CSR5G_KN(6) CSR5G_KN(7)
+      CSR5G_KN(8)
+#undef CSR5G_KN
+      default:
+        return nullptr;
+    }
+  }
   if (vr) {
     switch (sigma) {
 #define CSR5G_KV(S) \
@@ -657,6 +674,12 @@ int spmv_plan(Handle* h, int sms) {
   }();
   h->vr = random && sigma <= kVrMaxSigma && vr_env != 0;
   if (vr_env == 1 && sigma <= kVrMaxSigma) h->vr = true;
+  static const int nf_env = [] {  // CSR5G_NF=0: keep the general kernel (A/B)
+    const char* e = std::getenv("CSR5G_NF");
+    return e ? std::atoi(e) : -1;
+  }();
+  h->nf = nf_env != 0 && !h->vr && sigma <= kNfMaxSigma && h->pcs > 0 && h->eo_entries == 0 &&
+          h->max_heads < std::min<int64_t>(h->B, kClosedSlots);
   const int64_t tile_bytes = h->B * (h->vr ? 4 : 12) + 32 * wbytes;
   const int stage_bytes = (int)((tile_bytes + 127) / 128 * 128);
   const int closed_bytes = (int)(std::min<int64_t>(h->B, kClosedSlots) * 8);
@@ -894,10 +917,9 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
       cfg.attrs = attr;
       cfg.numAttrs = 1;
     }
-    if (int rc = func_attrs((const void*)spmv_fn(a.sigma, h->vr), h->device, h->smem_bytes,
-                            h->carveout_pct))
-      return rc;
-    CSR5G_CUDA(cudaLaunchKernelEx(&cfg, spmv_fn(a.sigma, h->vr), a));
+    const SpmvFn fn = spmv_fn(a.sigma, h->vr, h->nf);
+    if (int rc = func_attrs((const void*)fn, h->device, h->smem_bytes, h->carveout_pct)) return rc;
+    CSR5G_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
   }
   if (ev1) CSR5G_CUDA(cudaEventRecord(ev1, stream));
   // the rows shared between warps were merged inside the kernel
