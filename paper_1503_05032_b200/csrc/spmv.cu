@@ -186,6 +186,9 @@ __device__ __forceinline__ void resolve_item_warp(const SpmvArgs& a, int64_t idx
 __host__ __device__ constexpr int spmv_threads(int sigma) {
   return sigma <= 5 ? 640 : sigma <= 13 ? 512 : sigma <= 32 ? 384 : 256;
 }
+__host__ __device__ constexpr int spmv_threads_nf(int sigma) {
+  return sigma <= 5 ? 768 : spmv_threads(sigma);  // 80 registers suffice without the flag paths
+}
 // closed-segment slots per warp in shared memory (tiles rarely have more heads)
 constexpr int kClosedSlots = 128;
 constexpr int kEoSlots = 128;  // >= kClosedSlots - 1 heads of a shared-slot tile
@@ -202,7 +205,8 @@ constexpr int kVrMaxSigma = 24;  // VR variants are instantiated up to this sigm
 // heads fit the shared-memory slots (Laplacian-like matrices), so the
 // empty_offset staging, the spill path and the empty-row zeroing compile out.
 template <int SIG, bool VR, bool NF = false>
-__global__ void __launch_bounds__(spmv_threads(SIG), 1) k_spmv(SpmvArgs a) {
+__global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG), 1)
+    k_spmv(SpmvArgs a) {
   using W = typename std::conditional<(SIG <= 17), uint32_t, uint64_t>::type;
   constexpr int B = 32 * SIG;
   constexpr int CH = SIG <= 32 ? SIG : (SIG + 1) / 2;  // x gathers in flight per lane
@@ -707,7 +711,7 @@ int spmv_plan(Handle* h, int sms) {
   // random gathers: two stages -- the shared memory a third would take is
   // worth more as L1 for outstanding gather misses (measured: R-MAT s24 at
   // 150 KB, 7 warps: 2 stages 1.67 ms, 3 stages 2.11 ms)
-  int nw = spmv_threads(sigma) / 32, stages = random ? 2 : 4;
+  int nw = (h->nf ? spmv_threads_nf(sigma) : spmv_threads(sigma)) / 32, stages = random ? 2 : 4;
   // one mbarrier per warp and stage at the start, 128-byte aligned
   auto bars = [](int w, int st) { return (w * st * 8 + 127) / 128 * 128; };
   auto need = [&](int w, int st) {
