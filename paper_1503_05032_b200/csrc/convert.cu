@@ -492,13 +492,15 @@ __global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __rest
 }
 
 // A few scalars of the held range, one thread: row_of_nonzero at two positions
-// and row_ptr at two rows (negative query = skip).
+// (negative query = skip) and row_ptr at the rows of tile_ptr[0] and
+// tile_ptr[ic] (the first row, the closing row).
 __global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0, int64_t g1,
-                          int64_t r0, int64_t r1, int64_t* __restrict__ out) {
+                          const uint32_t* __restrict__ tile_ptr, int64_t ic,
+                          int64_t* __restrict__ out) {
   out[0] = g0 >= 0 ? row_of_nonzero_dev(rp, m, g0) : -1;
   out[1] = g1 >= 0 ? row_of_nonzero_dev(rp, m, g1) : -1;
-  out[2] = (r0 >= 0 && r0 <= m) ? rp[r0] : -1;
-  out[3] = (r1 >= 0 && r1 <= m) ? rp[r1] : -1;
+  out[2] = rp[tile_ptr[0] & 0x7fffffffu];
+  out[3] = rp[tile_ptr[ic] & 0x7fffffffu];
 }
 
 // Gather locality of the SpMV: for `samples` evenly spaced tiles, the number
@@ -506,6 +508,9 @@ __global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0,
 // touches, summed into *acc.  1 = perfectly coalesced, 32 = fully random.
 __global__ void k_locality(const int32_t* __restrict__ col, int64_t pcs, int sigma, int64_t samples,
                            unsigned long long* __restrict__ acc) {
+  // col is the caller's CSR-order col_idx: tile k's column i, depth j sits at
+  // k*B + i*sigma + j (the SpMV reads it transposed, the lines touched by one
+  // warp-wide gather are the same), so the sample runs beside the transposition
   const int lane = threadIdx.x & 31;
   const int64_t sidx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (sidx >= samples) return;
@@ -513,7 +518,7 @@ __global__ void k_locality(const int32_t* __restrict__ col, int64_t pcs, int sig
   const int B = 32 * sigma;
   unsigned total = 0;
   for (int j = 0; j < sigma; ++j) {
-    const int32_t line = col[k * B + (int64_t)j * 32 + lane] >> 4;
+    const int32_t line = col[k * B + (int64_t)lane * sigma + j] >> 4;
     const unsigned peers = __match_any_sync(kFull, line);
     total += (__ffs(peers) - 1) == lane;  // one leader per distinct line
   }
@@ -878,29 +883,42 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     TRYC(cub::DeviceScan::InclusiveSum(t2, need, work, work_prefix, (int)pcs, side));
   }
 
-  // Scalars of the held range.
+  // gather locality over up to 4096 sampled tiles (drives the SpMV plan), from
+  // the input col_idx, read back with the scalars; its counter sits after them
+  h->lines_per_gather = 1.0;
+  unsigned long long lines = 0;
+  const int64_t samples = std::min<int64_t>(pcs, 4096);
+  if (pcs > 0) {
+    auto* ctr = reinterpret_cast<unsigned long long*>(scal + 4);
+    TRYC(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), side));
+    k_locality<<<(unsigned)((samples * 32 + 255) / 256), 256, 0, side>>>(d_col_idx, pcs,
+                                                                       (int)sigma, samples, ctr);
+    TRYC(cudaGetLastError());
+    TRYC(cudaMemcpyAsync(&lines, ctr, sizeof lines, cudaMemcpyDeviceToHost, side));
+  }
+
+  // Scalars of the held range, all read back with one sync of the side stream.
+  // queries: g0 = last position of the held complete tiles, g1 = nnz - 1
   int64_t ptr_first = 0, ptr_close = 0, eo_total = 0;
+  const int64_t ic = pcs < tile_ptr_len ? pcs : tile_ptr_len - 1;
+  const int64_t g0 = pcs > 0 ? tile_end * B - 1 : -1;
+  const int64_t g1 = nnz > 0 ? nnz - 1 : -1;
+  int64_t sv[4] = {-1, -1, -1, -1};
+  if (m > 0) {
+    k_scalars<<<1, 1, 0, side>>>(h->row_ptr, m, g0, g1, h->tile_ptr, ic, scal);
+    TRYC(cudaGetLastError());
+    TRYC(cudaMemcpyAsync(sv, scal, sizeof sv, cudaMemcpyDeviceToHost, side));
+  }
   TRYC(cudaMemcpyAsync(&eo_total, h->eo_ptr + pcs, sizeof(int64_t), cudaMemcpyDeviceToHost, side));
   uint32_t tp0 = 0, tpc = 0;
   int max_heads = 0;
   TRYC(cudaMemcpyAsync(&max_heads, max_heads_d, sizeof(int), cudaMemcpyDeviceToHost, side));
   TRYC(cudaMemcpyAsync(&tp0, h->tile_ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, side));
-  TRYC(cudaMemcpyAsync(&tpc, h->tile_ptr + (pcs < tile_ptr_len ? pcs : tile_ptr_len - 1),
-                       sizeof(uint32_t), cudaMemcpyDeviceToHost, side));
+  TRYC(cudaMemcpyAsync(&tpc, h->tile_ptr + ic, sizeof(uint32_t), cudaMemcpyDeviceToHost, side));
   TRYC(cudaStreamSynchronize(side));  // the transposition keeps running on `stream`
   trace.mark("scan");
   ptr_first = tp0 & 0x7fffffffu;
   ptr_close = tpc & 0x7fffffffu;
-  // queries: g0 = last position of the held complete tiles, g1 = nnz - 1;
-  // r0 = row_ptr[first row], r1 = row_ptr[closing row]
-  const int64_t g0 = pcs > 0 ? tile_end * B - 1 : -1;
-  const int64_t g1 = nnz > 0 ? nnz - 1 : -1;
-  if (m > 0) {
-    k_scalars<<<1, 1, 0, side>>>(h->row_ptr, m, g0, g1, ptr_first, ptr_close, scal);
-    TRYC(cudaGetLastError());
-  }
-  int64_t sv[4] = {-1, -1, -1, -1};
-  if (m > 0) TRYC(cudaMemcpyAsync(sv, scal, sizeof sv, cudaMemcpyDeviceToHost, side));
   TRY(dev_alloc(&h->eo, (size_t)eo_total, &alloc_ms, &bytes));
   if (pcs > 0 && eo_total > 0) {
     const int64_t threads = pcs * 32;
@@ -911,23 +929,8 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRYC(cudaEventRecord(ev_join, side));
   t_alloc_stream = stream;
   trace.mark("eo");
-  // gather locality over up to 4096 sampled tiles (drives the SpMV plan), on
-  // `stream` after the transposition; its counter sits after the four scalars
-  h->lines_per_gather = 1.0;
-  unsigned long long lines = 0;
-  const int64_t samples = std::min<int64_t>(pcs, 4096);
-  if (pcs > 0) {
-    auto* ctr = reinterpret_cast<unsigned long long*>(scal + 4);
-    TRYC(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), stream));
-    k_locality<<<(unsigned)((samples * 32 + 255) / 256), 256, 0, stream>>>(h->col, pcs, (int)sigma,
-                                                                         samples, ctr);
-    TRYC(cudaGetLastError());
-    TRYC(cudaMemcpyAsync(&lines, ctr, sizeof lines, cudaMemcpyDeviceToHost, stream));
-  }
-  TRYC(cudaStreamWaitEvent(stream, ev_join, 0));  // join: eo, eo_ptr, scalars, work prefix
-  TRYC(cudaStreamSynchronize(stream));
   if (pcs > 0) h->lines_per_gather = (double)lines / (double)(samples * sigma);
-  trace.mark("locality");
+  TRYC(cudaStreamWaitEvent(stream, ev_join, 0));  // join: eo, eo_ptr, work prefix
 
   // ---- SpMV plan ----
   const bool is_first = tile_begin == 0;
@@ -1038,6 +1041,10 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   in.smem_bytes = h->smem_bytes;
   in.x_mode = h->x_mode;
   in.x_window = h->x_window ? 1 : 0;
+  // the build is synchronous (format.hpp:182 returns a finished value): the
+  // handle is usable from any stream once it returns
+  TRYC(cudaStreamSynchronize(stream));
+  trace.mark("final");
   in.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
   *out = h;
   return cleanup(CSR5G_OK);
