@@ -318,6 +318,14 @@ def test_concurrent_streams_one_handle(g, orc):
     a5 = gpu_build(g, a, sigma)
     rng = orc.rng(12)
     xs = [rng.random_x(a.n) for _ in range(4)]
+    # the build is synchronous: a stream that never saw it can use the handle at once
+    fresh = torch.cuda.Stream()
+    x0 = torch.as_tensor(xs[0]).cuda()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(fresh):
+        y0 = g.spmv_csr5(a5, x0, stream=fresh)
+    fresh.synchronize()
+    assert_y_close(y0.cpu().numpy(), orc.spmv(a, xs[0], 32, sigma), a, xs[0], "fresh stream")
     ref = [gpu_y(g, a5, x) for x in xs]
     streams = [torch.cuda.Stream() for _ in xs]
     xd = [torch.as_tensor(x).cuda() for x in xs]
