@@ -315,13 +315,14 @@ def test_concurrent_streams_one_handle(g, orc):
     equals the single-stream result bit for bit (deterministic mode)."""
     a = orc.generate_synthetic(2, 20000, 15000, 600000, 8)
     sigma = orc.select_sigma(a.nnz / a.m)
-    a5 = gpu_build(g, a, sigma)
     rng = orc.rng(12)
     xs = [rng.random_x(a.n) for _ in range(4)]
     # the build is synchronous: a stream that never saw it can use the handle at once
     fresh = torch.cuda.Stream()
     x0 = torch.as_tensor(xs[0]).cuda()
+    d = to_dev(g, a)
     torch.cuda.synchronize()
+    a5 = g.csr_to_csr5(d, g.TuningParams(sigma=sigma))
     with torch.cuda.stream(fresh):
         y0 = g.spmv_csr5(a5, x0, stream=fresh)
     fresh.synchronize()
