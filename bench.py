@@ -688,7 +688,8 @@ def run_ours(args, workload_name, workload):
                        "spmv_plan": {"lines_per_gather": round(info.lines_per_gather, 2),
                                      "warps_per_cta": info.warps_per_cta, "stages": info.stages,
                                      "smem_bytes": info.smem_bytes, "x_mode": info.x_mode,
-                                     "x_l2_window": info.x_window},
+                                     "x_l2_window": info.x_window,
+                                     "kernel_variant": ["general", "VR", "NF"][info.kernel_variant]},
                        "parallelism": f"tile-range shards x{world}, x replicated",
                        "l2": (f"L2 flushed between timed calls ({2 * l2_bytes / 1e6:.0f} MB "
                               f"read outside the events); working set "

@@ -69,7 +69,8 @@ typedef struct {
   double build_ms, alloc_ms;    /* last build: total and allocation share */
   /* SpMV plan chosen from the sampled gather locality */
   double lines_per_gather;      /* distinct 128 B x lines per warp gather (1..32) */
-  int32_t warps_per_cta, stages, smem_bytes, x_mode, x_window, pad_;
+  int32_t warps_per_cta, stages, smem_bytes, x_mode, x_window;
+  int32_t kernel_variant;       /* 0 general, 1 VR (values with the gathers), 2 NF (no flag paths) */
 } csr5g_info;
 
 /* One boundary partial of a shard: row = -1 when there is none. */

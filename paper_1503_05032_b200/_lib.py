@@ -42,7 +42,7 @@ class Info(C.Structure):
         ("build_ms", C.c_double), ("alloc_ms", C.c_double),
         ("lines_per_gather", C.c_double),
         ("warps_per_cta", C.c_int32), ("stages", C.c_int32), ("smem_bytes", C.c_int32),
-        ("x_mode", C.c_int32), ("x_window", C.c_int32), ("pad_", C.c_int32),
+        ("x_mode", C.c_int32), ("x_window", C.c_int32), ("kernel_variant", C.c_int32),
     ]
 
 

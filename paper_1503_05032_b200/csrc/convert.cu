@@ -1041,6 +1041,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   in.smem_bytes = h->smem_bytes;
   in.x_mode = h->x_mode;
   in.x_window = h->x_window ? 1 : 0;
+  in.kernel_variant = h->vr ? 1 : (h->nf ? 2 : 0);
   // the build is synchronous (format.hpp:182 returns a finished value): the
   // handle is usable from any stream once it returns
   TRYC(cudaStreamSynchronize(stream));

@@ -375,6 +375,36 @@ def test_cuda_graph_capture(g, orc):
     a5.release()
 
 
+def test_kernel_variants(g, orc):
+    """The plan's kernel variants on matrices made for them, each against the
+    oracle: NF (no flagged tile, heads fit the slots, sigma <= 8) on a 2D
+    5-point Laplacian and a banded matrix, the general kernel on the same
+    Laplacian with empty rows spliced in (flagged tiles), VR on random columns."""
+    from oracle.oracle import stencil
+    lap = stencil(orc, 0, 40, 40)  # 1600 rows, sigma 5
+    rows = np.repeat(np.arange(3000), 7)
+    band = orc.coo_to_csr(rows.tolist(), ((rows + np.tile(np.arange(7), 3000)) % 3000).tolist(),
+                          np.linspace(0.5, 1.5, rows.size), 3000, 3000)
+    r2 = [r + r // 50 for r in lap_rows(lap)]  # every 50th row becomes empty
+    gap = orc.coo_to_csr(r2, lap.col_idx.tolist(), lap.val.tolist(), max(r2) + 1, lap.n)
+    rr = np.repeat(np.arange(40000), 8)
+    rc = np.random.default_rng(31).integers(0, 400000, rr.size)
+    rnd = orc.coo_to_csr(rr.tolist(), rc.tolist(), np.linspace(0.5, 1.5, rr.size), 40000, 400000)
+    for name, a, want in (("laplacian", lap, 2), ("band", band, 2), ("gaps", gap, 0),
+                          ("random", rnd, 1)):
+        sigma = orc.select_sigma(a.nnz / a.m)
+        a5 = gpu_build(g, a, sigma)
+        assert a5.info.kernel_variant == want, (name, sigma, a5.info.kernel_variant)
+        x = orc.rng(5).random_x(a.n)
+        assert_y_close(gpu_y(g, a5, x), orc.spmv(a, x, 32, sigma), a, x, name)
+        compare_arrays(a5.export(), orc.build(a, 32, sigma), name)
+        a5.release()
+
+
+def lap_rows(a):
+    return np.repeat(np.arange(a.m), np.diff(np.asarray(a.row_ptr))).tolist()
+
+
 def test_host_vector_paths(g, orc):
     """csr5g_spmv_host and the pipelined csr5g_spmv_host_batch (pinned and
     pageable host vectors, batches longer than the two buffer pairs, a second
