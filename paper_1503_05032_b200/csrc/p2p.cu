@@ -307,6 +307,7 @@ int csr5g_mailbox_create(int device, int32_t world, int32_t rank, int64_t vec_le
   if (e != cudaSuccess) {
     cudaFree(m->local);
     cudaFree(m->d_peer_ack);
+    cudaFree(m->d_peer_xready);
     delete m;
     return cuda_fail(e, "csr5g_mailbox_create");
   }
