@@ -451,9 +451,15 @@ __global__ void k_item_keys(const int64_t* __restrict__ warp_begin,
 // scans of k_warp_bounds_fix.
 __global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __restrict__ key, int n,
                                                            int32_t* __restrict__ run_first,
-                                                           int32_t* __restrict__ run_last) {
+                                                           int32_t* __restrict__ run_last,
+                                                           int32_t* __restrict__ run_cnt,
+                                                           double* __restrict__ item_val) {
   __shared__ int part[kFixThreads];
   const int t = threadIdx.x;
+  for (int i = t; i < n; i += kFixThreads) {  // per-launch state: no arrivals, idle pair slots
+    run_cnt[i] = 0;
+    item_val[i] = __longlong_as_double(-1ll);
+  }
   const int per = (n + kFixThreads - 1) / kFixThreads;
   const int lo = min(n, t * per), hi = min(n, lo + per);
   int m = -1;
@@ -491,16 +497,26 @@ __global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __rest
   }
 }
 
-// A few scalars of the held range, one thread: row_of_nonzero at two positions
-// (negative query = skip) and row_ptr at the rows of tile_ptr[0] and
-// tile_ptr[ic] (the first row, the closing row).
+// Every scalar the host needs from the build, gathered by one thread into one
+// block for a single read-back: row_of_nonzero at two positions (negative
+// query = skip), row_ptr at the first and the closing row, the empty_offset
+// total, the largest head count, the two tile_ptr words, the locality count.
 __global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0, int64_t g1,
                           const uint32_t* __restrict__ tile_ptr, int64_t ic,
+                          const int64_t* __restrict__ eo_ptr, int64_t pcs,
+                          const int* __restrict__ max_heads,
+                          const unsigned long long* __restrict__ lines,
                           int64_t* __restrict__ out) {
-  out[0] = g0 >= 0 ? row_of_nonzero_dev(rp, m, g0) : -1;
-  out[1] = g1 >= 0 ? row_of_nonzero_dev(rp, m, g1) : -1;
-  out[2] = rp[tile_ptr[0] & 0x7fffffffu];
-  out[3] = rp[tile_ptr[ic] & 0x7fffffffu];
+  const bool rows = m > 0;
+  out[0] = rows && g0 >= 0 ? row_of_nonzero_dev(rp, m, g0) : -1;
+  out[1] = rows && g1 >= 0 ? row_of_nonzero_dev(rp, m, g1) : -1;
+  out[2] = rows ? rp[tile_ptr[0] & 0x7fffffffu] : -1;
+  out[3] = rows ? rp[tile_ptr[ic] & 0x7fffffffu] : -1;
+  out[4] = eo_ptr[pcs];
+  out[5] = *max_heads;
+  out[6] = tile_ptr[0];
+  out[7] = tile_ptr[ic];
+  out[8] = (int64_t)*lines;
 }
 
 // Gather locality of the SpMV: for `samples` evenly spaced tiles, the number
@@ -764,7 +780,8 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRY(dev_alloc(&head_bits, (size_t)head_words, &alloc_ms, &tmp_bytes));
   TRY(dev_alloc(&empty_bits, (size_t)empty_words, &alloc_ms, &tmp_bytes));
   TRY(dev_alloc(&eo_cnt, (size_t)pcs + 1, &alloc_ms, &tmp_bytes));
-  TRY(dev_alloc(&scal, 10, &alloc_ms, &tmp_bytes));  // 0-3 scalars, 4 lines, 6 emax, 8 max heads
+  // 4 lines, 6 emax, 8 max heads, 10-18 the scalars read back
+  TRY(dev_alloc(&scal, 20, &alloc_ms, &tmp_bytes));
 
   trace.mark("alloc");
   if (m > 0) TRYC(cudaMemcpyAsync(h->row_ptr, d_row_ptr, sizeof(int64_t) * (m + 1),
@@ -888,35 +905,34 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   h->lines_per_gather = 1.0;
   unsigned long long lines = 0;
   const int64_t samples = std::min<int64_t>(pcs, 4096);
+  auto* ctr = reinterpret_cast<unsigned long long*>(scal + 4);
+  TRYC(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), side));
   if (pcs > 0) {
-    auto* ctr = reinterpret_cast<unsigned long long*>(scal + 4);
-    TRYC(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), side));
     k_locality<<<(unsigned)((samples * 32 + 255) / 256), 256, 0, side>>>(d_col_idx, pcs,
                                                                        (int)sigma, samples, ctr);
     TRYC(cudaGetLastError());
-    TRYC(cudaMemcpyAsync(&lines, ctr, sizeof lines, cudaMemcpyDeviceToHost, side));
   }
 
-  // Scalars of the held range, all read back with one sync of the side stream.
-  // queries: g0 = last position of the held complete tiles, g1 = nnz - 1
+  // Scalars of the held range, all read back in one copy and one sync of the
+  // side stream.  queries: g0 = last position of the held complete tiles,
+  // g1 = nnz - 1
   int64_t ptr_first = 0, ptr_close = 0, eo_total = 0;
   const int64_t ic = pcs < tile_ptr_len ? pcs : tile_ptr_len - 1;
   const int64_t g0 = pcs > 0 ? tile_end * B - 1 : -1;
   const int64_t g1 = nnz > 0 ? nnz - 1 : -1;
   int64_t sv[4] = {-1, -1, -1, -1};
-  if (m > 0) {
-    k_scalars<<<1, 1, 0, side>>>(h->row_ptr, m, g0, g1, h->tile_ptr, ic, scal);
-    TRYC(cudaGetLastError());
-    TRYC(cudaMemcpyAsync(sv, scal, sizeof sv, cudaMemcpyDeviceToHost, side));
-  }
-  TRYC(cudaMemcpyAsync(&eo_total, h->eo_ptr + pcs, sizeof(int64_t), cudaMemcpyDeviceToHost, side));
-  uint32_t tp0 = 0, tpc = 0;
-  int max_heads = 0;
-  TRYC(cudaMemcpyAsync(&max_heads, max_heads_d, sizeof(int), cudaMemcpyDeviceToHost, side));
-  TRYC(cudaMemcpyAsync(&tp0, h->tile_ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, side));
-  TRYC(cudaMemcpyAsync(&tpc, h->tile_ptr + ic, sizeof(uint32_t), cudaMemcpyDeviceToHost, side));
+  int64_t hs[9];
+  k_scalars<<<1, 1, 0, side>>>(h->row_ptr, m, g0, g1, h->tile_ptr, ic, h->eo_ptr, pcs, max_heads_d,
+                               reinterpret_cast<const unsigned long long*>(scal + 4), scal + 10);
+  TRYC(cudaGetLastError());
+  TRYC(cudaMemcpyAsync(hs, scal + 10, sizeof hs, cudaMemcpyDeviceToHost, side));
   TRYC(cudaStreamSynchronize(side));  // the transposition keeps running on `stream`
   trace.mark("scan");
+  for (int q = 0; q < 4; ++q) sv[q] = hs[q];
+  eo_total = hs[4];
+  const int max_heads = (int)hs[5];
+  const uint32_t tp0 = (uint32_t)hs[6], tpc = (uint32_t)hs[7];
+  lines = (unsigned long long)hs[8];
   ptr_first = tp0 & 0x7fffffffu;
   ptr_close = tpc & 0x7fffffffu;
   TRY(dev_alloc(&h->eo, (size_t)eo_total, &alloc_ms, &bytes));
@@ -961,8 +977,6 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRY(dev_alloc(&h->run_first, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->run_last, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->run_cnt, (size_t)items, &alloc_ms, &bytes));
-  TRYC(cudaMemsetAsync(h->run_cnt, 0, sizeof(int32_t) * items, stream));
-  TRYC(cudaMemsetAsync(h->item_val, 0xff, sizeof(double) * items, stream));  // idle pair slots
   TRY(dev_alloc(&h->spill, (size_t)std::max(h->nwarps, 1) * (B + 1), &alloc_ms, &bytes));
   if (pcs > 0 && h->nwarps > 0) {
     TRY(dev_alloc(&h->warp_begin, (size_t)h->nwarps + 1, &alloc_ms, &bytes));
@@ -992,7 +1006,8 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
             h->warp_begin, h->tile_ptr, (const uint32_t*)h->desc, h->eo_ptr, h->eo, (int)sigma,
             h->nwarps, h->has_tail_item ? 1 : 0, h->tail_row_begin, item_key);
       TRYC(cudaGetLastError());
-      k_item_runs<<<1, kFixThreads, 0, stream>>>(item_key, n_items, h->run_first, h->run_last);
+      k_item_runs<<<1, kFixThreads, 0, stream>>>(item_key, n_items, h->run_first, h->run_last,
+                                                 h->run_cnt, h->item_val);
       TRYC(cudaGetLastError());
     }
   }
