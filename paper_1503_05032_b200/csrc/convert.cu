@@ -30,8 +30,9 @@ namespace {
 
 __global__ void k_rowscan(const int64_t* __restrict__ rp, int64_t m, int64_t pos_begin,
                           int64_t pos_end, uint32_t* __restrict__ empty_bits,
-                          uint32_t* __restrict__ head_bits) {
+                          uint32_t* __restrict__ head_bits, csr5g_partial* __restrict__ send) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) *send = csr5g_partial{-1, 0.0};  // no boundary record yet
   const int lane = threadIdx.x & 31;
   const bool inr = r < m;
   int64_t lo = 0, hi = 0;
@@ -738,6 +739,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   uint32_t *head_bits = nullptr, *empty_bits = nullptr;
   int64_t* eo_cnt = nullptr;
   int64_t* scal = nullptr;
+  char* zblock = nullptr;  // head_bits | empty_bits | eo_cnt | scal, zeroed by one memset
   void* cub_tmp = nullptr;
   void* cub_tmp2 = nullptr;
   int64_t* work_prefix = nullptr;
@@ -747,8 +749,8 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   auto cleanup = [&](int code) {
     if (side && code) cudaStreamSynchronize(side);  // error path: side work may be in flight
-    for (void* p : {(void*)head_bits, (void*)empty_bits, (void*)eo_cnt, (void*)scal, cub_tmp,
-                    cub_tmp2, (void*)work_prefix, (void*)work, (void*)item_key})
+    for (void* p : {(void*)zblock, cub_tmp, cub_tmp2, (void*)work_prefix, (void*)work,
+                    (void*)item_key})
       if (p) cudaFreeAsync(p, stream);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -777,26 +779,31 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   int64_t tmp_bytes = 0;
   const int64_t head_words = (pcs * B + 31) / 32 + 3;
   const int64_t empty_words = (m + 31) / 32 + 1;
-  TRY(dev_alloc(&head_bits, (size_t)head_words, &alloc_ms, &tmp_bytes));
-  TRY(dev_alloc(&empty_bits, (size_t)empty_words, &alloc_ms, &tmp_bytes));
-  TRY(dev_alloc(&eo_cnt, (size_t)pcs + 1, &alloc_ms, &tmp_bytes));
-  // 4 lines, 6 emax, 8 max heads, 10-18 the scalars read back
-  TRY(dev_alloc(&scal, 20, &alloc_ms, &tmp_bytes));
+  // one zeroed block: the two bitmaps, the per-tile head counts and the
+  // scalars (4 lines, 6 emax, 8 max heads, 10-18 the values read back)
+  const size_t hb_bytes = ((size_t)head_words * 4 + 7) / 8 * 8;
+  const size_t eb_bytes = ((size_t)empty_words * 4 + 7) / 8 * 8;
+  const size_t zbytes = hb_bytes + eb_bytes + 8 * ((size_t)pcs + 1) + 8 * 20;
+  TRY(dev_alloc(&zblock, zbytes, &alloc_ms, &tmp_bytes));
+  head_bits = reinterpret_cast<uint32_t*>(zblock);
+  empty_bits = reinterpret_cast<uint32_t*>(zblock + hb_bytes);
+  eo_cnt = reinterpret_cast<int64_t*>(zblock + hb_bytes + eb_bytes);
+  scal = eo_cnt + pcs + 1;
 
   trace.mark("alloc");
   if (m > 0) TRYC(cudaMemcpyAsync(h->row_ptr, d_row_ptr, sizeof(int64_t) * (m + 1),
                                   cudaMemcpyDeviceToDevice, stream));
-  TRYC(cudaMemsetAsync(head_bits, 0, sizeof(uint32_t) * head_words, stream));
-  TRYC(cudaMemsetAsync(empty_bits, 0, sizeof(uint32_t) * empty_words, stream));
-  TRYC(cudaMemsetAsync(eo_cnt, 0, sizeof(int64_t) * (pcs + 1), stream));
-  TRYC(cudaMemsetAsync(&h->send->row, 0xff, sizeof(int64_t), stream));  // no record: row -1
-  TRYC(cudaMemsetAsync(&h->send->value, 0, sizeof(double), stream));
+  TRYC(cudaMemsetAsync(zblock, 0, zbytes, stream));
+  if (m == 0) {  // (else k_rowscan writes it)
+    TRYC(cudaMemsetAsync(&h->send->row, 0xff, sizeof(int64_t), stream));  // no record: row -1
+    TRYC(cudaMemsetAsync(&h->send->value, 0, sizeof(double), stream));
+  }
 
   const int64_t pos0 = tile_begin * B;
   trace.mark("init");
   if (m > 0) {
     k_rowscan<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(h->row_ptr, m, pos0, pos0 + pcs * B,
-                                                               empty_bits, head_bits);
+                                                               empty_bits, head_bits, h->send);
     TRYC(cudaGetLastError());
     trace.mark("rowscan");
     k_tile_ptr<<<(unsigned)((tile_ptr_len + 255) / 256), 256, 0, stream>>>(
@@ -875,8 +882,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     const char* e = std::getenv("CSR5G_WROW");
     return e ? std::atoi(e) : 1;
   }();
-  int* max_heads_d = reinterpret_cast<int*>(scal + 8);
-  TRYC(cudaMemsetAsync(max_heads_d, 0, sizeof(int), side));
+  int* max_heads_d = reinterpret_cast<int*>(scal + 8);  // zeroed with the block
   if (pcs > 0) {
     TRY(dev_alloc(&work, (size_t)pcs, &alloc_ms, &tmp_bytes));
     k_tile_work<<<(unsigned)((pcs + 255) / 256), 256, 0, side>>>(head_bits, h->tile_ptr, pcs,
@@ -905,8 +911,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   h->lines_per_gather = 1.0;
   unsigned long long lines = 0;
   const int64_t samples = std::min<int64_t>(pcs, 4096);
-  auto* ctr = reinterpret_cast<unsigned long long*>(scal + 4);
-  TRYC(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), side));
+  auto* ctr = reinterpret_cast<unsigned long long*>(scal + 4);  // zeroed with the block
   if (pcs > 0) {
     k_locality<<<(unsigned)((samples * 32 + 255) / 256), 256, 0, side>>>(d_col_idx, pcs,
                                                                        (int)sigma, samples, ctr);
@@ -980,8 +985,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   TRY(dev_alloc(&h->spill, (size_t)std::max(h->nwarps, 1) * (B + 1), &alloc_ms, &bytes));
   if (pcs > 0 && h->nwarps > 0) {
     TRY(dev_alloc(&h->warp_begin, (size_t)h->nwarps + 1, &alloc_ms, &bytes));
-    auto* emax = reinterpret_cast<unsigned long long*>(scal + 6);
-    TRYC(cudaMemsetAsync(emax, 0, sizeof(unsigned long long), stream));
+    auto* emax = reinterpret_cast<unsigned long long*>(scal + 6);  // zeroed with the block
     k_equal_split_max<<<(unsigned)((h->nwarps + 255) / 256), 256, 0, stream>>>(
         work_prefix, pcs, h->nwarps, emax);
     TRYC(cudaGetLastError());
