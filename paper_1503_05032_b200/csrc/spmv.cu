@@ -456,10 +456,14 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
       const uint64_t above = (uint64_t)hb >> (lane + 1);
       const int end = above ? lane + __ffsll((long long)above) - 1 : 31;
       double acc = tmp;
+      // every column holds a head (rows no longer than sigma: stencils,
+      // Laplacians): end == lane on every lane, the scan adds nothing
+      if (hb != kFull) {
   #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const double o = __shfl_down_sync(kFull, acc, d);
-        if (lane + d <= end) acc += o;
+        for (int d = 1; d < 32; d <<= 1) {
+          const double o = __shfl_down_sync(kFull, acc, d);
+          if (lane + d <= end) acc += o;
+        }
       }
       if (seen) {  // the column's bottom piece
         if (fast)
