@@ -715,7 +715,11 @@ int spmv_plan(Handle* h, int sms) {
   // random gathers: two stages -- the shared memory a third would take is
   // worth more as L1 for outstanding gather misses (measured: R-MAT s24 at
   // 150 KB, 7 warps: 2 stages 1.67 ms, 3 stages 2.11 ms)
-  int nw = (h->nf ? spmv_threads_nf(sigma) : spmv_threads(sigma)) / 32, stages = random ? 2 : 4;
+  // NF plans (short tiles, sigma <= 8): two stages too -- the 2 KB tile
+  // arrives well within one tile's work, and the smaller ring leaves more L1
+  // (Laplacian 1000^2 at 24 warps: 2 / 3 stages 25.1 / 26.0 us mean)
+  int nw = (h->nf ? spmv_threads_nf(sigma) : spmv_threads(sigma)) / 32,
+      stages = random || h->nf ? 2 : 4;
   // one mbarrier per warp and stage at the start, 128-byte aligned
   auto bars = [](int w, int st) { return (w * st * 8 + 127) / 128 * 128; };
   auto need = [&](int w, int st) {
