@@ -270,12 +270,13 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
   if (has_tiles) {
     double* __restrict__ y = a.y;
     const bool yh = a.y_hint != 0;
+    const bool mirrored = a.mir.n != 0;
     auto put_y = [&](int64_t r, double v) {
       if (yh)
         st_hint(y + r, v, pol_s);
       else
         y[r] = v;
-      if (a.mir.n) mirror_store(a.mir, r, v);
+      if (mirrored) mirror_store(a.mir, r, v);
     };
     int64_t pend_row = -1;
     double pend_val = 0.0;
@@ -453,12 +454,12 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
       double tmp = __shfl_down_sync(kFull, give, 1);
       if (lane == 31) tmp = 0.0;
       const uint32_t hb = __ballot_sync(kFull, seen);
-      const uint64_t above = (uint64_t)hb >> (lane + 1);
-      const int end = above ? lane + __ffsll((long long)above) - 1 : 31;
       double acc = tmp;
       // every column holds a head (rows no longer than sigma: stencils,
       // Laplacians): end == lane on every lane, the scan adds nothing
       if (hb != kFull) {
+        const uint64_t above = (uint64_t)hb >> (lane + 1);
+        const int end = above ? lane + __ffsll((long long)above) - 1 : 31;
   #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
           const double o = __shfl_down_sync(kFull, acc, d);
