@@ -1,19 +1,23 @@
 #!/usr/bin/env python
 """CSR5 fp64 SpMV benchmark on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload st27_200]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload rmat27]
     python bench.py --impl reference ...        # the reference's CPU path
 
 One step = one CSR5 SpMV y = A x over the whole matrix (one pass of the hot
-path).  At N=1 the workload is BASELINE config 2, the 3D 27-point stencil
-200^3 (213.8M nnz, sigma = 27 by the reference rule, 64-bit descriptors).
-Under torchrun (N>1) the matrix is tile-range sharded over the ranks with x
-replicated; a step includes the boundary-row exchange (NVLink P2P
-stores into the owner's mailbox, p2p.cu; no collective).  Default
---scaling weak: the global matrix is N times the 1-GPU one (the stencil N
-times deeper along z, graphs log2 N scales larger: R-MAT s24 -> s27 at N=8,
-BASELINE config 5), so per-GPU work is fixed; --scaling strong shards the
-1-GPU matrix itself.
+path).  The workload at every N is BASELINE config 5, R-MAT scale 27 edge
+factor 16 (2^27 rows, 2.115G nonzeros after de-duplication, vertices
+permuted, sigma = 16): the largest single-GPU configuration and the one the
+1/2/4/8-GPU curve is quoted on.  Under torchrun (N>1) the matrix is
+tile-range sharded over the ranks with x replicated (--scaling strong: the
+same global matrix at every N, each rank generating only its slice); a step
+includes the boundary-row exchange (NVLink P2P stores into the owner's
+mailbox, p2p.cu; no collective).
+
+At N=1 the line also carries `sub_results` for the other BASELINE configs
+(27-point stencil 200^3, R-MAT s24, mixed 2^23, 2D Laplacian 1000^2), each
+measured the same way with its own roofline, conversion, e2e and CPU
+baseline (--sub none skips them).
 
 `value` is GFLOP/s = 2*nnz / t with A and x resident in HBM; t is the max over
 ranks of CUDA-event time on the launching stream.  L2 is flushed between timed
@@ -26,6 +30,7 @@ algorithmic bytes of SURVEY 8(d).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -39,6 +44,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "CSR5 fp64 SpMV GFLOP/s + HBM GB/s (% roofline) at 1/2/4/8 B200; conv cost"
 UNIT = "GFLOP/s"
+DEFAULT_WORKLOAD = "rmat27"
+SUB_WORKLOADS = ("st27_200", "rmat24", "mixed23", "lap5_1000")
 
 
 def peaks():
@@ -114,6 +121,13 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def pin_openmp():
+    """SURVEY 8d / BASELINE.md §3: the reference's OpenMP threads pinned one per
+    core.  Set before the reference library (and its libgomp) is loaded."""
+    os.environ.setdefault("OMP_PLACES", "cores")
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+
+
 # --------------------------------------------------------------------------
 # the reference's CPU path (oracle/_ref = the unmodified reference library)
 # --------------------------------------------------------------------------
@@ -122,16 +136,23 @@ def host_matrix(workload: dict):
     Stencils come from the host generator (oracle/testgen.c, no GPU needed);
     the graph workloads are generated on the device and copied back."""
     import numpy as np
+    import torch
 
     from oracle.oracle import Csr, Oracle, stencil
     if workload["gen"] == "stencil":
         return stencil(Oracle(), workload["kind"], workload["a"], workload.get("layers"))
     from paper_1503_05032_b200.synthetic import make_matrix
     d = make_matrix(workload, "cuda")
-    a = Csr(d.m, d.n, d.row_ptr.cpu().numpy(), d.col_idx.cpu().numpy().astype(np.int64),
-            d.val.cpu().numpy())
+    rp = d.row_ptr.cpu().numpy()
+    col = np.empty(d.nnz, dtype=np.int64)
+    step = 1 << 28  # int32 -> int64 in slices (no whole int32 host copy)
+    for lo in range(0, d.nnz, step):
+        col[lo:lo + step] = d.col_idx[lo:lo + step].cpu().numpy()
+    val = d.val.cpu().numpy()
+    m, n = d.m, d.n
     del d
-    return a
+    torch.cuda.empty_cache()
+    return Csr(m, n, rp, col, val)
 
 
 def workload_n(workload: dict) -> int:
@@ -141,59 +162,58 @@ def workload_n(workload: dict) -> int:
     return 1 << (workload["scale"] if workload["gen"] == "rmat" else workload["log2_m"])
 
 
-def reference_cpu(workload: dict, x, budget_s: float, omega=4, sigma=16, steps=None, warmup=0,
-                  also_w32=False):
-    """Time the reference csr5::spmv_csr5 (deterministic) on the host cores.
+def reference_cpu(workload: dict, x, budget_s: float, configs=((4, 16),), steps=None, warmup=0):
+    """Time the reference csr5::spmv_csr5 (deterministic) on the host cores,
+    once per (omega, sigma) in `configs` (sigma 0 = the reference's own
+    select_sigma rule).  Handles are built one at a time and the host CSR is
+    dropped as soon as the last one exists (R-MAT s27 in the reference's
+    int64 form is ~35 GB per copy).
 
     steps=None: the bench.cpp:147-160 protocol (samples of `inner` back-to-back
-    calls, best sample reported) within ~budget_s.  steps=K: K single calls
-    after `warmup` calls (the --impl reference step loop)."""
+    calls, best sample reported) within ~budget_s per config.  steps=K: K single
+    calls after `warmup` calls (the --impl reference step loop)."""
     import ctypes
 
     import numpy as np
 
-    from oracle.oracle import Ref
+    from oracle.oracle import Oracle, Ref
     ref = Ref()
     t0 = time.time()
     a = host_matrix(workload)
     gen_s = time.time() - t0
-    h, conv_ms = ref.build_handle(a, omega, sigma)
+    m, n, nnz = a.m, a.n, a.nnz
     dp = ctypes.POINTER(ctypes.c_double)
-    xv = ref.L.ref_vec_new(np.ascontiguousarray(x).ctypes.data_as(dp), a.n)
-    y = np.zeros(a.m)
+    xv = ref.L.ref_vec_new(np.ascontiguousarray(x).ctypes.data_as(dp), n)
+    out = []
+    y = np.zeros(m)
     yp = y.ctypes.data_as(dp)
-    first = ref.L.ref_time_spmv(h, xv, yp, 0, 1)
-    if steps is None:
-        inner = max(1, int(0.5 / max(first / 1e3, 1e-6)))
-        samples = []
-        t_end = time.time() + budget_s
-        while (time.time() < t_end or len(samples) < 2) and len(samples) < 10:
-            samples.append(ref.L.ref_time_spmv(h, xv, yp, 0, inner))
-    else:
-        inner = 1
-        for _ in range(warmup):
-            ref.L.ref_time_spmv(h, xv, yp, 0, 1)
-        samples = [ref.L.ref_time_spmv(h, xv, yp, 0, 1) for _ in range(steps)]
-    scalar = ref.L.ref_time_csr_scalar(h, xv, yp, 3)
-    ref.L.ref_time_spmv(h, xv, yp, 0, 1)  # leave y = the csr5 result
-    threads = ref.max_threads()
-    w32 = None
-    if also_w32:  # SURVEY 8d: the GPU's own omega = 32, sigma = auto on the CPU too
-        from oracle.oracle import Oracle
-        s32 = Oracle().select_sigma(a.nnz / max(a.m, 1))
-        h32, conv32 = ref.build_handle(a, 32, s32)
-        y32 = np.zeros(a.m)
-        p32 = y32.ctypes.data_as(dp)
-        one = ref.L.ref_time_spmv(h32, xv, p32, 0, 1)
-        inner32 = max(1, int(0.5 / max(one / 1e3, 1e-6)))
-        best = min(ref.L.ref_time_spmv(h32, xv, p32, 0, inner32) for _ in range(3))
-        ref.L.ref_free(h32)
-        w32 = dict(omega=32, sigma=s32, best_ms=best, conv_ms=conv32, inner=inner32)
+    for ci, (omega, sigma) in enumerate(configs):
+        if sigma == 0:
+            sigma = Oracle().select_sigma(nnz / max(m, 1))
+        h, conv_ms = ref.build_handle(a, omega, sigma)
+        if ci == len(configs) - 1:
+            a = None  # the handle holds its own copy of the CSR
+            gc.collect()
+        first = ref.L.ref_time_spmv(h, xv, yp, 0, 1)
+        if steps is None:
+            inner = max(1, int(0.5 / max(first / 1e3, 1e-6)))
+            samples = []
+            t_end = time.time() + budget_s
+            while (time.time() < t_end or len(samples) < 2) and len(samples) < 10:
+                samples.append(ref.L.ref_time_spmv(h, xv, yp, 0, inner))
+        else:
+            inner = 1
+            for _ in range(warmup):
+                ref.L.ref_time_spmv(h, xv, yp, 0, 1)
+            samples = [ref.L.ref_time_spmv(h, xv, yp, 0, 1) for _ in range(steps)]
+        scalar = ref.L.ref_time_csr_scalar(h, xv, yp, 2) if ci == 0 else None
+        ref.L.ref_time_spmv(h, xv, yp, 0, 1)  # leave y = the csr5 result
+        ref.L.ref_free(h)
+        out.append(dict(omega=omega, sigma=sigma, best_ms=min(samples),
+                        mean_ms=sum(samples) / len(samples), samples=samples, inner=inner,
+                        conv_ms=conv_ms, csr_scalar_ms=scalar))
     ref.L.ref_vec_free(xv)
-    ref.L.ref_free(h)
-    return dict(nnz=a.nnz, m=a.m, best_ms=min(samples), mean_ms=sum(samples) / len(samples),
-                samples=samples, inner=inner, conv_ms=conv_ms, gen_s=gen_s, threads=threads,
-                csr_scalar_ms=scalar, omega=omega, sigma=sigma, y=y, w32=w32)
+    return dict(nnz=nnz, m=m, n=n, gen_s=gen_s, threads=ref.max_threads(), runs=out, y=y)
 
 
 def est_nnz(wl: dict) -> int:
@@ -230,183 +250,149 @@ def cpu_info():
     return model, os.cpu_count()
 
 
+def host_fits(wl: dict) -> tuple[bool, str]:
+    """Can the host hold the reference's copies of this matrix?  ~56 B per
+    nonzero at the peak: the int64 CSR handed over, the reference's own copy
+    and the Csr5Matrix being built."""
+    need = 56 * est_nnz(wl)
+    avail = mem_available()
+    if avail is None or need < 0.85 * avail:
+        return True, ""
+    return False, (f"needs ~{need / 1e9:.0f} GB of host RAM for the reference's copies, "
+                   f"{avail / 1e9:.0f} GB available")
+
+
 def run_reference(args, workload_name, workload):
     """--impl reference: the reference's own CPU implementation (oracle/_ref,
-    compiled from /root/reference/proj/core/src) on all host threads; rank 0
-    only under torchrun."""
+    compiled from /root/reference/proj/core/src) on all host threads, OpenMP
+    pinned; rank 0 only under torchrun.  Both its CPU default (omega=4,
+    sigma=16, tuning.hpp:14-15) and the GPU's omega=32 / sigma=auto are
+    stepped; `value` is the faster of the two."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_1503_05032_b200.synthetic import bench_x, scaled_workload
-    note = "1-GPU workload"
+    from paper_1503_05032_b200.synthetic import WORKLOADS, bench_x, scaled_workload
+    note = "the benchmark workload"
     if world > 1 and args.scaling == "weak":
-        # the same global matrix as our arm, when the host can hold the
-        # reference's copies of it (~40 B per nonzero: int64 CSR + Csr5Matrix)
-        wl_g = scaled_workload(workload, world)
-        need = 40 * est_nnz(wl_g)
-        avail = mem_available()
-        if avail is None or need < 0.6 * avail:
-            workload, note = wl_g, f"global matrix of the {world}-GPU weak-scaling run"
-        else:
-            note = (f"1-GPU workload: the {world}x matrix needs ~{need / 1e9:.0f} GB of host RAM, "
-                    f"{avail / 1e9:.0f} GB available")
-    r = reference_cpu(workload, bench_x(workload_n(workload)), 0.0, steps=args.steps,
-                      warmup=args.warmup)
-    ms = r["mean_ms"]
-    gf = 2.0 * r["nnz"] / (ms * 1e6)
+        workload, note = scaled_workload(workload, world), f"global matrix of the {world}-GPU run"
+    ok, why = host_fits(workload)
+    if not ok:  # fall back to the largest graph config the host holds
+        workload_name, workload = "rmat24", WORKLOADS["rmat24"]
+        note = f"R-MAT s24 instead: {why}"
+    r = reference_cpu(workload, bench_x(workload_n(workload)), 0.0,
+                      configs=((4, 16), (32, 0)), steps=args.steps, warmup=args.warmup)
     model, ncpu = cpu_info()
+    runs = r["runs"]
+    gf = [2.0 * r["nnz"] / (q["mean_ms"] * 1e6) for q in runs]
+    best = max(range(len(runs)), key=lambda i: gf[i])
+    q = runs[best]
+    ms = q["mean_ms"]
     sample = (f"full {workload_name} matrix ({note}, nnz={r['nnz']}), reference csr5::spmv_csr5 "
-              f"omega={r['omega']} sigma={r['sigma']} deterministic, one call per step")
+              f"deterministic, one call per step; omega/sigma {runs[0]['omega']}/"
+              f"{runs[0]['sigma']} (its CPU default) and {runs[1]['omega']}/{runs[1]['sigma']} "
+              f"(the GPU's), the faster reported")
     line = {
-        "impl": "reference", "metric": METRIC, "value": gf, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference", "metric": METRIC, "value": gf[best], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": workload_name, "desc": workload["desc"], "nnz": r["nnz"],
-                   "m": r["m"], "omega": r["omega"], "sigma": r["sigma"], "mode": "deterministic"},
-        "cpu_baseline": {"value": gf, "unit": UNIT, "cores": r["threads"], "kind": "reference",
-                         "sample": sample, "cpu_model": model, "nproc": ncpu,
-                         "conv_ms": r["conv_ms"], "conv_spmv_equiv": r["conv_ms"] / ms,
-                         "csr_scalar_gflops": 2.0 * r["nnz"] / (r["csr_scalar_ms"] * 1e6)},
-        "e2e": {"value": gf, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "m": r["m"], "omega": q["omega"], "sigma": q["sigma"],
+                   "mode": "deterministic"},
+        "cpu_baseline": {"value": gf[best], "unit": UNIT, "cores": r["threads"],
+                         "kind": "reference", "sample": sample, "cpu_model": model,
+                         "nproc": ncpu,
+                         "omp": {k: os.environ.get(k) for k in ("OMP_PLACES", "OMP_PROC_BIND")},
+                         "runs": [{"omega": p["omega"], "sigma": p["sigma"], "gflops": g,
+                                   "ms_per_step": p["mean_ms"], "conv_ms": p["conv_ms"],
+                                   "conv_spmv_equiv": p["conv_ms"] / p["mean_ms"]}
+                                  for p, g in zip(runs, gf)],
+                         "csr_scalar_gflops": 2.0 * r["nnz"] / (runs[0]["csr_scalar_ms"] * 1e6)},
+        "e2e": {"value": gf[best], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def cpu_baseline(args, name, wl, x_host, y_gpu):
+    """The reference on the host cores of this box, a bounded sample: both
+    configurations, best of a few samples each (bench.cpp:147-160)."""
+    import numpy as np
+    ok, why = host_fits(wl)
+    if not ok:
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
+                "sample": f"skipped: {why}"}
+    try:
+        budget = args.cpu_seconds if name == args.workload else args.cpu_seconds / 2
+        r = reference_cpu(wl, x_host, budget_s=budget, configs=((4, 16), (32, 0)))
+    except Exception as e:  # the CPU number is reported, never gating
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
+                "sample": f"failed: {e}"}
+    model, ncpu = cpu_info()
+    yr = r.pop("y")
+    d, w32 = r["runs"]
+    return {"value": 2.0 * r["nnz"] / (d["best_ms"] * 1e6), "unit": UNIT,
+            "cores": r["threads"], "kind": "reference",
+            "sample": (f"full {name} matrix, reference csr5::spmv_csr5 omega={d['omega']} "
+                       f"sigma={d['sigma']} deterministic; best of {len(d['samples'])} samples "
+                       f"x {d['inner']} calls"),
+            "cpu_model": model, "nproc": ncpu,
+            "omp": {k: os.environ.get(k) for k in ("OMP_PLACES", "OMP_PROC_BIND")},
+            "conv_ms": d["conv_ms"],
+            # SURVEY 8d: the reference's own widths (8 B val + 8 B col_idx), x
+            # and y once; its small metadata excluded
+            "gbs_ref_widths": (16 * r["nnz"] + 8 * (r["m"] + r["n"])) / (d["best_ms"] * 1e6),
+            "conv_spmv_equiv": d["conv_ms"] / d["best_ms"],
+            "csr_scalar_gflops": 2.0 * r["nnz"] / (d["csr_scalar_ms"] * 1e6),
+            "y_max_rel_err_vs_gpu": float(np.max(np.abs(yr - y_gpu) /
+                                                 np.maximum(1.0, np.abs(yr)))),
+            "omega32": {"sigma": w32["sigma"],
+                        "gflops": 2.0 * r["nnz"] / (w32["best_ms"] * 1e6),
+                        "conv_ms": w32["conv_ms"],
+                        "sample": f"best of {len(w32['samples'])} samples x {w32['inner']} calls"}}
+
+
 # --------------------------------------------------------------------------
-# our arm
+# our arm, one GPU
 # --------------------------------------------------------------------------
-def run_ours(args, workload_name, workload):
+def measure_one(args, name, workload, dev, local):
+    """Every measurement of one workload on one GPU: conversion, correctness
+    guard, K timed steps, the tile kernel's roofline, e2e through host buffers,
+    comparators and the CPU baseline.  Returns the result dict."""
     import numpy as np
     import torch
 
-    from paper_1503_05032_b200 import csr5, mg
-    from paper_1503_05032_b200.synthetic import bench_x
-    rank, world, local = dist_env()
-    if world > 1:
-        # a rank that never sees a peer's flag would block its stream forever:
-        # turn such a hang into a loud failure (the whole run takes minutes)
-        limit = float(os.environ.get("CSR5G_WATCHDOG_S", "300"))
-
-        def _watchdog():
-            time.sleep(limit)
-            sys.stderr.write(f"bench.py rank {rank}: no completion after {limit:.0f} s "
-                             "(multi-GPU exchange stalled?); aborting\n")
-            sys.stderr.flush()
-            os._exit(3)
-
-        threading.Thread(target=_watchdog, daemon=True).start()
-    if os.environ.get("CSR5G_SHARE_GPU") == "1":  # functional multi-rank check on one GPU
-        local %= torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        # NCCL over NVLink; CSR5G_DIST_BACKEND=gloo lets several ranks share one
-        # GPU for a functional check of the sharded flow (not a timing)
-        backend = os.environ.get("CSR5G_DIST_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
-
-    from paper_1503_05032_b200.synthetic import WorkloadMatrix, make_matrix, scaled_workload
-    if world == 1:
-        a = make_matrix(workload, dev)
-        m, n, nnz = a.m, a.n, a.nnz
-    else:
-        # weak: the global matrix is `world` times the 1-GPU one; strong: the
-        # 1-GPU matrix itself.  Either way each rank generates the global
-        # row_ptr and only its own slice of entries where the generator allows.
-        if args.scaling == "weak":
-            workload = scaled_workload(workload, world)
-        W = WorkloadMatrix(workload, dev)
-        m, n, nnz = W.m, W.n, W.nnz
+    from paper_1503_05032_b200 import csr5
+    from paper_1503_05032_b200.synthetic import bench_x, make_matrix
+    a = make_matrix(workload, dev)
+    m, n, nnz = a.m, a.n, a.nnz
     torch.cuda.synchronize()
     x_host = bench_x(n)
     x = torch.as_tensor(x_host).to(dev)
     y = torch.empty(m, dtype=torch.float64, device=dev)
     sigma = csr5.select_sigma(nnz / m)
+    big = nnz > 1_000_000_000
 
     # -- conversion (device-resident CSR -> usable CSR5), timed twice --------
-    if world == 1:
-        a5 = csr5.csr_to_csr5(a, csr5.TuningParams(sigma=sigma))
-        a5.release()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        a5 = csr5.csr_to_csr5(a, csr5.TuningParams(sigma=sigma))
-        conv_ms = (time.perf_counter() - t0) * 1e3
-        info = a5.info
-        run = lambda: csr5.spmv_csr5(a5, x, y)  # noqa: E731
-    else:
-        lo, hi = mg.Csr5Sharded.slices_for(nnz, sigma, rank, world)
-        col_s, val_s = W.entries(lo, hi)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        sh = mg.Csr5Sharded(W.row_ptr, col_s, val_s, m, n, nnz, sigma, rank, world,
-                            iterative=args.iterative and m == n)
-        torch.cuda.synchronize()
-        conv_ms = (time.perf_counter() - t0) * 1e3
-        del col_s, val_s
-        a5 = sh.a5
-        info = a5.info if a5 is not None else None
-        run = lambda: sh.spmv(x, y)  # noqa: E731
+    a5 = csr5.csr_to_csr5(a, csr5.TuningParams(sigma=sigma))
+    a5.release()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a5 = csr5.csr_to_csr5(a, csr5.TuningParams(sigma=sigma))
+    conv_ms = (time.perf_counter() - t0) * 1e3
+    info = a5.info
+    run = lambda: csr5.spmv_csr5(a5, x, y)  # noqa: E731
 
-    # -- correctness guard before timing (bench.cpp:130-141 analogue) --------
-    # y over the rows this rank writes, against cuSPARSE (torch sparse CSR)
+    # -- correctness guard before timing (bench.cpp:130-141 analogue): y
+    # against cuSPARSE (torch sparse CSR) --------------------------------------
     run()
     torch.cuda.synchronize()
-    if world == 1:
-        own = (0, m)
-        rp_own, col_own, val_own = a.row_ptr, a.col_idx, a.val
-    else:
-        own = sh.own
-        rp_own = W.row_ptr[own[0]:own[1] + 1]
-        e0, e1 = (int(rp_own[0]), int(rp_own[-1])) if own[1] > own[0] else (0, 0)
-        col_own, val_own = W.entries(e0, e1)
-        rp_own = rp_own - e0
-    err = 0.0
-    if own[1] > own[0]:
-        A = torch.sparse_csr_tensor(rp_own, col_own.long(), val_own, (own[1] - own[0], n))
-        y_chk = (A @ x.unsqueeze(1)).squeeze(1)
-        err = ((y[own[0]:own[1]] - y_chk).abs() / y_chk.abs().clamp(min=1.0)).max().item()
-        del A, y_chk
-    del rp_own, col_own, val_own
-    if world > 1:
-        W.drop()
+    A = torch.sparse_csr_tensor(a.row_ptr, a.col_idx.long(), a.val, (m, n))
+    y_chk = (A @ x.unsqueeze(1)).squeeze(1)
+    err = ((y - y_chk).abs() / y_chk.abs().clamp(min=1.0)).max().item()
+    del A, y_chk
+    torch.cuda.empty_cache()
     if not err <= 1e-12:
-        raise SystemExit(f"correctness guard: max relative error {err} > 1e-12")
-    it_ctr = [0]
-    if world > 1 and sh.iterative:
-        # fused y -> x (p2p.cu): one step from x must leave every active rank
-        # with the same x_1, whose owned rows are the y just checked (bit for bit)
-        sh.x_buffer(0).copy_(x)
-        x1 = sh.spmv_iter(0)
-        it_ctr[0] = 1
-        torch.cuda.synchronize()
-        same = bool(torch.equal(x1[own[0]:own[1]], y[own[0]:own[1]])) if sh.active else True
-        h = torch.tensor([int(sh.active), int(same),
-                          int(x1.view(torch.int64).sum().item()) if sh.active else 0],
-                         dtype=torch.int64, device=dev if dist.get_backend() == "nccl" else "cpu")
-        hs = [torch.empty_like(h) for _ in range(world)]
-        dist.all_gather(hs, h)
-        act = [v for v in hs if int(v[0])]
-        if not all(int(v[1]) for v in act) or len({int(v[2]) for v in act}) != 1:
-            raise SystemExit("correctness guard: fused iterative x_1 differs between ranks or from y")
-        if sh.mailbox_errors():
-            raise SystemExit("correctness guard: P2P mailbox protocol errors")
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-
-    def max_over_ranks(v: float) -> float:
-        if dist is None:
-            return v
-        t = torch.tensor([v], dtype=torch.float64,
-                         device=dev if dist.get_backend() == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return t.item()
+        raise SystemExit(f"{name}: correctness guard: max relative error {err} > 1e-12")
 
     # L2 flushed between timed calls (a 2x-L2 read outside the events), so no
     # step starts with x or the matrix left in L2 by the previous one; a read
@@ -420,33 +406,19 @@ def run_ours(args, workload_name, workload):
     tk = [(csr5.Event(), csr5.Event()) for _ in range(args.steps)]
     clocks = ClockSampler(local)
     torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
-    # the steps: the public call alone between the events (iterative mode:
-    # plus y -> x, the all-gather of the owned ranges at N>1)
-    if args.iterative:
-        if m != n:
-            raise SystemExit("--iterative needs a square matrix")
+    if args.iterative:  # ping-pong: y of this step is x of the next
         x_keep = x.clone()
         bufs = [x, y]
 
         def step():
-            if world == 1:  # ping-pong: y of this step is x of the next
-                csr5.spmv_csr5(a5, bufs[0], bufs[1])
-                bufs.reverse()
-            elif sh.iterative:  # fused: the SpMV stores y into every rank's next x
-                sh.spmv_iter(it_ctr[0])
-                it_ctr[0] += 1
-            else:
-                run()
-                sh.gather_y_into_x(y, x)
+            csr5.spmv_csr5(a5, bufs[0], bufs[1])
+            bufs.reverse()
     else:
         step = run
     for k in range(args.steps):
-        if scrub is not None:
-            scrub.sum()  # read-only flush: evicts without leaving dirty lines
+        scrub.sum()  # read-only flush: evicts without leaving dirty lines
         steps_ev[k][0].record()
         step()
         steps_ev[k][1].record()
@@ -454,140 +426,121 @@ def run_ours(args, workload_name, workload):
         x.copy_(x_keep)
         del x_keep
     torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
     # the dominant kernel for the roofline: the same steps again with events
     # recorded around the tile kernel on its stream
     for k in range(args.steps):
-        if scrub is not None:
-            scrub.sum()  # read-only flush: evicts without leaving dirty lines
-        if world == 1:
-            csr5.spmv_csr5_evt(a5, x, y, tk[k][0], tk[k][1])
-        elif a5 is not None:
-            sh.spmv(x, y, events=tk[k])
-        else:
-            run()
-    torch.cuda.synchronize()
-    barrier()
+        scrub.sum()
+        csr5.spmv_csr5_evt(a5, x, y, tk[k][0], tk[k][1])
     torch.cuda.synchronize()
     clk = clocks.stop()
-    total_ms = max_over_ranks(sum(b.elapsed_ms(e) for b, e in steps_ev))
-    ms = total_ms / args.steps
-    tile_all = sorted(b.elapsed_ms(e) for b, e in tk) if a5 is not None else None
-    tile_ms = (sum(tile_all) / args.steps) if tile_all else None
+    ms = sum(b.elapsed_ms(e) for b, e in steps_ev) / args.steps
+    tile_all = sorted(b.elapsed_ms(e) for b, e in tk)
+    tile_ms = sum(tile_all) / args.steps
 
     # -- end to end through the host-buffer call ------------------------------
-    # Every step moves its own x in from pinned host memory and its y out.
-    # N=1: csr5.spmv_host_batch (csr5g_spmv_host_batch), which pipelines step
-    # k+1's x H2D and step k's y D2H around SpMV k on separate copy engines.
-    # The serial form (H2D, SpMV, D2H back to back on one stream) is reported
-    # beside it.  N>1: the serial form through the sharded driver.
-    ring = min(args.steps, 4)
+    # Every step moves its own x in from pinned host memory and its y out:
+    # csr5.spmv_host_batch (csr5g_spmv_host_batch) pipelines step k+1's x H2D
+    # and step k's y D2H around SpMV k on separate copy engines.  The serial
+    # form (H2D, SpMV, D2H back to back on one stream) is reported beside it.
+    ring = 2 if big else min(args.steps, 4)
     xh = [torch.as_tensor(x_host).pin_memory() for _ in range(ring)]
     yh = [torch.empty(m, dtype=torch.float64).pin_memory() for _ in range(ring)]
+
+    def timed(fn):
+        e0, e1 = csr5.Event(), csr5.Event()
+        torch.cuda.synchronize()
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_ms(e1) / args.steps
 
     def e2e_serial(k):
         x.copy_(xh[k % ring], non_blocking=True)
         run()
         yh[k % ring].copy_(y, non_blocking=True)
 
-    def e2e_timed(fn):
-        e0, e1 = csr5.Event(), csr5.Event()
-        torch.cuda.synchronize()
-        barrier()
-        e0.record()
-        fn()
-        e1.record()
-        torch.cuda.synchronize()
-        return max_over_ranks(e0.elapsed_ms(e1)) / args.steps
-
-    for k in range(args.warmup):
+    for k in range(min(args.warmup, 2)):
         e2e_serial(k)
-    e2e_serial_ms = e2e_timed(lambda: [e2e_serial(k) for k in range(args.steps)])
-    e2e_path = "serial: pinned x H2D + spmv + y D2H per step, one stream, CUDA events"
-    e2e_ms = e2e_serial_ms
-    e2e_trials = None
-    pcie_ms = None
-    if world == 1:
-        xs = [xh[k % ring] for k in range(args.steps)]
-        ys = [yh[k % ring] for k in range(args.steps)]
-        csr5.spmv_host_batch(a5, xs[:args.warmup], ys[:args.warmup])
-        # three runs of the K-step batch, the median reported: a single run
-        # is exposed to host-side PCIe hiccups (one default run on a fresh box
-        # saw its copies alone 10% slower and the batch 60% slower)
-        e2e_trials = sorted(e2e_timed(lambda: csr5.spmv_host_batch(a5, xs, ys)) for _ in range(3))
-        e2e_ms = e2e_trials[1]
-        e2e_path = ("csr5.spmv_host_batch (csr5g_spmv_host_batch): per step pinned x H2D + SpMV + "
-                    "y D2H, x_{k+1} H2D and y_k D2H overlapping SpMV k; CUDA events on the "
-                    "caller stream")
-        err_h = float(np.max(np.abs(yh[(args.steps - 1) % ring].numpy() - y.cpu().numpy())))
-        if err_h != 0.0:
-            raise SystemExit(f"host-batch path differs from the device path by {err_h}")
-        # the PCIe ceiling of this e2e: the same per-step copies (x in, y out,
-        # concurrently on two streams) with no SpMV at all
-        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-        xd2, yd2 = torch.empty_like(x), y.clone()
+    e2e_serial_ms = timed(lambda: [e2e_serial(k) for k in range(args.steps)])
+    xs = [xh[k % ring] for k in range(args.steps)]
+    ys = [yh[k % ring] for k in range(args.steps)]
+    csr5.spmv_host_batch(a5, xs[:2], ys[:2])
+    # three runs of the K-step batch, the median reported: a single run is
+    # exposed to host-side PCIe hiccups
+    e2e_trials = sorted(timed(lambda: csr5.spmv_host_batch(a5, xs, ys)) for _ in range(3))
+    e2e_ms = e2e_trials[1]
+    x.copy_(xh[0])
+    run()
+    torch.cuda.synchronize()
+    err_h = float((yh[(args.steps - 1) % ring].to(dev) - y).abs().max().item())
+    if err_h != 0.0:
+        raise SystemExit(f"{name}: host-batch path differs from the device path by {err_h}")
+    # the PCIe ceiling of this e2e: the same per-step copies (x in, y out,
+    # concurrently on two streams) with no SpMV at all
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    xd2, yd2 = torch.empty_like(x), y.clone()
 
-        def duplex():
-            cur = torch.cuda.current_stream()
-            s_in.wait_stream(cur)
-            s_out.wait_stream(cur)
-            for k in range(args.steps):
-                with torch.cuda.stream(s_in):
-                    xd2.copy_(xh[k % ring], non_blocking=True)
-                with torch.cuda.stream(s_out):
-                    yh[k % ring].copy_(yd2, non_blocking=True)
-            cur.wait_stream(s_in)
-            cur.wait_stream(s_out)
+    def duplex():
+        cur = torch.cuda.current_stream()
+        s_in.wait_stream(cur)
+        s_out.wait_stream(cur)
+        for k in range(args.steps):
+            with torch.cuda.stream(s_in):
+                xd2.copy_(xh[k % ring], non_blocking=True)
+            with torch.cuda.stream(s_out):
+                yh[k % ring].copy_(yd2, non_blocking=True)
+        cur.wait_stream(s_in)
+        cur.wait_stream(s_out)
 
-        duplex()
-        pcie_ms = sorted(e2e_timed(duplex) for _ in range(3))[1]
+    duplex()
+    pcie_ms = sorted(timed(duplex) for _ in range(3))[1]
+    del xh, yh, xs, ys, xd2, yd2
 
     # -- iteration scenario (bench.cpp:86-90, 164-175): the GPU plain-CSR
     # baseline beside CSR5, conversion amortised over n solver iterations ----
-    iteration = None
-    if world == 1:
-        from paper_1503_05032_b200.benchmark import iteration_speedup
-        # every comparator timed like the CSR5 step: L2 flushed before each call
-        # (a read of 2x L2), CUDA events around the call alone
-        def timed_flushed(fn, reps=5):
-            fn()
-            tot = 0.0
-            for _ in range(reps):
-                scrub.sum()
-                b, e = csr5.Event(), csr5.Event()
-                b.record()
-                fn()
-                e.record()
-                torch.cuda.synchronize()
-                tot += b.elapsed_ms(e)
-            return tot / reps
+    from paper_1503_05032_b200.benchmark import iteration_speedup
 
-        t_csr = {}
-        for k in ("csr-scalar", "csr-segsum"):
-            try:
-                t_csr[k] = timed_flushed(lambda: csr5.spmv_csr(a, x, y, kernel=k))
-            except MemoryError:
-                t_csr[k] = None
-        # library comparator: cuSPARSE csrmv through torch sparse CSR (int64
-        # indices, so it moves 16 B per nonzero to our 12)
-        t_lib = None
+    def timed_flushed(fn, reps=3):
+        fn()
+        tot = 0.0
+        for _ in range(reps):
+            scrub.sum()
+            b, e = csr5.Event(), csr5.Event()
+            b.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize()
+            tot += b.elapsed_ms(e)
+        return tot / reps
+
+    t_csr = {}
+    for k in ("csr-scalar", "csr-segsum"):
         try:
-            A = torch.sparse_csr_tensor(a.row_ptr, a.col_idx.long(), a.val, (m, n))
-            xc = x.unsqueeze(1)
-            t_lib = timed_flushed(lambda: A @ xc)
-            del A, xc
-        except Exception:
-            pass
-        if t_csr["csr-scalar"]:
-            iteration = {"t_cusparse_csrmv_ms": t_lib,"t_csr_scalar_ms": t_csr["csr-scalar"],
-                         "t_csr_segsum_ms": t_csr["csr-segsum"], "t_csr5_ms": ms,
-                         "t_conv_ms": conv_ms,
-                         "speedup_n50": iteration_speedup(t_csr["csr-scalar"], conv_ms, ms, 50),
-                         "speedup_n500": iteration_speedup(t_csr["csr-scalar"], conv_ms, ms, 500),
-                         "baseline": "GPU csr-scalar (one thread per row), spmv.cpp:139-154"}
-        # ingest: device COO -> CSR (csr.cpp:35-72) of this matrix's entries in
-        # a random order (sort + duplicate merge + row_ptr)
+            t_csr[k] = timed_flushed(lambda: csr5.spmv_csr(a, x, y, kernel=k))
+        except (MemoryError, RuntimeError):
+            t_csr[k] = None
+    # library comparator: cuSPARSE csrmv through torch sparse CSR (int64
+    # indices, so it moves 16 B per nonzero to our 12)
+    t_lib = None
+    try:
+        A = torch.sparse_csr_tensor(a.row_ptr, a.col_idx.long(), a.val, (m, n))
+        xc = x.unsqueeze(1)
+        t_lib = timed_flushed(lambda: A @ xc)
+        del A, xc
+    except Exception:
+        pass
+    torch.cuda.empty_cache()
+    iteration = {"t_cusparse_csrmv_ms": t_lib, "t_csr_scalar_ms": t_csr["csr-scalar"],
+                 "t_csr_segsum_ms": t_csr["csr-segsum"], "t_csr5_ms": ms, "t_conv_ms": conv_ms,
+                 "baseline": "GPU csr-scalar (one thread per row), spmv.cpp:139-154"}
+    if t_csr["csr-scalar"]:
+        iteration["speedup_n50"] = iteration_speedup(t_csr["csr-scalar"], conv_ms, ms, 50)
+        iteration["speedup_n500"] = iteration_speedup(t_csr["csr-scalar"], conv_ms, ms, 500)
+    # ingest: device COO -> CSR (csr.cpp:35-72) of this matrix's entries in a
+    # random order (sort + duplicate merge + row_ptr); skipped for the 2G-entry
+    # graph, whose COO copies would not fit beside the matrix
+    if not big:
         try:
             g = torch.Generator(device=dev).manual_seed(1)
             perm = torch.randperm(nnz, device=dev, generator=g)
@@ -608,125 +561,324 @@ def run_ours(args, workload_name, workload):
                                    "order": "random permutation", "equals_generator_csr": same}
             del rows, cols, vals, c2
         except (MemoryError, RuntimeError, TypeError) as e:
-            if iteration is not None:
-                iteration["ingest"] = {"error": str(e)[:200]}
-        # gather ceiling: the same nnz x-gathers alone (torch.index_select over
-        # this matrix's col_idx, a library kernel) -- what the x traffic costs
-        # without the matrix stream and the reduction
-        try:
-            idx = a.col_idx.long()
-            xs = x.index_select(0, idx)
-            iteration["gather_only_ms"] = timed_flushed(
-                lambda: torch.index_select(x, 0, idx, out=xs))
-            del idx, xs
-        except (MemoryError, RuntimeError, TypeError):
-            pass
-        run()  # leave y = the CSR5 result for the CPU comparison below
+            iteration["ingest"] = {"error": str(e)[:200]}
+    # gather ceiling: the same nnz x-gathers alone (torch.index_select over this
+    # matrix's col_idx, a library kernel) -- what the x traffic costs without
+    # the matrix stream and the reduction
+    try:
+        idx = a.col_idx.long()
+        xs_ = x.index_select(0, idx)
+        iteration["gather_only_ms"] = timed_flushed(lambda: torch.index_select(x, 0, idx, out=xs_))
+        iteration["gather_only_over_kernel"] = iteration["gather_only_ms"] / tile_ms
+        del idx, xs_
+    except (MemoryError, RuntimeError, TypeError):
+        pass
+    torch.cuda.empty_cache()
+    run()  # leave y = the CSR5 result for the CPU comparison below
+    torch.cuda.synchronize()
+    y_host = y.cpu().numpy()
+    plan = {"lines_per_gather": round(info.lines_per_gather, 2),
+            "warps_per_cta": info.warps_per_cta, "stages": info.stages,
+            "smem_bytes": info.smem_bytes, "x_mode": info.x_mode,
+            "x_l2_window": info.x_window,
+            "kernel_variant": ["general", "VR", "NF"][info.kernel_variant]}
+    bytes_alg = info.spmv_bytes
+    conv_alloc = info.alloc_ms
+    p_tiles, word_bits = info.p, info.word_bits
+    a5.release()
+    del a5, a, x, y, scrub
+    gc.collect()
+    torch.cuda.empty_cache()
+
+    peak, peak_src = peaks()
+    achieved = bytes_alg / (tile_ms * 1e-3) / 1e9
+    flops = 2.0 * nnz
+    res = {
+        "value": flops / (ms * 1e6), "unit": UNIT, "ms_per_step": ms,
+        "config": {"workload": name, "desc": workload["desc"], "m": m, "n": n, "nnz": nnz,
+                   "omega": 32, "sigma": sigma, "p": p_tiles, "desc_word_bits": word_bits,
+                   "mode": "deterministic",
+                   "step": "iterative: SpMV, y -> x" if args.iterative else "SpMV",
+                   "spmv_plan": plan,
+                   "l2": (f"L2 flushed between timed calls ({2 * l2_bytes / 1e6:.0f} MB read "
+                          f"outside the events); working set {bytes_alg / 1e6:.0f} MB per SpMV"),
+                   "x": "mt19937_64(1), 0.5 + (rng()>>11)*2^-53 (bench.cpp:103-105)"},
+        "gbs_effective": bytes_alg / (ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(name),
+                     "kernel": "k_spmv (tile kernel)", "kernel_ms": tile_ms,
+                     "kernel_ms_best": tile_all[0], "kernel_ms_median": tile_all[len(tile_all) // 2],
+                     "algorithmic_bytes": bytes_alg, "peak_source": peak_src,
+                     "frac_of_8TBs_spec": achieved / 8000.0},
+        "conversion": {"ms": conv_ms, "alloc_ms": conv_alloc, "spmv_equiv": conv_ms / ms,
+                       "spmv_equiv_excl_alloc": (conv_ms - conv_alloc) / ms},
+        "iteration": iteration,
+        "e2e": {"value": flops / (e2e_ms * 1e6), "unit": UNIT,
+                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * m,
+                "ms_per_step": e2e_ms,
+                "path": ("csr5.spmv_host_batch (csr5g_spmv_host_batch): per step pinned x H2D + "
+                         "SpMV + y D2H, x_{k+1} H2D and y_k D2H overlapping SpMV k; CUDA events "
+                         "on the caller stream"),
+                "trials_ms_per_step": e2e_trials, "serial_value": flops / (e2e_serial_ms * 1e6),
+                "serial_ms_per_step": e2e_serial_ms, "pcie_duplex_ms_per_step": pcie_ms,
+                "frac_of_pcie_duplex": pcie_ms / e2e_ms},
+        "gpu_launches": args.steps,  # one k_spmv per step (the calibration runs inside it)
+        "clocks": clk,
+        "correctness_max_rel_err": err,
+    }
+    if not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(args, name, workload, x_host, y_host)
+    return res
+
+
+# --------------------------------------------------------------------------
+# our arm, N GPUs (one process per GPU)
+# --------------------------------------------------------------------------
+def measure_sharded(args, name, workload, dev, local, dist, rank, world):
+    import torch
+
+    from paper_1503_05032_b200 import csr5, mg
+    from paper_1503_05032_b200.synthetic import WorkloadMatrix, bench_x, scaled_workload
+    # strong: the same global matrix at every N; weak: `world` times the
+    # 1-GPU one.  Either way each rank generates the global row_ptr and only
+    # its own slice of entries.
+    if args.scaling == "weak":
+        workload = scaled_workload(workload, world)
+    W = WorkloadMatrix(workload, dev)
+    m, n, nnz = W.m, W.n, W.nnz
+    torch.cuda.synchronize()
+    x_host = bench_x(n)
+    x = torch.as_tensor(x_host).to(dev)
+    y = torch.empty(m, dtype=torch.float64, device=dev)
+    sigma = csr5.select_sigma(nnz / m)
+    lo, hi = mg.Csr5Sharded.slices_for(nnz, sigma, rank, world)
+    col_s, val_s = W.entries(lo, hi)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sh = mg.Csr5Sharded(W.row_ptr, col_s, val_s, m, n, nnz, sigma, rank, world,
+                        iterative=args.iterative and m == n)
+    torch.cuda.synchronize()
+    conv_ms = (time.perf_counter() - t0) * 1e3
+    del col_s, val_s
+    a5 = sh.a5
+    info = a5.info if a5 is not None else None
+    run = lambda: sh.spmv(x, y)  # noqa: E731
+
+    # -- correctness guard: this rank's owned rows of y against cuSPARSE ------
+    run()
+    torch.cuda.synchronize()
+    own = sh.own
+    err = 0.0
+    if own[1] > own[0]:
+        rp_own = W.row_ptr[own[0]:own[1] + 1]
+        e0, e1 = int(rp_own[0]), int(rp_own[-1])
+        col_own, val_own = W.entries(e0, e1)
+        A = torch.sparse_csr_tensor(rp_own - e0, col_own.long(), val_own, (own[1] - own[0], n))
+        y_chk = (A @ x.unsqueeze(1)).squeeze(1)
+        err = ((y[own[0]:own[1]] - y_chk).abs() / y_chk.abs().clamp(min=1.0)).max().item()
+        del A, y_chk, rp_own, col_own, val_own
+    W.drop()
+    torch.cuda.empty_cache()
+    if not err <= 1e-12:
+        raise SystemExit(f"correctness guard: max relative error {err} > 1e-12")
+    it_ctr = [0]
+    if sh.iterative:
+        # fused y -> x (p2p.cu): one step from x must leave every active rank
+        # with the same x_1, whose owned rows are the y just checked (bit for bit)
+        sh.x_buffer(0).copy_(x)
+        x1 = sh.spmv_iter(0)
+        it_ctr[0] = 1
         torch.cuda.synchronize()
+        same = bool(torch.equal(x1[own[0]:own[1]], y[own[0]:own[1]])) if sh.active else True
+        h = torch.tensor([int(sh.active), int(same),
+                          int(x1.view(torch.int64).sum().item()) if sh.active else 0],
+                         dtype=torch.int64, device=dev if dist.get_backend() == "nccl" else "cpu")
+        hs = [torch.empty_like(h) for _ in range(world)]
+        dist.all_gather(hs, h)
+        act = [v for v in hs if int(v[0])]
+        if not all(int(v[1]) for v in act) or len({int(v[2]) for v in act}) != 1:
+            raise SystemExit("correctness guard: fused iterative x_1 differs between ranks or from y")
+        if sh.mailbox_errors():
+            raise SystemExit("correctness guard: P2P mailbox protocol errors")
+
+    def max_over_ranks(v: float) -> float:
+        t = torch.tensor([v], dtype=torch.float64,
+                         device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    scrub = torch.empty(2 * l2_bytes // 8 + 1, dtype=torch.float64, device=dev)
+    for _ in range(args.warmup):
+        run()
+    steps_ev = [(csr5.Event(), csr5.Event()) for _ in range(args.steps)]
+    tk = [(csr5.Event(), csr5.Event()) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    if args.iterative:
+        def step():
+            if sh.iterative:  # fused: the SpMV stores y into every rank's next x
+                sh.spmv_iter(it_ctr[0])
+                it_ctr[0] += 1
+            else:
+                run()
+                sh.gather_y_into_x(y, x)
+    else:
+        step = run
+    x_keep = x.clone() if args.iterative else None
+    for k in range(args.steps):
+        scrub.sum()
+        steps_ev[k][0].record()
+        step()
+        steps_ev[k][1].record()
+    if x_keep is not None:
+        x.copy_(x_keep)
+        del x_keep
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        scrub.sum()
+        if a5 is not None:
+            sh.spmv(x, y, events=tk[k])
+        else:
+            run()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = max_over_ranks(sum(b.elapsed_ms(e) for b, e in steps_ev)) / args.steps
+    tile_ms = (sum(b.elapsed_ms(e) for b, e in tk) / args.steps) if a5 is not None else 0.0
+    tile_ms_max = max_over_ranks(tile_ms)
+
+    # -- e2e: the serial form through the sharded driver ----------------------
+    ring = 2
+    xh = [torch.as_tensor(x_host).pin_memory() for _ in range(ring)]
+    yh = [torch.empty(m, dtype=torch.float64).pin_memory() for _ in range(ring)]
+
+    def e2e_serial(k):
+        x.copy_(xh[k % ring], non_blocking=True)
+        run()
+        yh[k % ring][own[0]:own[1]].copy_(y[own[0]:own[1]], non_blocking=True)
+
+    for k in range(min(args.warmup, 2)):
+        e2e_serial(k)
+    e0, e1 = csr5.Event(), csr5.Event()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    for k in range(args.steps):
+        e2e_serial(k)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_ms(e1)) / args.steps
+    del xh, yh
 
     flops = 2.0 * nnz
-    value = flops / (ms * 1e6)
     peak, peak_src = peaks()
     line = None
     if rank == 0:
-        bytes_alg = info.spmv_bytes
-        roof = None
-        if tile_ms:
-            achieved = bytes_alg / (tile_ms * 1e-3) / 1e9
-            traffic = ncu_traffic(workload_name)
-            if iteration and iteration.get("gather_only_ms"):
-                iteration["gather_only_over_kernel"] = iteration["gather_only_ms"] / tile_ms
-            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": traffic,
-                    "kernel": "k_spmv (tile kernel)", "kernel_ms": tile_ms,
-                    "kernel_ms_best": tile_all[0],
-                    "kernel_ms_median": tile_all[len(tile_all) // 2],
-                    "algorithmic_bytes": bytes_alg, "peak_source": peak_src,
-                    "frac_of_8TBs_spec": achieved / 8000.0}
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            try:
-                r = reference_cpu(workload, x_host, budget_s=args.cpu_seconds, also_w32=True)
-                model, ncpu = cpu_info()
-                yr = r.pop("y")
-                w32 = r.pop("w32")
-                cpu = {"value": 2.0 * r["nnz"] / (r["best_ms"] * 1e6), "unit": UNIT,
-                       "cores": r["threads"], "kind": "reference",
-                       "sample": (f"full {workload_name} matrix, reference csr5::spmv_csr5 "
-                                  f"omega={r['omega']} sigma={r['sigma']} deterministic; best of "
-                                  f"{len(r['samples'])} samples x {r['inner']} calls"),
-                       "cpu_model": model, "nproc": ncpu, "conv_ms": r["conv_ms"],
-                       # the reference's own widths (8 B val + 8 B
-                       # col_idx), x and y once; its small metadata excluded
-                       "gbs_ref_widths": (16 * r["nnz"] + 8 * (m + n)) / (r["best_ms"] * 1e6),
-                       "conv_spmv_equiv": r["conv_ms"] / r["best_ms"],
-                       "csr_scalar_gflops": 2.0 * r["nnz"] / (r["csr_scalar_ms"] * 1e6),
-                       "y_max_rel_err_vs_gpu": float(np.max(np.abs(yr - y.cpu().numpy()) /
-                                                            np.maximum(1.0, np.abs(yr)))),
-                       "omega32": {"sigma": w32["sigma"],
-                                   "gflops": 2.0 * r["nnz"] / (w32["best_ms"] * 1e6),
-                                   "conv_ms": w32["conv_ms"],
-                                   "sample": f"best of 3 samples x {w32['inner']} calls"}}
-            except Exception as e:  # the CPU number is reported, never gating
-                cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
-                       "sample": f"failed: {e}"}
-        launches_per_step = 1
-        if world > 1 and sh.active:
+        launches = 1
+        if sh.active:
             if sh.exchange == "p2p":
                 sb, se = sh.senders[sh.rank]
-                launches_per_step += int(se > sb) + int(bool(args.iterative and sh.iterative))
+                launches += int(se > sb) + int(bool(args.iterative and sh.iterative))
             else:
-                launches_per_step += 1
+                launches += 1
+        bytes_alg = info.spmv_bytes
+        achieved = bytes_alg / (tile_ms * 1e-3) / 1e9 if tile_ms else None
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name, "desc": workload["desc"], "m": m, "n": n,
-                       "nnz": nnz, "omega": 32, "sigma": sigma, "p": info.p,
-                       "desc_word_bits": info.word_bits, "mode": "deterministic",
+            "metric": METRIC, "value": flops / (ms * 1e6), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": name, "desc": workload["desc"], "m": m, "n": n, "nnz": nnz,
+                       "omega": 32, "sigma": sigma, "mode": "deterministic",
                        "step": (("iterative: SpMV with y stored into every rank's next x over "
-                                 "NVLink (fused, p2p.cu)" if world > 1 and sh.iterative else
+                                 "NVLink (fused, p2p.cu)" if sh.iterative else
                                  "iterative: SpMV + y->x all-gather") if args.iterative else
-                                "SpMV (+ boundary exchange at N>1)"),
-                       "exchange": (os.environ.get("CSR5G_EXCHANGE", "p2p") if world > 1
-                                    else None),
-                       "spmv_plan": {"lines_per_gather": round(info.lines_per_gather, 2),
-                                     "warps_per_cta": info.warps_per_cta, "stages": info.stages,
-                                     "smem_bytes": info.smem_bytes, "x_mode": info.x_mode,
-                                     "x_l2_window": info.x_window,
-                                     "kernel_variant": ["general", "VR", "NF"][info.kernel_variant]},
+                                "SpMV + boundary exchange"),
+                       "exchange": os.environ.get("CSR5G_EXCHANGE", "p2p"),
                        "parallelism": f"tile-range shards x{world}, x replicated",
-                       "l2": (f"L2 flushed between timed calls ({2 * l2_bytes / 1e6:.0f} MB "
-                              f"read outside the events); working set "
-                              f"{info.spmv_bytes / 1e6:.0f} MB per SpMV"),
+                       "l2": f"L2 flushed between timed calls ({2 * l2_bytes / 1e6:.0f} MB read)",
                        "x": "mt19937_64(1), 0.5 + (rng()>>11)*2^-53 (bench.cpp:103-105)"},
-            "gbs_effective": info.spmv_bytes * world / (ms * 1e-3) / 1e9 if world == 1 else None,
-            "roofline": roof,
-            "conversion": {"ms": conv_ms, "alloc_ms": info.alloc_ms,
-                           "spmv_equiv": conv_ms / ms,
-                           "spmv_equiv_excl_alloc": (conv_ms - info.alloc_ms) / ms},
-            "cpu_baseline": cpu,
-            "iteration": iteration,
+            "roofline": ({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                          "frac": achieved / peak, "traffic": None,
+                          "kernel": "k_spmv (rank 0's shard)", "kernel_ms": tile_ms,
+                          "kernel_ms_max_over_ranks": tile_ms_max,
+                          "algorithmic_bytes": bytes_alg, "peak_source": peak_src}
+                         if achieved else None),
+            "conversion": {"ms": conv_ms, "spmv_equiv": conv_ms / ms},
+            "cpu_baseline": None,
             "e2e": {"value": flops / (e2e_ms * 1e6), "unit": UNIT,
-                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * m,
-                    "ms_per_step": e2e_ms, "path": e2e_path,
-                    "trials_ms_per_step": e2e_trials,  # N=1: median of three K-step runs
-                    "serial_value": flops / (e2e_serial_ms * 1e6),
-                    "pcie_duplex_ms_per_step": pcie_ms if world == 1 else None,
-                    "frac_of_pcie_duplex": (pcie_ms / e2e_ms) if world == 1 else None,
-                    "serial_ms_per_step": e2e_serial_ms},
-            # our kernels per step: the SpMV (calibration inside it); at N>1 plus
-            # the P2P fix-up on an owner with senders and, fused iterative, the
-            # ready signal (collective exchange: plus k_fixup)
-            "gpu_launches": args.steps * launches_per_step,
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * (own[1] - own[0]),
+                    "ms_per_step": e2e_ms,
+                    "path": "serial per rank: pinned x H2D + sharded SpMV + owned y D2H"},
+            "gpu_launches": args.steps * launches,
             "clocks": clk,
             "correctness_max_rel_err": err,
         }
+    sh.close()
+    return line
+
+
+def run_ours(args, workload_name, workload):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        # a rank that never sees a peer's flag would block its stream forever:
+        # turn such a hang into a loud failure (the whole run takes minutes)
+        limit = float(os.environ.get("CSR5G_WATCHDOG_S", "600"))
+
+        def _watchdog():
+            time.sleep(limit)
+            sys.stderr.write(f"bench.py rank {rank}: no completion after {limit:.0f} s "
+                             "(multi-GPU exchange stalled?); aborting\n")
+            sys.stderr.flush()
+            os._exit(3)
+
+        threading.Thread(target=_watchdog, daemon=True).start()
+    if os.environ.get("CSR5G_SHARE_GPU") == "1":  # functional multi-rank check on one GPU
+        local %= torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world == 1:
+        from paper_1503_05032_b200.synthetic import WORKLOADS
+        res = measure_one(args, workload_name, workload, dev, local)
+        line = {"metric": METRIC, "value": res.pop("value"), "unit": UNIT, "n_gpus": 1,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": res.pop("ms_per_step"),
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic"}
+        line.update(res)
+        line["config"]["parallelism"] = "1 GPU (tile-range shards x1)"
+        subs = {}
+        for w in args.sub:
+            if w == workload_name:
+                continue
+            r = measure_one(args, w, WORKLOADS[w], dev, local)
+            r.pop("gpu_launches", None)
+            subs[w] = r
+        if subs:
+            line["sub_results"] = subs
         print(json.dumps(line), flush=True)
-    a5 = None
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
+        return line
+    import torch.distributed as dist
+    # NCCL over NVLink; CSR5G_DIST_BACKEND=gloo lets several ranks share one
+    # GPU for a functional check of the sharded flow (not a timing)
+    backend = os.environ.get("CSR5G_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+    line = measure_sharded(args, workload_name, workload, dev, local, dist, rank, world)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
     return line
 
 
@@ -737,18 +889,26 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="st27_200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
+    ap.add_argument("--sub", default=",".join(SUB_WORKLOADS),
+                    help="N=1: comma-separated workloads measured as sub_results ('none': skip)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--iterative", action="store_true",
                     help="y -> x mode (square A): each step is SpMV plus the all-gather of y "
                          "into every rank's x (N=1: x and y swap roles every step)")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="N>1: weak = the global matrix is N times the 1-GPU workload (stencils "
-                         "N times deeper, graphs log2 N scales larger); strong = the same matrix")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                    help="N>1: strong = the same global matrix at every N (default); weak = the "
+                         "global matrix is N times the 1-GPU workload (stencils N times deeper, "
+                         "graphs log2 N scales larger)")
     args = ap.parse_args()
+    args.sub = [] if args.sub in ("", "none") else [w for w in args.sub.split(",") if w]
+    for w in args.sub:
+        if w not in WORKLOADS:
+            ap.error(f"--sub: unknown workload {w!r}")
     if args.warmup < 3:
         args.warmup = 3
+    pin_openmp()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, args.workload, wl)

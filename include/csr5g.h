@@ -238,6 +238,9 @@ CSR5G_API int csr5g_csr_spmv(int device, int32_t kernel, int64_t m, int64_t n, i
 typedef struct csr5g_coo_s *csr5g_coo;
 CSR5G_API int csr5g_mm_read(const char *path, csr5g_coo *out, int64_t *m, int64_t *n,
                             int64_t *count);
+/* The same parser over an in-memory text (read_matrix_market(std::istream&)). */
+CSR5G_API int csr5g_mm_parse(const char *text, int64_t len, csr5g_coo *out, int64_t *m,
+                             int64_t *n, int64_t *count);
 CSR5G_API int csr5g_coo_get(csr5g_coo c, int64_t *h_rows, int64_t *h_cols, double *h_vals);
 CSR5G_API int csr5g_coo_release(csr5g_coo c);
 
@@ -260,6 +263,17 @@ CSR5G_API int csr5g_coo_to_csr_host(int device, int64_t m, int64_t n, int64_t co
                                     const int64_t *h_rows, const int64_t *h_cols,
                                     const double *h_vals, int64_t *h_row_ptr,
                                     int64_t *h_col_idx, double *h_val, int64_t *nnz);
+
+/* Host-staged csr-scalar / csr-segsum (spmv.hpp spmv_csr_scalar /
+ * spmv_csr_segsum and csr.hpp dense_spmv_oracle take host vectors): int64
+ * col_idx as in the reference; device < 0 = the current device. */
+CSR5G_API int csr5g_csr_spmv_host(int device, int32_t kernel, int64_t m, int64_t n, int64_t nnz,
+                                  const int64_t *h_row_ptr, const int64_t *h_col_idx,
+                                  const double *h_val, const double *h_x, double *h_y);
+
+/* Csr5Matrix::row_ptr (format.hpp:168): the handle's copy of the CSR row
+ * pointer, m+1 entries, into host memory (csr5_to_csr(a5) needs nothing else). */
+CSR5G_API int csr5g_export_row_ptr(csr5g_matrix h, int64_t *h_row_ptr);
 
 /* Implicit destruction of Csr5Matrix (value type) -> explicit release. */
 CSR5G_API int csr5g_release(csr5g_matrix h);
@@ -290,6 +304,10 @@ CSR5G_API int csr5g_stencil_box_fill(int32_t kind, int64_t a, int64_t layers, in
                                      int64_t pos_end, int64_t *d_row_ptr, int32_t *d_col_idx,
                                      double *d_val, void *stream);
 
+/* The benchmark harness's x (bench.cpp:103-105): std::mt19937_64(seed),
+ * x_i = 0.5 + (rng() >> 11) * 2^-53, written into the host array h_x[n]. */
+CSR5G_API int csr5g_bench_x(int64_t n, uint64_t seed, double *h_x);
+
 /* Irregular synthetic matrices on the device (BASELINE configs 3-5).  Two
  * phases: *_create generates and sizes the matrix (m, nnz) and keeps it in a
  * generator object; csr5g_gen_fill writes the CSR into caller buffers
@@ -307,6 +325,12 @@ CSR5G_API int csr5g_mixed_create(int32_t log2_m, double p_empty, int32_t n_long,
                                  csr5g_gen *out, int64_t *m, int64_t *nnz);
 CSR5G_API int csr5g_gen_fill(csr5g_gen g, int64_t *d_row_ptr, int32_t *d_col_idx, double *d_val,
                              void *stream);
+/* Only the entries at global positions [pos_begin, pos_end), written at
+ * position - pos_begin (a multi-GPU rank's slice), and the full row_ptr when
+ * d_row_ptr is not NULL. */
+CSR5G_API int csr5g_gen_fill_range(csr5g_gen g, int64_t pos_begin, int64_t pos_end,
+                                   int64_t *d_row_ptr, int32_t *d_col_idx, double *d_val,
+                                   void *stream);
 CSR5G_API int csr5g_gen_release(csr5g_gen g);
 
 #ifdef __cplusplus

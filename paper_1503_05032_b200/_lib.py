@@ -94,7 +94,11 @@ SIGNATURES = {
     "csr5g_to_csr_host": (C.c_int, [_vp, _vp, _vp]),
     "csr5g_mm_read": (C.c_int, [C.c_char_p, C.POINTER(_vp), C.POINTER(_i64), C.POINTER(_i64),
                                 C.POINTER(_i64)]),
+    "csr5g_mm_parse": (C.c_int, [C.c_char_p, _i64, C.POINTER(_vp), C.POINTER(_i64),
+                                 C.POINTER(_i64), C.POINTER(_i64)]),
     "csr5g_coo_get": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "csr5g_csr_spmv_host": (C.c_int, [C.c_int, _i32, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "csr5g_export_row_ptr": (C.c_int, [_vp, _vp]),
     "csr5g_coo_release": (C.c_int, [_vp]),
     "csr5g_coo_to_csr": (C.c_int, [C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                    C.POINTER(_i64), _vp]),
@@ -115,6 +119,8 @@ SIGNATURES = {
     "csr5g_mixed_create": (C.c_int, [_i32, C.c_double, _i32, _i64, _i32, _i32, C.c_uint64, _vp,
                                      C.POINTER(_vp), C.POINTER(_i64), C.POINTER(_i64)]),
     "csr5g_gen_fill": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "csr5g_bench_x": (C.c_int, [_i64, C.c_uint64, _vp]),
+    "csr5g_gen_fill_range": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "csr5g_gen_release": (C.c_int, [_vp]),
 }
 

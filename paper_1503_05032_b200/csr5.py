@@ -392,39 +392,85 @@ def stencil_box(kind: int, a: int, layers: int, pos_begin: int = 0, pos_end: int
     return m, nnz, rp, ci, va
 
 
-def _from_generator(gen: C.c_void_p, m: int, nnz: int, device, stream) -> CsrMatrix:
-    try:
-        rp = torch.empty(m + 1, dtype=torch.int64, device=device)
-        ci = torch.empty(nnz, dtype=torch.int32, device=device)
-        va = torch.empty(nnz, dtype=torch.float64, device=device)
-        check(lib().csr5g_gen_fill(gen, rp.data_ptr(), ci.data_ptr(), va.data_ptr(),
-                                   _stream_ptr(stream)))
-        torch.cuda.synchronize(device)
-    finally:
-        lib().csr5g_gen_release(gen)
-    return CsrMatrix(m, m, rp, ci, va)
+class Generator:
+    """A sized synthetic matrix on the device (csr5g_rmat_create /
+    csr5g_mixed_create): the full row_ptr and any slice of the entries."""
+
+    def __init__(self, gen: C.c_void_p, m: int, nnz: int, device):
+        self._g, self.m, self.n, self.nnz, self.device = gen, m, m, nnz, torch.device(device)
+
+    def fill(self, pos_begin: int = 0, pos_end: int | None = None, with_row_ptr: bool = True,
+             stream=None):
+        """(row_ptr or None, col_idx[pos_begin:pos_end], val[pos_begin:pos_end])."""
+        hi = self.nnz if pos_end is None else pos_end
+        with torch.cuda.device(self.device):
+            rp = (torch.empty(self.m + 1, dtype=torch.int64, device=self.device)
+                  if with_row_ptr else None)
+            ci = torch.empty(max(hi - pos_begin, 0), dtype=torch.int32, device=self.device)
+            va = torch.empty(max(hi - pos_begin, 0), dtype=torch.float64, device=self.device)
+            check(lib().csr5g_gen_fill_range(self._g, pos_begin, hi,
+                                             rp.data_ptr() if rp is not None else None,
+                                             ci.data_ptr(), va.data_ptr(), _stream_ptr(stream)))
+            torch.cuda.synchronize(self.device)
+        return rp, ci, va
+
+    def matrix(self, stream=None) -> CsrMatrix:
+        rp, ci, va = self.fill(stream=stream)
+        return CsrMatrix(self.m, self.n, rp, ci, va)
+
+    def release(self) -> None:
+        if self._g:
+            lib().csr5g_gen_release(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
 
 
-def rmat(scale: int, edge_factor: int = 16, seed: int = 1, permute: bool = True,
-         device="cuda", stream=None) -> CsrMatrix:
+def rmat_generator(scale: int, edge_factor: int = 16, seed: int = 1, permute: bool = True,
+                   device="cuda", stream=None) -> Generator:
     """Graph500 R-MAT (a,b,c,d = .57,.19,.19,.05), duplicates removed."""
     g, m, nnz = C.c_void_p(), C.c_int64(), C.c_int64()
     with torch.cuda.device(torch.device(device)):
         check(lib().csr5g_rmat_create(scale, edge_factor, seed, int(permute), _stream_ptr(stream),
                                       C.byref(g), C.byref(m), C.byref(nnz)))
-        return _from_generator(g, m.value, nnz.value, device, stream)
+    return Generator(g, m.value, nnz.value, device)
 
 
-def mixed(log2_m: int = 23, p_empty: float = 0.4, n_long: int = 4, long_len: int = 1 << 20,
-          min_len: int = 1, max_len: int = 32, seed: int = 1, device="cuda",
-          stream=None) -> CsrMatrix:
+def mixed_generator(log2_m: int = 23, p_empty: float = 0.4, n_long: int = 4,
+                    long_len: int = 1 << 20, min_len: int = 1, max_len: int = 32, seed: int = 1,
+                    device="cuda", stream=None) -> Generator:
     """40% empty rows plus a few 1M-nnz rows."""
     g, m, nnz = C.c_void_p(), C.c_int64(), C.c_int64()
     with torch.cuda.device(torch.device(device)):
         check(lib().csr5g_mixed_create(log2_m, p_empty, n_long, long_len, min_len, max_len, seed,
                                        _stream_ptr(stream), C.byref(g), C.byref(m),
                                        C.byref(nnz)))
-        return _from_generator(g, m.value, nnz.value, device, stream)
+    return Generator(g, m.value, nnz.value, device)
+
+
+def rmat(scale: int, edge_factor: int = 16, seed: int = 1, permute: bool = True,
+         device="cuda", stream=None) -> CsrMatrix:
+    """Graph500 R-MAT (a,b,c,d = .57,.19,.19,.05), duplicates removed."""
+    g = rmat_generator(scale, edge_factor, seed, permute, device, stream)
+    try:
+        return g.matrix(stream)
+    finally:
+        g.release()
+
+
+def mixed(log2_m: int = 23, p_empty: float = 0.4, n_long: int = 4, long_len: int = 1 << 20,
+          min_len: int = 1, max_len: int = 32, seed: int = 1, device="cuda",
+          stream=None) -> CsrMatrix:
+    """40% empty rows plus a few 1M-nnz rows."""
+    g = mixed_generator(log2_m, p_empty, n_long, long_len, min_len, max_len, seed, device, stream)
+    try:
+        return g.matrix(stream)
+    finally:
+        g.release()
 
 
 class Event:

@@ -33,6 +33,18 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 using namespace csr5g;
 
+namespace {
+// device < 0: the calling thread's current CUDA device (the reference's API
+// has no device argument)
+int resolve_device(int* device) {
+  int ndev = 0;
+  CSR5G_CUDA(cudaGetDeviceCount(&ndev));
+  if (*device < 0) CSR5G_CUDA(cudaGetDevice(device));
+  if (*device >= ndev) return fail(CSR5G_ECUDA, "csr5g: no such CUDA device");
+  return CSR5G_OK;
+}
+}  // namespace
+
 struct csr5g_matrix_s {
   Handle* h;
 };
@@ -203,9 +215,7 @@ int csr5g_build_host(int device, int64_t m, int64_t n, int64_t nnz, const int64_
   if (m > 0 && !h_row_ptr) return fail(CSR5G_EINVAL, "csr5g: row_ptr is NULL");
   if (m > 0 && h_row_ptr[m] != nnz)
     return fail(CSR5G_EINVAL, "csr: col_idx/val size does not match row_ptr[m]");
-  int ndev = 0;
-  CSR5G_CUDA(cudaGetDeviceCount(&ndev));
-  if (device < 0 || device >= ndev) return fail(CSR5G_ECUDA, "csr5g: no such CUDA device");
+  if (int rc = resolve_device(&device)) return rc;
   CSR5G_CUDA(cudaSetDevice(device));
   std::vector<int32_t> c32((size_t)nnz);
   for (int64_t i = 0; i < nnz; ++i) c32[(size_t)i] = (int32_t)h_col_idx[i];
@@ -280,6 +290,65 @@ int csr5g_csr_spmv(int device, int32_t kernel, int64_t m, int64_t n, int64_t nnz
     return fail(CSR5G_ERANGE, "csr5g: m >= 2^31 rows is unsupported");
   return csr_spmv(device, kernel, m, n, nnz, d_row_ptr, d_col_idx, d_val, d_x, d_y,
                   static_cast<cudaStream_t>(stream));
+}
+
+int csr5g_csr_spmv_host(int device, int32_t kernel, int64_t m, int64_t n, int64_t nnz,
+                        const int64_t* h_row_ptr, const int64_t* h_col_idx, const double* h_val,
+                        const double* h_x, double* h_y) {
+  if (m < 0 || n < 0 || nnz < 0) return fail(CSR5G_EINVAL, "csr: negative dimension");
+  if (m > 0 && (!h_row_ptr || !h_y)) return fail(CSR5G_EINVAL, "spmv: row_ptr or y is NULL");
+  if (nnz > 0 && (!h_col_idx || !h_val || !h_x))
+    return fail(CSR5G_EINVAL, "spmv: col_idx, val or x is NULL");
+  if (m > 0 && h_row_ptr[m] != nnz)
+    return fail(CSR5G_EINVAL, "csr: col_idx/val size does not match row_ptr[m]");
+  if (n >= (int64_t(1) << 31))
+    return fail(CSR5G_ERANGE, "csr5g: n >= 2^31 columns does not fit the int32 col_idx");
+  if (int rc = resolve_device(&device)) return rc;
+  CSR5G_CUDA(cudaSetDevice(device));
+  std::vector<int32_t> c32((size_t)nnz);
+  for (int64_t i = 0; i < nnz; ++i) c32[(size_t)i] = (int32_t)h_col_idx[i];
+  int64_t* d_rp = nullptr;
+  int32_t* d_ci = nullptr;
+  double *d_va = nullptr, *d_x = nullptr, *d_y = nullptr;
+  auto done = [&](int rc) {
+    for (void* q : {(void*)d_rp, (void*)d_ci, (void*)d_va, (void*)d_x, (void*)d_y}) cudaFree(q);
+    return rc;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&d_rp, sizeof(int64_t) * (m + 1))) != cudaSuccess ||
+      (e = cudaMalloc(&d_ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1))) != cudaSuccess ||
+      (e = cudaMalloc(&d_va, sizeof(double) * std::max<int64_t>(nnz, 1))) != cudaSuccess ||
+      (e = cudaMalloc(&d_x, sizeof(double) * std::max<int64_t>(n, 1))) != cudaSuccess ||
+      (e = cudaMalloc(&d_y, sizeof(double) * std::max<int64_t>(m, 1))) != cudaSuccess)
+    return done(cuda_fail(e, "cudaMalloc(csr staging)"));
+  if ((m > 0 && (e = cudaMemcpy(d_rp, h_row_ptr, sizeof(int64_t) * (m + 1),
+                                cudaMemcpyHostToDevice)) != cudaSuccess) ||
+      (nnz > 0 && ((e = cudaMemcpy(d_ci, c32.data(), sizeof(int32_t) * nnz,
+                                   cudaMemcpyHostToDevice)) != cudaSuccess ||
+                   (e = cudaMemcpy(d_va, h_val, sizeof(double) * nnz, cudaMemcpyHostToDevice)) !=
+                       cudaSuccess)) ||
+      (n > 0 && (e = cudaMemcpy(d_x, h_x, sizeof(double) * n, cudaMemcpyHostToDevice)) !=
+                    cudaSuccess))
+    return done(cuda_fail(e, "cudaMemcpy(csr staging)"));
+  int rc = csr5g_csr_spmv(device, kernel, m, n, nnz, d_rp, d_ci, d_va, d_x, d_y, nullptr);
+  if (rc) return done(rc);
+  if (m > 0 && (e = cudaMemcpy(h_y, d_y, sizeof(double) * m, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return done(cuda_fail(e, "cudaMemcpy(y)"));
+  return done(CSR5G_OK);
+}
+
+int csr5g_export_row_ptr(csr5g_matrix hm, int64_t* h_row_ptr) {
+  if (!hm || !h_row_ptr) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  Handle* h = hm->h;
+  CSR5G_CUDA(cudaSetDevice(h->device));
+  CSR5G_CUDA(cudaDeviceSynchronize());
+  if (h->info.m == 0) {
+    h_row_ptr[0] = 0;
+    return CSR5G_OK;
+  }
+  CSR5G_CUDA(cudaMemcpy(h_row_ptr, h->row_ptr, sizeof(int64_t) * (h->info.m + 1),
+                        cudaMemcpyDeviceToHost));
+  return CSR5G_OK;
 }
 
 int csr5g_to_csr_host(csr5g_matrix h, int64_t* h_col_idx, double* h_val) {

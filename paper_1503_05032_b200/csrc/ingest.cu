@@ -196,6 +196,29 @@ int csr5g_mm_read(const char* path, csr5g_coo* out, int64_t* m, int64_t* n, int6
   return CSR5G_OK;
 }
 
+int csr5g_mm_parse(const char* text, int64_t len, csr5g_coo* out, int64_t* m, int64_t* n,
+                   int64_t* count) {
+  if ((!text && len > 0) || len < 0 || !out || !m || !n || !count)
+    return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  *out = nullptr;
+  std::istringstream in(std::string(text ? text : "", (size_t)len));
+  auto* c = new csr5g_coo_s;
+  try {
+    parse_mm(in, *c);
+  } catch (const MmError& e) {
+    delete c;
+    return fail(CSR5G_ERUNTIME, e.msg);
+  } catch (const std::bad_alloc&) {
+    delete c;
+    return fail(CSR5G_ENOMEM, "matrix market: out of host memory");
+  }
+  *out = c;
+  *m = c->m;
+  *n = c->n;
+  *count = (int64_t)c->rows.size();
+  return CSR5G_OK;
+}
+
 int csr5g_coo_get(csr5g_coo c, int64_t* h_rows, int64_t* h_cols, double* h_vals) {
   if (!c) return fail(CSR5G_EINVAL, "csr5g: NULL COO");
   if (h_rows) std::copy(c->rows.begin(), c->rows.end(), h_rows);

@@ -710,6 +710,9 @@ int spmv_plan(Handle* h, int sms) {
   // the launch and slowed the next unrelated SpMV by 13% (st27 0.504 vs 0.446
   // ms).  CSR5G_XWINDOW=1 turns it on for experiments.
   h->x_window = false;
+  // experiment overrides, read when the plan is made
+  if (const char* e = std::getenv("CSR5G_XMODE")) h->x_mode = std::atoi(e);
+  if (const char* e = std::getenv("CSR5G_XWINDOW")) h->x_window = std::atoi(e) != 0;
   // stages: the tile being reduced + the next tile (its gathers go out as
   // soon as the current depth loop ends) + TMA lead; 2 minimum
   const int min_stages = 2;
@@ -871,17 +874,8 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.mir = h->mir;
   const int grid = std::max(h->tile_blocks, h->rows_blocks);
   const int threads = 32 * h->warps_per_block;
-  // the plan's gather path; CSR5G_XMODE / CSR5G_XWINDOW override it (experiments)
-  static const int x_mode_env = [] {
-    const char* e = std::getenv("CSR5G_XMODE");
-    return e ? std::atoi(e) : -1;
-  }();
-  static const int x_window_env = [] {
-    const char* e = std::getenv("CSR5G_XWINDOW");
-    return e ? std::atoi(e) : -1;
-  }();
-  const int x_mode = x_mode_env >= 0 ? x_mode_env : h->x_mode;
-  const bool x_window = x_window_env >= 0 ? x_window_env != 0 : h->x_window;
+  const int x_mode = h->x_mode;
+  const bool x_window = h->x_window;
   a.x_mode = x_mode;
   a.early_gather = h->lines_per_gather >= 8.0 ? 1 : 0;
   static const float x_frac_env = [] {

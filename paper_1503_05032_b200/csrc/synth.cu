@@ -4,6 +4,8 @@
 // (csr.cpp:9-33).  Diagonal 4 / 26, off-diagonal -1.
 #include <cub/cub.cuh>
 
+#include <random>
+
 #include "internal.cuh"
 
 namespace csr5g {
@@ -130,6 +132,16 @@ int csr5g_stencil_fill(int32_t kind, int64_t a, int64_t* d_row_ptr, int32_t* d_c
   int rc = csr5g_stencil_box_size(kind, a, a, &m, &nnz);
   if (rc) return rc;
   return csr5g_stencil_box_fill(kind, a, a, 0, nnz, d_row_ptr, d_col_idx, d_val, stream_v);
+}
+
+// The benchmark's x (bench.cpp:103-105): std::mt19937_64(seed), x_i = 0.5 +
+// (rng() >> 11) * 2^-53, on the host (the engine is sequential; 134M values
+// for R-MAT s27 take ~1 s here against ~30 s vectorised in numpy).
+int csr5g_bench_x(int64_t n, uint64_t seed, double* h_x) {
+  if (n < 0 || (n > 0 && !h_x)) return fail(CSR5G_EINVAL, "csr5g: bad bench_x arguments");
+  std::mt19937_64 rng(seed);
+  for (int64_t i = 0; i < n; ++i) h_x[i] = 0.5 + (double)(rng() >> 11) * 0x1.0p-53;
+  return CSR5G_OK;
 }
 
 }  // extern "C"

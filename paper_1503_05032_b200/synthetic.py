@@ -55,10 +55,22 @@ def mt19937_64(seed: int, count: int) -> np.ndarray:
     return out[:count]
 
 
-def bench_x(n: int, seed: int = 1) -> np.ndarray:
-    """x as run_benchmark generates it (bench.cpp:103-105)."""
+def bench_x_numpy(n: int, seed: int = 1) -> np.ndarray:
+    """x as run_benchmark generates it (bench.cpp:103-105), restated in numpy
+    (the cross-check of the native generator)."""
     r = mt19937_64(seed, n)
     return 0.5 + (r >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def bench_x(n: int, seed: int = 1) -> np.ndarray:
+    """x as run_benchmark generates it (bench.cpp:103-105): std::mt19937_64 in
+    libcsr5g (csr5g_bench_x, host code; no GPU needed)."""
+    import ctypes
+
+    from ._lib import check, lib
+    x = np.empty(n, dtype=np.float64)
+    check(lib().csr5g_bench_x(n, seed, x.ctypes.data_as(ctypes.c_void_p)))
+    return x
 
 
 WORKLOADS = {
@@ -111,34 +123,50 @@ def scaled_workload(wl: dict, world: int) -> dict:
 class WorkloadMatrix:
     """A workload's global CSR for a multi-GPU rank: the full row_ptr on the
     device and `entries(lo, hi)` giving (col_idx, val) at global positions
-    [lo, hi).  Stencils generate only what is asked for; graphs are generated
-    whole (their dedup is global) and sliced."""
+    [lo, hi).  Every generator produces just the asked-for slice (graphs
+    regenerate the row blocks that hold it, synth_graph.cu), so no rank ever
+    holds the whole matrix."""
 
     def __init__(self, wl: dict, device="cuda"):
         from . import csr5
         self.wl, self.device = wl, device
+        self.gen = None
         if wl["gen"] == "stencil":
             self.layers = wl.get("layers", wl["a"])
             self.m, self.nnz = csr5.stencil_box_size(wl["kind"], wl["a"], self.layers)
             _, _, self.row_ptr, _, _ = csr5.stencil_box(wl["kind"], wl["a"], self.layers, 0, 0,
                                                         device=device)
-            self.full = None
         else:
-            self.full = _make_matrix(wl, device)
-            self.m, self.nnz, self.row_ptr = self.full.m, self.full.nnz, self.full.row_ptr
+            self.gen = _generator(wl, device)
+            self.m, self.nnz = self.gen.m, self.gen.nnz
+            self.row_ptr = self.gen.fill(0, 0)[0]
         self.n = self.m
 
     def entries(self, lo: int, hi: int):
         from . import csr5
-        if self.full is not None:
-            return self.full.col_idx[lo:hi], self.full.val[lo:hi]
+        if self.gen is not None:
+            _, ci, va = self.gen.fill(lo, hi, with_row_ptr=False)
+            return ci, va
         _, _, _, ci, va = csr5.stencil_box(self.wl["kind"], self.wl["a"], self.layers, lo, hi,
                                            device=self.device)
         return ci, va
 
     def drop(self):
-        """Release the whole-matrix arrays of a generated graph."""
-        self.full = None
+        """Release the generator state (its device row_ptr copy)."""
+        if self.gen is not None:
+            self.gen.release()
+            self.gen = None
+
+
+def _generator(wl: dict, device="cuda"):
+    from . import csr5
+    if wl["gen"] == "rmat":
+        return csr5.rmat_generator(wl["scale"], wl["edge_factor"], wl["seed"], wl["permute"],
+                                   device=device)
+    if wl["gen"] == "mixed":
+        return csr5.mixed_generator(wl["log2_m"], wl["p_empty"], wl["n_long"], wl["long_len"],
+                                    wl["min_len"], wl["max_len"], wl["seed"], device=device)
+    raise ValueError(f"unknown generator {wl['gen']!r}")
 
 
 def _make_matrix(wl: dict, device="cuda"):

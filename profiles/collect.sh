@@ -10,7 +10,7 @@ set -u
 tag=${1:-r01}
 mkdir -p gpurun_out
 for w in ${WORKLOADS:-st27_200 rmat24}; do
-  cmd="python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline"
+  cmd="python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --sub none"
   if $cmd > gpurun_out/${tag}_${w}_plain.log 2>&1; then
     ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
         --log-file gpurun_out/${tag}_${w}_launches.csv $cmd > gpurun_out/${tag}_${w}_ncu_list.log 2>&1

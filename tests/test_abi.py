@@ -91,3 +91,16 @@ def test_stencil_box_sizes_and_weak_scaling():
     assert scaled_workload(WORKLOADS["mixed23"], 4)["log2_m"] == 25
     with pytest.raises(ValueError, match="power-of-two"):
         scaled_workload(WORKLOADS["rmat24"], 3)
+
+
+def test_bench_x_matches_the_reference_engine(orc):
+    """bench.cpp:103-105 x: the native generator (csr5g_bench_x, host code),
+    the numpy restatement and the oracle's mt19937_64 agree bit for bit."""
+    import numpy as np
+
+    from paper_1503_05032_b200.synthetic import bench_x, bench_x_numpy, mt19937_64
+    assert int(mt19937_64(5489, 10000)[-1]) == 9981545732273789042  # std KAT
+    for n in (0, 1, 311, 312, 313, 5000):
+        a, b = bench_x(n), bench_x_numpy(n)
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    assert np.array_equal(bench_x(4000, seed=1), orc.rng(1).random_x(4000))
