@@ -10,7 +10,10 @@ SRCS     := $(wildcard $(PKG)/csrc/*.cu)
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 HDRS     := $(wildcard $(PKG)/csrc/*.cuh) include/csr5g.h
 
-.PHONY: all lib oracle shim probe clean
+# the SpMV kernel variants are separate units (spmv_inst_*.cu): build them in parallel
+MAKEFLAGS += -j$(shell nproc 2>/dev/null || echo 8)
+
+.PHONY: all lib oracle cpp probe clean
 all: lib oracle
 
 lib: $(PKG)/libcsr5g.so
@@ -20,18 +23,15 @@ build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -DCSR5G_BUILD -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; false)
 
 $(PKG)/libcsr5g.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC $(OBJS) -o $@
+	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -Xlinker -soname=libcsr5g.so $(OBJS) -o $@
 
 oracle:
 	$(MAKE) -C oracle
 
-# C++ drop-in shim test (include/csr5g.hpp); needs a GPU to run
-CXX_SYS  := $(if $(wildcard /usr/bin/g++),/usr/bin/g++,g++)
-shim: build/shim_test
-build/shim_test: tests/cpp/shim_test.cpp include/csr5g.hpp include/csr5g.h $(PKG)/libcsr5g.so
-	@mkdir -p build
-	$(CXX_SYS) -std=c++20 -O2 -Wall -pthread -Iinclude $< -L$(PKG) -lcsr5g \
-	  -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
+# C++ drop-in (include/csr5/*.hpp) through the CMake package (cmake/); the
+# programs need a GPU to run (tests/test_gpu_cpp.py)
+cpp: $(PKG)/libcsr5g.so
+	cmake -S tests/cpp -B build/cpp -Dcsr5_DIR=$(CURDIR)/cmake && cmake --build build/cpp
 
 # measurement tool (random-gather ceiling), not part of the product
 probe: build/gather_probe

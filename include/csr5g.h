@@ -197,7 +197,8 @@ CSR5G_API int csr5g_to_csr(csr5g_matrix h, int32_t *d_col_idx, double *d_val, vo
  * stage through the device and synchronise -- not the timed path).
  * csr_to_csr5 from a host CSR with the reference's int64 col_idx
  * (format.hpp:182); spmv_csr5 with host x / y (spmv.hpp:58-61);
- * csr5_to_csr into host buffers (format.hpp:186). */
+ * csr5_to_csr into host buffers (format.hpp:186).  device < 0 = the calling
+ * thread's current CUDA device (the reference's API has no device argument). */
 CSR5G_API int csr5g_build_host(int device, int64_t m, int64_t n, int64_t nnz,
                                const int64_t *h_row_ptr, const int64_t *h_col_idx,
                                const double *h_val, const csr5g_params *params,
@@ -258,7 +259,7 @@ CSR5G_API int csr5g_coo_to_csr(int device, int64_t m, int64_t n, int64_t count,
 
 /* Host-staged form of csr5g_coo_to_csr (the reference's host coo_to_csr
  * signature, csr.hpp): host COO in, host CSR out with int64 col_idx; the
- * output buffers hold m+1 / count entries. */
+ * output buffers hold m+1 / count entries; device < 0 = the current device. */
 CSR5G_API int csr5g_coo_to_csr_host(int device, int64_t m, int64_t n, int64_t count,
                                     const int64_t *h_rows, const int64_t *h_cols,
                                     const double *h_vals, int64_t *h_row_ptr,
@@ -274,6 +275,16 @@ CSR5G_API int csr5g_csr_spmv_host(int device, int32_t kernel, int64_t m, int64_t
 /* Csr5Matrix::row_ptr (format.hpp:168): the handle's copy of the CSR row
  * pointer, m+1 entries, into host memory (csr5_to_csr(a5) needs nothing else). */
 CSR5G_API int csr5g_export_row_ptr(csr5g_matrix h, int64_t *h_row_ptr);
+
+/* spmv.cpp:211-222 spmv_csr5_tile (the TileContribution test hook): the
+ * contributions of complete tile `tid` (a global tile id inside the handle's
+ * range) for host x, computed by the SpMV tile kernel itself (its trace
+ * instantiation), in the reference's emission order: per column the segments
+ * sealed inside it (accumulate = head 0 only), then each head-bearing
+ * column's bottom piece (accumulate).  Up to `cap` entries; *count = number
+ * written (= the tile's heads). */
+CSR5G_API int csr5g_spmv_tile(csr5g_matrix h, int64_t tid, const double *h_x, int64_t *h_rows,
+                              double *h_vals, uint8_t *h_acc, int64_t cap, int64_t *count);
 
 /* Implicit destruction of Csr5Matrix (value type) -> explicit release. */
 CSR5G_API int csr5g_release(csr5g_matrix h);

@@ -99,6 +99,7 @@ SIGNATURES = {
     "csr5g_coo_get": (C.c_int, [_vp, _vp, _vp, _vp]),
     "csr5g_csr_spmv_host": (C.c_int, [C.c_int, _i32, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "csr5g_export_row_ptr": (C.c_int, [_vp, _vp]),
+    "csr5g_spmv_tile": (C.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _i64, C.POINTER(_i64)]),
     "csr5g_coo_release": (C.c_int, [_vp]),
     "csr5g_coo_to_csr": (C.c_int, [C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                    C.POINTER(_i64), _vp]),

@@ -33,7 +33,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 using namespace csr5g;
 
-namespace {
+namespace csr5g {
 // device < 0: the calling thread's current CUDA device (the reference's API
 // has no device argument)
 int resolve_device(int* device) {
@@ -43,7 +43,7 @@ int resolve_device(int* device) {
   if (*device >= ndev) return fail(CSR5G_ECUDA, "csr5g: no such CUDA device");
   return CSR5G_OK;
 }
-}  // namespace
+}  // namespace csr5g
 
 struct csr5g_matrix_s {
   Handle* h;
@@ -335,6 +335,80 @@ int csr5g_csr_spmv_host(int device, int32_t kernel, int64_t m, int64_t n, int64_
   if (m > 0 && (e = cudaMemcpy(h_y, d_y, sizeof(double) * m, cudaMemcpyDeviceToHost)) != cudaSuccess)
     return done(cuda_fail(e, "cudaMemcpy(y)"));
   return done(CSR5G_OK);
+}
+
+int csr5g_spmv_tile(csr5g_matrix hm, int64_t tid, const double* h_x, int64_t* h_rows,
+                    double* h_vals, uint8_t* h_acc, int64_t cap, int64_t* count) {
+  if (!hm || !count) return fail(CSR5G_EINVAL, "csr5g: NULL argument");
+  Handle* h = hm->h;
+  const csr5g_info& in = h->info;
+  if (tid < in.tile_begin || tid >= in.tile_end)
+    return fail(CSR5G_EINVAL, "spmv_csr5_tile: tile " + std::to_string(tid) +
+                                  " is not a complete tile");
+  if (in.n > 0 && !h_x) return fail(CSR5G_EINVAL, "csr5g: x is NULL");
+  const int64_t k = tid - in.tile_begin, B = h->B;
+  CSR5G_CUDA(cudaSetDevice(h->device));
+  double *d_x = nullptr, *d_vals = nullptr;
+  int64_t* d_rows = nullptr;
+  int32_t* d_count = nullptr;
+  auto done = [&](int rc) {
+    for (void* q : {(void*)d_x, (void*)d_vals, (void*)d_rows, (void*)d_count}) cudaFree(q);
+    return rc;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&d_x, sizeof(double) * std::max<int64_t>(in.n, 1))) != cudaSuccess ||
+      (e = cudaMalloc(&d_vals, sizeof(double) * B)) != cudaSuccess ||
+      (e = cudaMalloc(&d_rows, sizeof(int64_t) * B)) != cudaSuccess ||
+      (e = cudaMalloc(&d_count, sizeof(int32_t))) != cudaSuccess)
+    return done(cuda_fail(e, "cudaMalloc(tile trace)"));
+  if (in.n > 0 && (e = cudaMemcpy(d_x, h_x, sizeof(double) * in.n, cudaMemcpyHostToDevice)) !=
+                      cudaSuccess)
+    return done(cuda_fail(e, "cudaMemcpy(x)"));
+  if (int rc = launch_tile_trace(h, k, d_x, d_rows, d_vals, d_count, nullptr)) return done(rc);
+  int32_t H = 0;
+  if ((e = cudaMemcpy(&H, d_count, sizeof H, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return done(cuda_fail(e, "tile trace"));
+  std::vector<int64_t> rows((size_t)H);
+  std::vector<double> vals((size_t)H);
+  std::vector<uint64_t> words(kOmega);
+  const size_t wb = h->wide ? 8 : 4;
+  std::vector<unsigned char> raw(kOmega * wb);
+  if ((e = cudaMemcpy(rows.data(), d_rows, sizeof(int64_t) * H, cudaMemcpyDeviceToHost)) !=
+          cudaSuccess ||
+      (e = cudaMemcpy(vals.data(), d_vals, sizeof(double) * H, cudaMemcpyDeviceToHost)) !=
+          cudaSuccess ||
+      (e = cudaMemcpy(raw.data(), static_cast<const unsigned char*>(h->desc) + k * kOmega * wb,
+                      kOmega * wb, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return done(cuda_fail(e, "tile trace"));
+  for (int i = 0; i < kOmega; ++i) {
+    uint64_t w = 0;
+    std::memcpy(&w, raw.data() + i * wb, wb);
+    words[i] = w;
+  }
+  if (cap < H) return done(fail(CSR5G_EINVAL, "csr5g: tile contribution buffer too small"));
+  // the reference's emission order (spmv.cpp:61-105): per column, the
+  // segments sealed inside it top to bottom (accumulate only for head 0),
+  // then every head-bearing column's bottom piece (accumulate)
+  const int sigma = (int)in.sigma;
+  const uint64_t fmask = sigma >= 64 ? ~0ull : (1ull << sigma) - 1;
+  int64_t q = 0;
+  auto emit = [&](int64_t head, bool acc) {
+    if (h_rows) h_rows[q] = rows[(size_t)head];
+    if (h_vals) h_vals[q] = vals[(size_t)head];
+    if (h_acc) h_acc[q] = acc ? 1 : 0;
+    ++q;
+  };
+  for (int pass = 0; pass < 2; ++pass)
+    for (int i = 0; i < kOmega; ++i) {
+      const int64_t y = (int64_t)(words[i] >> (kSegBits + sigma));
+      const int cnt = __builtin_popcountll(words[i] & fmask);
+      if (pass == 0)
+        for (int s = 0; s + 1 < cnt; ++s) emit(y + s, y + s == 0);
+      else if (cnt > 0)
+        emit(y + cnt - 1, true);
+    }
+  *count = q;
+  return done(q == H ? CSR5G_OK : fail(CSR5G_ERUNTIME, "csr5g: tile trace head count mismatch"));
 }
 
 int csr5g_export_row_ptr(csr5g_matrix hm, int64_t* h_row_ptr) {

@@ -670,8 +670,11 @@ void free_handle(Handle* h) {
                   (void*)h->run_last, (void*)h->run_cnt, (void*)h->send, (void*)h->spill,
                   (void*)h->warp_begin})
     if (p) cudaFreeAsync(p, 0);
-  for (const StreamScratch& x : h->extra_scratch)
-    for (void* p : {(void*)x.item_val, (void*)x.run_cnt, (void*)x.spill}) cudaFreeAsync(p, 0);
+  for (const StreamScratch& x : h->scratch) {
+    if (x.owned)
+      for (void* p : {(void*)x.item_val, (void*)x.run_cnt, (void*)x.spill}) cudaFreeAsync(p, 0);
+    if (x.done) cudaEventDestroy(x.done);
+  }
   cudaDeviceSynchronize();
   cudaSetDevice(prev);
   delete h;

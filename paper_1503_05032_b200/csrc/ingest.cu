@@ -242,6 +242,7 @@ int csr5g_coo_to_csr(int device, int64_t m, int64_t n, int64_t count, const int6
     return fail(CSR5G_ERANGE, "csr5g: m or n >= 2^31 does not fit the device CSR");
   if (!d_row_ptr || (count > 0 && (!d_rows || !d_cols || !d_vals || !d_col_idx || !d_val)))
     return fail(CSR5G_EINVAL, "csr5g: NULL device buffer");
+  if (int rc = resolve_device(&device)) return rc;
   CSR5G_CUDA(cudaSetDevice(device));
   cudaStream_t st = static_cast<cudaStream_t>(stream_v);
   int sms = 148;
@@ -334,6 +335,7 @@ int csr5g_coo_to_csr_host(int device, int64_t m, int64_t n, int64_t count, const
     return fail(CSR5G_EINVAL, "csr5g: NULL argument");
   *nnz = 0;
   if (m < 0 || n < 0 || count < 0) return fail(CSR5G_EINVAL, "csr: negative dimension");
+  if (int rc = resolve_device(&device)) return rc;
   CSR5G_CUDA(cudaSetDevice(device));
   const size_t k = (size_t)std::max<int64_t>(count, 1);
   int64_t *dr = nullptr, *dc = nullptr, *drp = nullptr;

@@ -84,12 +84,18 @@ struct SpmvArgs {
   int32_t stage_bytes;     // one tile: val | col_idx | descriptor words
   int32_t bar_bytes;       // mbarrier area at the start of shared memory
   int32_t atomic;          // SpmvMode::atomic
-  int32_t x_mode;          // x gather path: 0 L1+evict_last, 1 L1 no-allocate+evict_last
+  int32_t x_mode;          // x gather path: 0 L1+evict_last, 1 L1 no-allocate+evict_last,
+                           // 2 LSU, 3 .cg, 4 plain .nc, 5 = 1 with a 64 B L2 prefetch,
+                           // 6 = 4 with 64 B, 7 / 8 = 1 / 5 in CSR order (VR only)
   int32_t stream_only;     // profiling: run the TMA ring without gathers/math
   int32_t early_gather;    // random gathers: issue tile k+1's gathers before tile k's depth loop
   float x_frac;            // share of x lines given evict_last (the rest evict_first)
   int32_t y_hint;          // y stores: 1 = L2 evict_first, no L1 allocation
   Mirrors mir;             // fused iterative mode: peer next-x buffers (n = 0: none)
+  int64_t trace_tile;      // trace launch (csr5g_spmv_tile): the tile and its outputs
+  int64_t* trace_row;
+  double* trace_val;
+  int32_t* trace_count;
 };
 
 struct Pipeline;  // pipeline.cu: host-vector copy/compute pipeline
@@ -102,7 +108,11 @@ struct StreamScratch {
   double* item_val;
   int32_t* run_cnt;
   double* spill;
+  cudaEvent_t done = nullptr;  // recorded after the last SpMV that used it
+  uint64_t last_use = 0;       // LRU stamp
+  bool owned = true;           // false: the handle's own arrays (freed with it)
 };
+constexpr size_t kMaxStreamScratch = 8;  // scratch sets per handle (LRU beyond)
 struct Binding;   // p2p.cu: a shard's NVLink boundary exchange
 
 struct Handle {
@@ -142,11 +152,10 @@ struct Handle {
   int64_t eo_entries = 0;         // empty_offset entries
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
   int carveout_pct = -1;  // preferred shared-memory carveout of the SpMV kernel
-  // scratch of streams other than the first one that ran an SpMV (which uses
-  // item_row / item_val / spill above); guarded by scratch_mu
-  bool scratch_claimed = false;
-  cudaStream_t scratch_stream = nullptr;
-  std::vector<StreamScratch> extra_scratch;
+  // per-stream SpMV scratch (the handle's own arrays are the first set);
+  // guarded by scratch_mu
+  std::vector<StreamScratch> scratch;
+  uint64_t scratch_clock = 0;
   std::mutex scratch_mu;
   Pipeline* pipe = nullptr;  // created by the first host-vector SpMV
   std::mutex pipe_mu;        // host-vector calls from several threads enqueue one at a time
@@ -156,6 +165,7 @@ struct Handle {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
+int resolve_device(int* device);  // device < 0: the current device
 
 #define CSR5G_CUDA(call)                                   \
   do {                                                     \
@@ -174,8 +184,11 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
 int launch_fixup(Handle* h, const csr5g_partial* d_all, int world, int rank, double* d_y,
                  cudaStream_t stream);
 int launch_to_csr(Handle* h, int32_t* d_col, double* d_val, cudaStream_t stream);
+int launch_tile_trace(Handle* h, int64_t k, const double* d_x, int64_t* d_rows, double* d_vals,
+                      int32_t* d_count, cudaStream_t stream);
 int spmv_plan(Handle* h, int sms);
 int func_attrs(const void* fn, int device, int smem, int carve);
+int scratch_done(Handle* h, cudaStream_t stream);
 int spmv_host_batch(Handle* h, const double* const* xs, double* const* ys, int64_t count,
                     int mode, cudaStream_t stream);
 void free_pipeline(Pipeline* p);
@@ -290,6 +303,21 @@ __device__ __forceinline__ double ld_x_lsu(const double* p, uint64_t pol) {
 __device__ __forceinline__ double ld_x_plain(const double* p) {
   double v;
   asm("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+// Random gathers with a 64-byte L2 prefetch size: without the qualifier a
+// random 8-byte load moves ~2.4 sectors from DRAM, with it ~1.5
+// (tools/sector_probe.cu, profiles/r02_sector_probe.txt).
+__device__ __forceinline__ double ld_keep_na64(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::64B.f64 %0, [%1], %2;"
+      : "=d"(v)
+      : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_x_plain64(const double* p) {
+  double v;
+  asm("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ double ld_x_cg(const double* p) {

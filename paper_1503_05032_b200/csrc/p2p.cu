@@ -314,9 +314,17 @@ int csr5g_mailbox_create(int device, int32_t world, int32_t rank, int64_t vec_le
   // every slot starts as "no record" (row -1)
   csr5g_partial none[kMaxWorld];
   for (auto& r : none) r = csr5g_partial{-1, 0.0};
-  CSR5G_CUDA(cudaMemcpy(m->local->slot, none, sizeof none, cudaMemcpyHostToDevice));
+  auto undo = [&](int rc) {  // every buffer allocated above, on any later failure
+    cudaFree(m->local);
+    cudaFree(m->d_peer_ack);
+    cudaFree(m->d_peer_xready);
+    delete m;
+    return rc;
+  };
+  if ((e = cudaMemcpy(m->local->slot, none, sizeof none, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return undo(cuda_fail(e, "csr5g_mailbox_create: slots"));
   m->peer[rank] = m->local;
-  if (int rc = refresh_peer_table(m)) return rc;
+  if (int rc = refresh_peer_table(m)) return undo(rc);
   *out = new csr5g_mailbox_s{m};
   return CSR5G_OK;
 }

@@ -87,6 +87,10 @@ WORKLOADS = {
                     min_len=1, max_len=32, seed=1,
                     desc="mixed 2^23 x 2^23: 40% empty rows, 4 rows of 1,048,576 nnz, others "
                          "U[1,32] nnz, values U[0.5,1.5)"),
+    "rmat25": dict(gen="rmat", scale=25, edge_factor=16, permute=True, seed=1,
+                   desc="R-MAT scale 25, edge factor 16, Graph500, dedup, vertices permuted"),
+    "rmat26": dict(gen="rmat", scale=26, edge_factor=16, permute=True, seed=1,
+                   desc="R-MAT scale 26, edge factor 16, Graph500, dedup, vertices permuted"),
     "rmat27": dict(gen="rmat", scale=27, edge_factor=16, permute=True, seed=1,
                    desc="R-MAT scale 27, edge factor 16, Graph500, dedup, vertices permuted"),
 }

@@ -455,3 +455,34 @@ def test_skewed_tile_work(g, orc):
                 assert_y_close(gpu_y(g, a5, x, mode), orc.spmv(a, x, 32, sigma), a, x,
                                f"skew sigma={sigma} {mode}")
             a5.release()
+
+
+@pytest.mark.parametrize("sigma", [1, 5, 16, 24])
+def test_gather_orders_give_identical_y(g, orc, sigma, monkeypatch):
+    """The VR kernel's x-gather paths (x_mode 1: lane-per-column order, the
+    default below 3x L2; 8: CSR order through the shared-memory exchange with a
+    64-byte L2 prefetch, the plan for x several times the L2; 5, 7: the other
+    two combinations) fetch the same x values into the same depth-loop slots,
+    so y is bit-identical across them and within tolerance of the oracle; the
+    arrays stay bit-exact."""
+    rng = np.random.default_rng(sigma)
+    m = 6000
+    lens = rng.integers(0, 2 * sigma + 1, m)
+    lens[rng.integers(0, m, 3)] = 900  # rows spanning tiles
+    rows = np.repeat(np.arange(m), lens)
+    cols = rng.integers(0, 500000, rows.size)
+    a = orc.coo_to_csr(rows.tolist(), cols.tolist(), rng.uniform(0.5, 1.5, rows.size).tolist(),
+                       m, 500000)
+    x = orc.rng(3).random_x(a.n)
+    ref = orc.build(a, 32, sigma)
+    ys = {}
+    for mode in ("1", "5", "7", "8"):
+        monkeypatch.setenv("CSR5G_XMODE", mode)
+        a5 = gpu_build(g, a, sigma)
+        assert a5.info.kernel_variant == 1 and a5.info.x_mode == int(mode), (mode, a5.info.x_mode)
+        ys[mode] = gpu_y(g, a5, x)
+        compare_arrays(a5.export(), ref, f"x_mode {mode}")
+        a5.release()
+    for mode, y in ys.items():
+        assert np.array_equal(y.view(np.int64), ys["1"].view(np.int64)), mode
+    assert_y_close(ys["8"], orc.spmv(a, x, 32, sigma), a, x, "csr-order gathers")

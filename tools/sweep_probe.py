@@ -28,6 +28,14 @@ for cfg in configs:
     for kv in cfg.split():
         k, v = kv.split("=", 1)
         os.environ[k] = v
+    if "L2_FETCH" in os.environ:  # cudaLimitMaxL2FetchGranularity (context-wide)
+        import ctypes
+        rt = ctypes.CDLL("libcudart.so.12")
+        lim = ctypes.c_size_t(int(os.environ["L2_FETCH"]))
+        rc = rt.cudaDeviceSetLimit(ctypes.c_int(0x05), lim)
+        got = ctypes.c_size_t(0)
+        rt.cudaDeviceGetLimit(ctypes.byref(got), ctypes.c_int(0x05))
+        print(f"  cudaLimitMaxL2FetchGranularity <- {lim.value}: rc {rc}, now {got.value}", flush=True)
     a5 = csr5.csr_to_csr5(a, csr5.TuningParams(sigma=sigma))
     reps = 10 if a.nnz < 1e9 else 5
     evs = [(csr5.Event(), csr5.Event()) for _ in range(reps)]
