@@ -651,7 +651,7 @@ def measure_sharded(args, name, workload, dev, local, dist, rank, world):
     x = torch.as_tensor(x_host).to(dev)
     y = torch.empty(m, dtype=torch.float64, device=dev)
     sigma = csr5.select_sigma(nnz / m)
-    lo, hi = mg.Csr5Sharded.slices_for(nnz, sigma, rank, world)
+    lo, hi = mg.Csr5Sharded.slices_for(nnz, sigma, rank, world, W.row_ptr)
     col_s, val_s = W.entries(lo, hi)
     torch.cuda.synchronize()
     t0 = time.perf_counter()

@@ -395,6 +395,8 @@ class Ref:
         L.ref_csr_get.argtypes = [C.c_void_p, _i64p, _i64p, _f64p]
         L.ref_csr_free.argtypes = [C.c_void_p]
         L.ref_max_threads.restype = C.c_int
+        L.ref_dump_format.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        L.ref_dump_format.restype = C.c_int64
         L.ref_set_threads.argtypes = [C.c_int]
 
     def _err(self, rc):
@@ -434,6 +436,17 @@ class Ref:
                               _p(eo, _i64p), _p(ci, _i64p), _p(va, _f64p))
             return Csr5Arrays(a.m, a.n, a.nnz, omega, sigma, p, pc, tail, tpb, wb, yb, sb, tile_ptr,
                               tile_desc, eo_ptr, eo, ci, va)
+        finally:
+            self.L.ref_free(h)
+
+    def dump_format(self, a: Csr, omega: int, sigma: int) -> str:
+        """format.cpp:267-305: the reference's own text dump of its build."""
+        h, _ = self.build_handle(a, omega, sigma)
+        try:
+            n = self.L.ref_dump_format(h, None, 0)
+            buf = C.create_string_buffer(n + 1)
+            self.L.ref_dump_format(h, buf, n)
+            return buf.raw[:n].decode()
         finally:
             self.L.ref_free(h)
 

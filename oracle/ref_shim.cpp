@@ -124,6 +124,16 @@ void ref_export(void* hv, uint64_t* tile_ptr, uint64_t* tile_desc, int64_t* eo_p
   std::memcpy(val, a5.val.data(), a5.val.size() * sizeof(double));
 }
 
+// dump_format (format.hpp:190): the reference's text dump into buf (at most
+// cap bytes); returns the full length.
+int64_t ref_dump_format(void* hv, char* buf, int64_t cap) {
+  std::ostringstream out;
+  csr5::dump_format(static_cast<RefHandle*>(hv)->a5, out);
+  const std::string t = out.str();
+  if (buf && cap > 0) std::memcpy(buf, t.data(), std::min<size_t>(t.size(), (size_t)cap));
+  return static_cast<int64_t>(t.size());
+}
+
 // spmv_csr5 (spmv.hpp:58); mode 0 deterministic, 1 atomic.
 int ref_spmv(void* hv, const double* x, double* y, int mode) {
   try {

@@ -326,6 +326,24 @@ def csr5_to_csr(a5: Csr5Matrix, row_ptr: torch.Tensor, stream=None) -> CsrMatrix
     return CsrMatrix(i.m, i.n, row_ptr, col, val)
 
 
+def spmv_csr5_tile(a5: Csr5Matrix, tid: int, x):
+    """spmv.cpp:211-222 (TileContribution hook): the contributions of complete
+    tile `tid`, computed by the GPU tile kernel itself (csr5g_spmv_tile), in
+    the reference's emission order.  Returns (rows, values, accumulate)."""
+    xh = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if xh.shape != (a5.n,):
+        raise ValueError(f"spmv: x has length {xh.size}, expected {a5.n}")
+    cap = 32 * a5.sigma + 1
+    rows = np.zeros(cap, dtype=np.int64)
+    vals = np.zeros(cap, dtype=np.float64)
+    acc = np.zeros(cap, dtype=np.uint8)
+    cnt = C.c_int64()
+    check(lib().csr5g_spmv_tile(a5.handle, tid, xh.ctypes.data, rows.ctypes.data,
+                                vals.ctypes.data, acc.ctypes.data, cap, C.byref(cnt)))
+    k = cnt.value
+    return rows[:k], vals[:k], acc[:k].astype(bool)
+
+
 def dump_format(a5: Csr5Matrix) -> str:
     """format.cpp:267-305 text dump, produced from the device arrays."""
     i = a5.info
@@ -504,5 +522,5 @@ def spmv_csr5_evt(a5: Csr5Matrix, x: torch.Tensor, y: torch.Tensor, ev0: Event, 
 
 
 __all__ = ["TuningParams", "CsrMatrix", "Csr5Matrix", "csr_to_csr5", "csr_to_csr5_shard",
-           "spmv_csr5", "spmv_csr", "read_matrix_market", "coo_to_csr", "load_matrix_market", "spmv_host", "spmv_host_batch", "csr5_to_csr", "dump_format", "select_sigma", "layout",
+           "spmv_csr5", "spmv_csr5_tile", "spmv_csr", "read_matrix_market", "coo_to_csr", "load_matrix_market", "spmv_host", "spmv_host_batch", "csr5_to_csr", "dump_format", "select_sigma", "layout",
            "stencil", "stencil_box", "stencil_box_size", "Event", "spmv_csr5_evt", "Partial"]

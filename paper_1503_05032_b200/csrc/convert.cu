@@ -420,31 +420,45 @@ __global__ void __launch_bounds__(kFixThreads) k_warp_bounds_fix(int64_t* __rest
   }
 }
 
-// Item rows of the in-kernel calibration (spmv.cu resolve_item): item 2w is
-// the row of warp w's first tile start, item 2w+1 the row holding the warp's
-// last nonzero -- the last head of its last tile t: H = y_offset + popc(flags)
-// of column 31, row = tile_row + (flagged ? eo[eo_ptr[t] + H - 1] : H - 1) --
-// and item 2*nwarps (tail) the tail's first row.  O(1) loads per item.
+// Item rows of the in-kernel calibration (spmv_kernel.cuh "row runs"): item
+// 2q is the row of chunk q's first tile start, item 2q+1 the row holding the
+// chunk's last nonzero -- the last head of its last tile t: H = y_offset +
+// popc(flags) of column 31, row = tile_row + (flagged ? eo[eo_ptr[t] + H - 1]
+// : H - 1) -- and item 2*nchunks (tail) the tail's first row.  O(1) loads per item.
 template <typename W>
-__global__ void k_item_keys(const int64_t* __restrict__ warp_begin,
+__global__ void k_item_keys(int64_t chunk_tiles, int64_t pcs, int64_t nchunks,
                             const uint32_t* __restrict__ tile_ptr, const W* __restrict__ desc,
                             const int64_t* __restrict__ eo_ptr, const int32_t* __restrict__ eo,
-                            int sigma, int nwarps, int has_tail_item, int64_t tail_row_begin,
+                            int sigma, int has_tail_item, int64_t tail_row_begin,
                             int64_t* __restrict__ key) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int n = 2 * nwarps + (has_tail_item ? 1 : 0);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = 2 * nchunks + (has_tail_item ? 1 : 0);
   if (i >= n) return;
-  if (i == 2 * nwarps) {
+  if (i == 2 * nchunks) {
     key[i] = tail_row_begin;
   } else if ((i & 1) == 0) {
-    key[i] = tile_ptr[warp_begin[i >> 1]] & 0x7fffffffu;
+    key[i] = tile_ptr[(i >> 1) * chunk_tiles] & 0x7fffffffu;
   } else {
-    const int64_t t = warp_begin[(i >> 1) + 1] - 1;
+    const int64_t t = min(((i >> 1) + 1) * chunk_tiles, pcs) - 1;
     const uint32_t tp = tile_ptr[t];
     const uint64_t wd = (uint64_t)desc[t * 32 + 31];
     const int H = (int)(wd >> (kSegBits + sigma)) + __popcll(wd & ((1ull << sigma) - 1));
     key[i] = (int64_t)(tp & 0x7fffffffu) + ((tp >> 31) ? (int64_t)eo[eo_ptr[t] + H - 1] : H - 1);
   }
+}
+
+// inclusive work prefix at every chunk end (the warp split is in whole chunks)
+__global__ void k_chunk_prefix(const int64_t* __restrict__ prefix, int64_t pcs,
+                               int64_t chunk_tiles, int64_t nchunks, int64_t* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < nchunks) out[c] = prefix[min((c + 1) * chunk_tiles, pcs) - 1];
+}
+
+// warp bounds: chunk index -> tile index
+__global__ void k_chunk_bounds_to_tiles(int64_t* __restrict__ begin, int nw, int64_t chunk_tiles,
+                                        int64_t pcs) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w <= nw) begin[w] = min(begin[w] * chunk_tiles, pcs);
 }
 
 // Runs of equal keys (keys are non-decreasing): run_first[i] = prefix max of
@@ -454,7 +468,8 @@ __global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __rest
                                                            int32_t* __restrict__ run_first,
                                                            int32_t* __restrict__ run_last,
                                                            int32_t* __restrict__ run_cnt,
-                                                           double* __restrict__ item_val) {
+                                                           double* __restrict__ item_val,
+                                                           uint8_t* __restrict__ item_cls) {
   __shared__ int part[kFixThreads];
   const int t = threadIdx.x;
   for (int i = t; i < n; i += kFixThreads) {  // per-launch state: no arrivals, idle pair slots
@@ -495,6 +510,11 @@ __global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __rest
   for (int i = hi - 1; i >= lo; --i) {
     if (i == n - 1 || key[i] != key[i + 1]) run = i;
     run_last[i] = run;
+  }
+  __syncthreads();
+  for (int i = t; i < n; i += kFixThreads) {  // length class | first-of-run
+    const int len = run_last[i] - run_first[i] + 1;
+    item_cls[i] = (uint8_t)((len == 1 ? 0 : len == 2 ? 1 : 2) | (run_first[i] == i ? 4 : 0));
   }
 }
 
@@ -667,7 +687,8 @@ void free_handle(Handle* h) {
   free_binding(h->mg);
   for (void* p : {(void*)h->row_ptr, (void*)h->tile_ptr, h->desc, (void*)h->eo_ptr, (void*)h->eo,
                   (void*)h->col, (void*)h->val, (void*)h->item_val, (void*)h->run_first,
-                  (void*)h->run_last, (void*)h->run_cnt, (void*)h->send, (void*)h->spill,
+                  (void*)h->run_last, (void*)h->run_cnt, (void*)h->item_cls, (void*)h->send,
+                  (void*)h->spill,
                   (void*)h->warp_begin})
     if (p) cudaFreeAsync(p, 0);
   for (const StreamScratch& x : h->scratch) {
@@ -715,6 +736,12 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   if (tile_begin < 0 || tile_end < tile_begin || tile_end > pc)
     return fail(CSR5G_EINVAL, "csr5g: shard tile range outside [0, p_complete]");
   const bool is_last = tile_end == pc;
+  {
+    const int64_t K = chunk_tiles_for(pc);
+    if (shard && (tile_begin % K != 0 || (tile_end % K != 0 && !is_last)))
+      return fail(CSR5G_EINVAL, "csr5g: a shard's tile range must be whole calibration chunks "
+                                "(multiples of " + std::to_string(K) + " tiles, csr5g_chunk_tiles)");
+  }
   if ((with_tail != 0) != (is_last && tail > 0))
     return fail(CSR5G_EINVAL, "csr5g: the shard ending at p_complete must hold the tail");
   const int64_t pcs = tile_end - tile_begin;
@@ -748,12 +775,13 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   int64_t* work_prefix = nullptr;
   int64_t* work = nullptr;
   int64_t* item_key = nullptr;
+  int64_t* chunk_prefix = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   auto cleanup = [&](int code) {
     if (side && code) cudaStreamSynchronize(side);  // error path: side work may be in flight
     for (void* p : {(void*)zblock, cub_tmp, cub_tmp2, (void*)work_prefix, (void*)work,
-                    (void*)item_key})
+                    (void*)item_key, (void*)chunk_prefix})
       if (p) cudaFreeAsync(p, stream);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -977,44 +1005,55 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   h->eo_entries = eo_total;
   h->info.sigma = sigma;  // spmv_plan picks the sigma-specialised kernel
   h->info.n = n;          // ... and sizes its shared memory by x
+  // calibration chunks: a function of the global matrix only, so every
+  // partition (warps, shards) folds a row's partials the same way
+  h->chunk_tiles = chunk_tiles_for(pc);
+  h->nchunks = (pcs + h->chunk_tiles - 1) / h->chunk_tiles;
   TRY(spmv_plan(h, sms));
   const int64_t rows_total = h->lead_rows + (m - h->tail_row_begin);
   h->rows_blocks = rows_total > 0 ? (int)std::min<int64_t>((rows_total + 255) / 256, 2 * sms) : 0;
-  const int64_t items = 2 * (int64_t)h->nwarps + 1;
+  const int64_t items = 2 * h->nchunks + 1;
   TRY(dev_alloc(&h->item_val, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->run_first, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->run_last, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->run_cnt, (size_t)items, &alloc_ms, &bytes));
+  TRY(dev_alloc(&h->item_cls, (size_t)items + 1, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->spill, (size_t)std::max(h->nwarps, 1) * (B + 1), &alloc_ms, &bytes));
   if (pcs > 0 && h->nwarps > 0) {
+    // warp ranges of whole chunks, split by the chunks' work
     TRY(dev_alloc(&h->warp_begin, (size_t)h->nwarps + 1, &alloc_ms, &bytes));
+    TRY(dev_alloc(&chunk_prefix, (size_t)h->nchunks, &alloc_ms, &tmp_bytes));
+    k_chunk_prefix<<<(unsigned)((h->nchunks + 255) / 256), 256, 0, stream>>>(
+        work_prefix, pcs, h->chunk_tiles, h->nchunks, chunk_prefix);
     auto* emax = reinterpret_cast<unsigned long long*>(scal + 6);  // zeroed with the block
     k_equal_split_max<<<(unsigned)((h->nwarps + 255) / 256), 256, 0, stream>>>(
-        work_prefix, pcs, h->nwarps, emax);
+        chunk_prefix, h->nchunks, h->nwarps, emax);
     TRYC(cudaGetLastError());
     k_warp_bounds<<<(unsigned)((h->nwarps + 1 + 255) / 256), 256, 0, stream>>>(
-        work_prefix, pcs, h->nwarps, emax, h->warp_begin);
+        chunk_prefix, h->nchunks, h->nwarps, emax, h->warp_begin);
     TRYC(cudaGetLastError());
     k_warp_bounds_fix<<<1, kFixThreads, 0, stream>>>(h->warp_begin, h->nwarps);
+    k_chunk_bounds_to_tiles<<<(unsigned)((h->nwarps + 1 + 255) / 256), 256, 0, stream>>>(
+        h->warp_begin, h->nwarps, h->chunk_tiles, pcs);
     TRYC(cudaGetLastError());
   }
   // runs of the calibration items (the rows warps / the tail share)
   {
-    const int n_items = 2 * h->nwarps + (h->has_tail_item ? 1 : 0);
+    const int n_items = (int)(2 * h->nchunks + (h->has_tail_item ? 1 : 0));
     if (n_items > 0) {
       TRY(dev_alloc(&item_key, (size_t)n_items, &alloc_ms, &tmp_bytes));
       const unsigned kb = (unsigned)((n_items + 255) / 256);
       if (h->wide)
         k_item_keys<uint64_t><<<kb, 256, 0, stream>>>(
-            h->warp_begin, h->tile_ptr, (const uint64_t*)h->desc, h->eo_ptr, h->eo, (int)sigma,
-            h->nwarps, h->has_tail_item ? 1 : 0, h->tail_row_begin, item_key);
+            h->chunk_tiles, pcs, h->nchunks, h->tile_ptr, (const uint64_t*)h->desc, h->eo_ptr,
+            h->eo, (int)sigma, h->has_tail_item ? 1 : 0, h->tail_row_begin, item_key);
       else
         k_item_keys<uint32_t><<<kb, 256, 0, stream>>>(
-            h->warp_begin, h->tile_ptr, (const uint32_t*)h->desc, h->eo_ptr, h->eo, (int)sigma,
-            h->nwarps, h->has_tail_item ? 1 : 0, h->tail_row_begin, item_key);
+            h->chunk_tiles, pcs, h->nchunks, h->tile_ptr, (const uint32_t*)h->desc, h->eo_ptr,
+            h->eo, (int)sigma, h->has_tail_item ? 1 : 0, h->tail_row_begin, item_key);
       TRYC(cudaGetLastError());
       k_item_runs<<<1, kFixThreads, 0, stream>>>(item_key, n_items, h->run_first, h->run_last,
-                                                 h->run_cnt, h->item_val);
+                                                 h->run_cnt, h->item_val, h->item_cls);
       TRYC(cudaGetLastError());
     }
   }
@@ -1064,6 +1103,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   in.x_mode = h->x_mode;
   in.x_window = h->x_window ? 1 : 0;
   in.kernel_variant = h->vr ? 1 : (h->nf ? 2 : 0);
+  in.chunk_tiles = h->chunk_tiles;
   // the build is synchronous (format.hpp:182 returns a finished value): the
   // handle is usable from any stream once it returns
   TRYC(cudaStreamSynchronize(stream));

@@ -60,6 +60,7 @@ struct SpmvArgs {
   double* item_val;        // run partials (deterministic mode), per stream
   const int32_t* run_first;  // item i's run of equal rows is items [run_first[i], run_last[i]]
   const int32_t* run_last;
+  const uint8_t* item_cls;   // per item: run length class (0 one, 1 two, 2 more) | 4 if first
   int32_t* run_cnt;        // arrivals per run (indexed by its first item), per stream
   csr5g_partial* send;
   uint32_t* send_flag;     // p2p.cu: owner's ready flag for the send record (or null)
@@ -76,13 +77,16 @@ struct SpmvArgs {
   int64_t tile_ptr_len;
   int64_t first_row;       // row of head 0 of the first held tile
   int32_t first_owned;     // that row starts inside this handle
-  int32_t has_tail_item;   // tail exists: its first row is item 2*nwarps
+  int32_t has_tail_item;   // tail exists: its first row is item 2*nchunks
   int32_t sigma;
   int32_t B;
-  int32_t nwarps;          // tile warps (each a contiguous tile range)
+  int32_t nwarps;          // tile warps (each a contiguous range of whole chunks)
+  int64_t chunk_tiles;     // tiles per calibration chunk (a function of the matrix alone)
+  int64_t nchunks;         // chunks held; items 2q / 2q+1 = chunk q's first / last run
   int32_t stages;          // TMA ring depth per warp
   int32_t stage_bytes;     // one tile: val | col_idx | descriptor words
   int32_t bar_bytes;       // mbarrier area at the start of shared memory
+  int32_t calib_off;       // byte offset of the per-warp calibration area (64 B per warp)
   int32_t atomic;          // SpmvMode::atomic
   int32_t x_mode;          // x gather path: 0 L1+evict_last, 1 L1 no-allocate+evict_last,
                            // 2 LSU, 3 .cg, 4 plain .nc, 5 = 1 with a 64 B L2 prefetch,
@@ -130,6 +134,7 @@ struct Handle {
   double* item_val = nullptr;
   int32_t* run_first = nullptr;  // static run structure of the items (built once)
   int32_t* run_last = nullptr;
+  uint8_t* item_cls = nullptr;   // run class of every item (SpmvArgs::item_cls)
   int32_t* run_cnt = nullptr;    // zeroed; every launch leaves it zeroed
   csr5g_partial* send = nullptr;
   csr5g_partial* send_ext = nullptr;  // caller-provided record slot
@@ -143,6 +148,7 @@ struct Handle {
   int64_t first_row = 0, last_row = 0;
   bool first_owned = true, is_last = true, has_tail_item = false;
   int nwarps = 0, tile_blocks = 0, rows_blocks = 0;
+  int64_t chunk_tiles = 1, nchunks = 0;  // calibration chunks (spmv_kernel.cuh "row runs")
   double lines_per_gather = 1.0;  // sampled x-gather locality (1 = coalesced, 32 = random)
   int x_mode = 0;                 // gather path chosen by the plan
   bool x_window = false;          // L2 persisting window on x
@@ -151,6 +157,7 @@ struct Handle {
   int max_heads = 0;              // most segment heads in one tile
   int64_t eo_entries = 0;         // empty_offset entries
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
+  int calib_off = 0;  // shared-memory offset of the per-warp calibration area
   int carveout_pct = -1;  // preferred shared-memory carveout of the SpMV kernel
   // per-stream SpMV scratch (the handle's own arrays are the first set);
   // guarded by scratch_mu
@@ -172,6 +179,10 @@ int resolve_device(int* device);  // device < 0: the current device
     cudaError_t e_ = (call);                               \
     if (e_ != cudaSuccess) return ::csr5g::cuda_fail(e_, #call); \
   } while (0)
+
+// Tiles per calibration chunk of a matrix with pc complete tiles: ~65536
+// chunks, so the items stay small and every SM's warps get many chunks.
+inline int64_t chunk_tiles_for(int64_t pc) { return (pc >> 16) > 1 ? (pc >> 16) : 1; }
 
 // ---- launchers implemented in convert.cu / spmv.cu -------------------------
 int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d_row_ptr,

@@ -141,7 +141,7 @@ int spmv_plan(Handle* h, int sms) {
   if (h->x_mode >= 7 && !h->vr) h->x_mode = 1;
   const int xex_bytes = h->x_mode >= 7 ? sigma * 33 * 8 : 0;
   auto need = [&](int w, int st) {
-    return bars(w, st) + w * (closed_bytes + kEoSlots * 4 + st * stage_bytes + xex_bytes);
+    return bars(w, st) + w * (closed_bytes + kEoSlots * 4 + st * stage_bytes + xex_bytes + 64);
   };
   // local gathers: warps per SM matter most (keep them, give up depth first);
   // random gathers: keep the TMA lead (depth), give up warps
@@ -159,6 +159,7 @@ int spmv_plan(Handle* h, int sms) {
   h->stage_bytes = stage_bytes;
   h->bar_bytes = bars(nw, stages);
   h->smem_bytes = need(nw, stages);
+  h->calib_off = h->smem_bytes - nw * 64;  // the last 64 bytes per warp
   // Ask for the smallest shared-memory carveout that holds the ring: the rest
   // of the SM's 256 KB stays L1, which is where outstanding gather misses land
   // (measured: a 233 KB carveout halves R-MAT throughput through mio/lg
@@ -173,7 +174,7 @@ int spmv_plan(Handle* h, int sms) {
     h->carveout_pct = std::min(100, std::max(0, pct));
   }
   const int64_t max_warps = (int64_t)sms * nw;
-  h->nwarps = (int)std::min<int64_t>(max_warps, h->pcs);
+  h->nwarps = (int)std::min<int64_t>(max_warps, h->nchunks);
   h->tile_blocks = (h->nwarps + nw - 1) / nw;
   return CSR5G_OK;
 }
@@ -222,7 +223,7 @@ int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, doubl
     x->stream = stream;
   }
   if (!x) {
-    const size_t items = 2 * (size_t)h->nwarps + 1;
+    const size_t items = 2 * (size_t)h->nchunks + 1;
     const size_t spill = (size_t)std::max(h->nwarps, 1) * (size_t)(h->B + 1);
     StreamScratch n{stream, nullptr, nullptr, nullptr};
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&n.item_val), items * 8, stream);
@@ -239,7 +240,12 @@ int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, doubl
     x = &h->scratch.back();
   }
   if (!x->done) CSR5G_CUDA(cudaEventCreateWithFlags(&x->done, cudaEventDisableTiming));
-  CSR5G_CUDA(cudaStreamWaitEvent(stream, x->done, 0));  // no-op until first recorded
+  // (inside a stream capture the graph's own ordering serialises the kernels;
+  // an event recorded outside it may not be waited on there)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CSR5G_CUDA(cudaStreamIsCapturing(stream, &cap));
+  if (cap == cudaStreamCaptureStatusNone)
+    CSR5G_CUDA(cudaStreamWaitEvent(stream, x->done, 0));  // no-op until first recorded
   x->last_use = ++h->scratch_clock;
   *iv = x->item_val;
   *rc = x->run_cnt;
@@ -249,6 +255,9 @@ int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, doubl
 
 // after the SpMV kernel of `stream`: its scratch set is free again from here
 int scratch_done(Handle* h, cudaStream_t stream) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CSR5G_CUDA(cudaStreamIsCapturing(stream, &cap));
+  if (cap != cudaStreamCaptureStatusNone) return CSR5G_OK;
   std::lock_guard<std::mutex> lock(h->scratch_mu);
   for (StreamScratch& s : h->scratch)
     if (s.stream == stream && s.done) CSR5G_CUDA(cudaEventRecord(s.done, stream));
@@ -283,6 +292,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   if (int rc = scratch_for(h, stream, &a.item_val, &a.run_cnt, &a.spill)) return rc;
   a.run_first = h->run_first;
   a.run_last = h->run_last;
+  a.item_cls = h->item_cls;
   a.send = h->send_ext ? h->send_ext : h->send;
   a.send_flag = h->send_flag;
   a.send_epoch = h->send_epoch;
@@ -301,9 +311,12 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.sigma = (int)in.sigma;
   a.B = (int)h->B;
   a.nwarps = h->nwarps;
+  a.chunk_tiles = h->chunk_tiles;
+  a.nchunks = h->nchunks;
   a.stages = h->stages;
   a.stage_bytes = h->stage_bytes;
   a.bar_bytes = h->bar_bytes;
+  a.calib_off = h->calib_off;
   a.atomic = atomic;
   a.mir = h->mir;
   const int grid = std::max(h->tile_blocks, h->rows_blocks);
@@ -328,7 +341,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     return e ? std::atoi(e) : 0;
   }();
   a.stream_only = stream_only;
-  const int64_t items = 2 * (int64_t)h->nwarps + (h->has_tail_item ? 1 : 0);
+  const int64_t items = 2 * h->nchunks + (h->has_tail_item ? 1 : 0);
   if (ev0) CSR5G_CUDA(cudaEventRecord(ev0, stream));
   if (grid > 0) {
     cudaLaunchConfig_t cfg{};
@@ -383,7 +396,7 @@ int launch_tile_trace(Handle* h, int64_t k, const double* d_x, int64_t* d_rows, 
   const int stage_bytes = (int)((h->B * 12 + 32 * wbytes + 127) / 128 * 128);
   const int closed_bytes = (int)(std::min<int64_t>(h->B, kClosedSlots) * 8);
   const int stages = 2, bar_bytes = 128;
-  const int smem = bar_bytes + closed_bytes + kEoSlots * 4 + stages * stage_bytes;
+  const int smem = bar_bytes + closed_bytes + kEoSlots * 4 + stages * stage_bytes + 64;
   double* spill = nullptr;
   CSR5G_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&spill), sizeof(double) * (h->B + 1), stream));
   SpmvArgs a{};
@@ -404,9 +417,12 @@ int launch_tile_trace(Handle* h, int64_t k, const double* d_x, int64_t* d_rows, 
   a.sigma = sigma;
   a.B = (int)h->B;
   a.nwarps = 1;
+  a.chunk_tiles = h->chunk_tiles;
+  a.nchunks = h->nchunks;
   a.stages = stages;
   a.stage_bytes = stage_bytes;
   a.bar_bytes = bar_bytes;
+  a.calib_off = smem - 64;
   a.x_mode = 4;
   a.x_frac = 1.0f;
   a.trace_tile = k;

@@ -68,7 +68,7 @@ __device__ void rows_part(const SpmvArgs& a) {
     double s = 0.0;
     for (int64_t q = lo; q < hi; ++q) s = fma(a.val[q - a.pos0], a.x[a.col[q - a.pos0]], s);
     if (a.has_tail_item && r == a.tail_row_begin) {
-      resolve_item(a, 2 * (int64_t)a.nwarps, r, s);
+      resolve_item(a, 2 * a.nchunks, r, s);
     } else {
       a.y[r] = s;
       if (a.mir.n) mirror_store(a.mir, r, s);
@@ -85,7 +85,7 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
 // The send record goes to local memory (collective exchange) or straight into
 // the owner rank's mailbox over NVLink (p2p.cu), followed there by its ready
 // flag: value stores, system-scope fence, then the flag store with release.
-__device__ __forceinline__ void write_run(int64_t row, double v, double* y, int64_t first_row,
+__device__ __noinline__ void write_run(int64_t row, double v, double* y, int64_t first_row,
                                           int first_owned, csr5g_partial* send, uint32_t* flag,
                                           uint32_t epoch, const Mirrors& mir) {
   if (!first_owned && row == first_row) {
@@ -178,8 +178,8 @@ __device__ void resolve_item(const SpmvArgs& a, int64_t idx, int64_t row, double
 
 // The same, called by a whole warp (idx, row, v uniform): the last arrival's
 // warp sums a long run 32 items at a time (fixed tree, deterministic).
-__device__ __forceinline__ void resolve_item_warp(const SpmvArgs& a, int64_t idx, int64_t row,
-                                                  double v, int lane) {
+__device__ __noinline__ void resolve_item_warp(const SpmvArgs& a, int64_t idx, int64_t row,
+                                               double v, int lane) {
   const int s = a.atomic ? 0 : a.run_first[idx], e = a.atomic ? 0 : a.run_last[idx];
   if (a.atomic || e <= s + 1) {  // single partial, pair exchange, or atomic mode
     if (lane == 0) resolve_item(a, idx, row, v);
@@ -312,13 +312,31 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
         y[r] = v;
       if (mirrored) mirror_store(a.mir, r, v);
     };
-    int64_t pend_row = -1;
-    double pend_val = 0.0;
-    bool pend_first = true;
-    // the warp's first run is resolved after its loop, together with the last
-    // one (both pair exchanges in flight at once, none stalls the tile loop)
-    int64_t first_row = -1;
-    double first_val = 0.0;
+    // ---- calibration state (see "row runs" below) ----
+    const int64_t KT = a.chunk_tiles;
+    int64_t run_row = -1;    // the current run of equal rows ...
+    double run_val = 0.0;    // ... its partial inside the current chunk
+    int64_t run_item = -1;   // >= 0: the run is its chunk's first run (that item)
+    bool outer_has = false;  // a two-item run whose other part ends the previous chunk
+    double outer_val = 0.0;
+    // items deferred to the end of the warp, when their pair exchange with a
+    // neighbouring warp goes out (both in flight at once, none stalls the
+    // loop): {first item, row, value, last item, row, value} in shared memory
+    int64_t* dfl = reinterpret_cast<int64_t*>(smem + a.calib_off) + (size_t)wib * 8;
+    if (lane == 0) dfl[0] = dfl[3] = -1;
+    // run classes of the items of 32 chunks from cb on, two bytes per lane
+    int64_t cb = -64;
+    uint32_t clsv = 0;
+    auto cls_of = [&](int64_t idx) -> uint32_t {  // warp-uniform
+      const int64_t q = idx >> 1;
+      if (q < cb || q >= cb + 32) {
+        cb = q;
+        const int64_t qq = q + lane;
+        clsv = qq < a.nchunks ? *reinterpret_cast<const uint16_t*>(a.item_cls + 2 * qq) : 0u;
+      }
+      const uint32_t v = __shfl_sync(kFull, clsv, (int)(q - cb));
+      return (idx & 1) ? (v >> 8) & 0xffu : v & 0xffu;
+    };
     uint32_t tpv = 0, tpv_next = 0;
     int64_t eov = 0;
     int s = 0;
@@ -365,6 +383,59 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
       } else {
   #pragma unroll
         for (int u = 0; u < CH; ++u) xv[u] = ld_keep(a.x + sc[u * 32 + lane], pol_x);
+      }
+    };
+    // a final row; item 0's row goes through write_run (a shard's first row
+    // may be owned upstream: its partial is sent instead)
+    auto put_row = [&](int64_t idx, int64_t row, double v) {
+      if (lane != 0) return;
+      if (idx == 0 && !a.first_owned)
+        write_run(row, v, a.y, a.first_row, a.first_owned, a.send, a.send_flag, a.send_epoch,
+                  a.mir);
+      else
+        put_y(row, v);
+    };
+    auto emit = [&](int64_t idx, int64_t row, double v, bool warp_edge) {  // warp-uniform
+      const uint32_t c = a.atomic ? 2u : cls_of(idx);
+      if ((c & 3u) == 2u) {  // three or more items (or atomic mode)
+        resolve_item_warp(a, idx, row, v, lane);
+      } else if ((c & 3u) == 0u) {  // the only item: final
+        put_row(idx, row, v);
+      } else if (warp_edge) {  // pair with the neighbouring warp: at the end
+        if (lane == 0) {
+          int64_t* d = dfl + ((c & 4u) ? 3 : 0);
+          d[0] = idx;
+          d[1] = row;
+          d[2] = __double_as_longlong(v);
+        }
+      } else {  // pair inside the warp: folded by the caller (outer)
+        outer_has = true;
+        outer_val = v;
+      }
+    };
+    // the current run ends inside its chunk (its row does not continue)
+    auto close_run = [&]() {
+      if (run_item < 0) {  // started and ended inside the chunk: final
+        if (lane == 0) put_y(run_row, run_val);
+      } else if (outer_has) {  // the second item of an in-warp pair
+        outer_has = false;
+        put_row(run_item, run_row, outer_val + run_val);
+      } else {
+        emit(run_item, run_row, run_val, true);
+      }
+    };
+    // chunk q ended; the current run is its last run (item 2q+1)
+    auto end_chunk = [&](int64_t q, bool next_in_warp) {
+      const int64_t il = 2 * q + 1;
+      if (run_item >= 0) {  // the whole chunk is one row: items 2q (value) and 2q+1 (0.0)
+        if (!a.atomic && (cls_of(il) & 3u) == 1u) {  // exactly these two items: final
+          put_row(run_item, run_row, run_val + 0.0);
+        } else {
+          emit(run_item, run_row, run_val, true);
+          emit(il, run_row, 0.0, true);
+        }
+      } else {
+        emit(il, run_row, run_val, !next_in_warp);
       }
     };
     double xa[CH];
@@ -592,74 +663,61 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
       }
       __syncwarp();  // closed[] is rewritten by the next tile
 
-      // ---- row runs across the warp's consecutive tiles ----
-      auto flush = [&]() {  // warp-uniform
-        if (pend_first) {
-          first_row = pend_row;
-          first_val = pend_val;
-        } else if (lane == 0) {
-          put_y(pend_row, pend_val);
-        }
-      };
-      if (k == kb) {
-        pend_row = tile_row;
-        pend_val = c0;
-        pend_first = true;
-      } else if (tile_row == pend_row) {
-        pend_val += c0;
+      // ---- row runs: chunk-canonical calibration ----
+      // The tiles form fixed chunks of KT tiles (a function of the matrix
+      // alone); warp ranges and shard edges are whole chunks.  A row's value
+      // is canonical, whatever the partition: the partials of its tiles are
+      // folded in tile order inside each chunk, giving one item per chunk
+      // edge it touches (items 2q / 2q+1: chunk q's first / last run); one
+      // item is the value, two are added (a + b, either order), three or more
+      // (rows spanning whole chunks) are summed by resolve_item's fixed order.
+      const bool chunk_start = k == kb || k % KT == 0;
+      if (chunk_start) {
+        if (k > kb) end_chunk(k / KT - 1, true);
+        run_row = tile_row;
+        run_val = c0;
+        run_item = 2 * (k / KT);
+      } else if (tile_row == run_row) {
+        run_val += c0;
       } else {
-        flush();
-        pend_row = tile_row;
-        pend_val = c0;
-        pend_first = false;
+        close_run();
+        run_row = tile_row;
+        run_val = c0;
+        run_item = -1;
       }
       if (H >= 2) {
-        flush();
-        pend_row = rL;
-        pend_val = cL;
-        pend_first = false;
+        close_run();
+        run_row = rL;
+        run_val = cL;
+        run_item = -1;
       }
     }
     if (a.stream_only) return;  // profiling knobs: no rows were produced
-    const int64_t i0 = 2 * (int64_t)w, i1 = i0 + 1;
-    const int64_t r0 = pend_first ? pend_row : first_row;
-    const double v0 = pend_first ? pend_val : first_val;
-    const double v1 = pend_first ? 0.0 : pend_val;
-    const bool short_runs = !a.atomic && a.run_last[i0] - a.run_first[i0] <= 1 &&
-                            a.run_last[i1] - a.run_first[i1] <= 1;
-    if (short_runs) {
-      // both runs hold one or two partials: lane 0 issues both exchanges, then
-      // finishes whichever it completed
-      if (lane == 0) {
-        const int s0 = a.run_first[i0], e0 = a.run_last[i0];
-        const int s1 = a.run_first[i1], e1 = a.run_last[i1];
-        unsigned long long o0 = 0, o1 = 0;
-        if (e0 > s0)
-          o0 = atomicExch(reinterpret_cast<unsigned long long*>(a.item_val + s0),
-                          (unsigned long long)__double_as_longlong(exchangeable(v0)));
-        if (e1 > s1)
-          o1 = atomicExch(reinterpret_cast<unsigned long long*>(a.item_val + s1),
-                          (unsigned long long)__double_as_longlong(exchangeable(v1)));
-        if (e0 == s0) {
-          write_run(r0, v0, a.y, a.first_row, a.first_owned, a.send, a.send_flag, a.send_epoch,
-                    a.mir);
-        } else if (o0 != kSlotIdle && !(s1 == s0 && e1 > s1)) {
-          a.item_val[s0] = __longlong_as_double((long long)kSlotIdle);
-          write_run(r0, __longlong_as_double((long long)o0) + v0, a.y, a.first_row,
-                    a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
-        }
-        if (e1 == s1) {
-          write_run(pend_row, v1, a.y, a.first_row, a.first_owned, a.send, a.send_flag,
-                    a.send_epoch, a.mir);
-        } else if (o1 != kSlotIdle) {
-          a.item_val[s1] = __longlong_as_double((long long)kSlotIdle);
-          write_run(pend_row, __longlong_as_double((long long)o1) + v1, a.y, a.first_row,
-                    a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
-        }
+    if (ke > kb) end_chunk((ke - 1) / KT, false);
+    // the pair exchanges with the neighbouring warps (atomic mode resolved
+    // every item already)
+    __syncwarp();
+    const int64_t dfi = dfl[0], dli = dfl[3];
+    if (lane == 0 && (dfi >= 0 || dli >= 0)) {
+      const int64_t dfr = dfl[1], dlr = dfl[4];
+      const double dfv = __longlong_as_double(dfl[2]), dlv = __longlong_as_double(dfl[5]);
+      unsigned long long of = 0, ol = 0;
+      if (dfi >= 0)  // the second item of a pair exchanges on the first's slot
+        of = atomicExch(reinterpret_cast<unsigned long long*>(a.item_val + dfi - 1),
+                        (unsigned long long)__double_as_longlong(exchangeable(dfv)));
+      if (dli >= 0)
+        ol = atomicExch(reinterpret_cast<unsigned long long*>(a.item_val + dli),
+                        (unsigned long long)__double_as_longlong(exchangeable(dlv)));
+      if (dfi >= 0 && of != kSlotIdle) {
+        a.item_val[dfi - 1] = __longlong_as_double((long long)kSlotIdle);
+        write_run(dfr, __longlong_as_double((long long)of) + dfv, a.y, a.first_row,
+                  a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
       }
-    } else {
-      resolve_item_warp(a, i0, r0, v0, lane);
-      resolve_item_warp(a, i1, pend_row, v1, lane);
+      if (dli >= 0 && ol != kSlotIdle) {
+        a.item_val[dli] = __longlong_as_double((long long)kSlotIdle);
+        write_run(dlr, __longlong_as_double((long long)ol) + dlv, a.y, a.first_row,
+                  a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
+      }
     }
   }
 }

@@ -39,15 +39,63 @@ import numpy as np
 from ._lib import IPC_HANDLE_BYTES, check, lib
 
 
-def plan_tiles(pc: int, world: int) -> list[tuple[int, int]]:
-    """Contiguous equal-tile ranges (CSR5 tiles are equal-nnz work units)."""
-    return [(g * pc // world, (g + 1) * pc // world) for g in range(world)]
+def chunk_tiles(pc: int) -> int:
+    """Tiles per calibration chunk (csr5g_chunk_tiles: max(1, pc >> 16)).
+    Deterministic mode folds a row's partials per chunk, so shard edges are
+    chunk edges and y does not depend on the number of shards."""
+    return max(1, pc >> 16)
+
+
+def plan_tiles(pc: int, world: int, row_ptr=None, B: int | None = None) -> list[tuple[int, int]]:
+    """Contiguous equal ranges of whole chunks (CSR5 tiles are equal-nnz work
+    units; a chunk is chunk_tiles(pc) of them).
+
+    With the matrix's row_ptr (numpy or torch) and the tile size B, an edge
+    whose row would bring three or more chunk partials from both sides (a row
+    covering a whole chunk next to the edge) moves to the row's first chunk,
+    so every row split by a shard edge gets exactly one partial from each side
+    and the fix-up's a + b is the single-device sum bit for bit."""
+    k = chunk_tiles(pc)
+    nch = -(-pc // k)
+    edges = [g * nch // world for g in range(world + 1)]
+    if row_ptr is not None and B and world > 1:
+        step = k * B
+        for g in range(1, world):
+            c = edges[g]
+            for _ in range(64):
+                if c <= edges[g - 1] or c >= nch:
+                    break
+                r = _row_of(row_ptr, c * step)
+                lo, hi = _at(row_ptr, r), _at(row_ptr, r + 1)
+                if lo == c * step:
+                    break  # the row starts at the edge: nothing of it on the left
+                if lo > (c - 1) * step and hi < (c + 1) * step:
+                    break  # the edge row touches one chunk on each side
+                c = lo // step  # start the shard at the row's first chunk
+            edges[g] = max(edges[g - 1], min(c, nch))
+    return [(min(edges[g] * k, pc), min(edges[g + 1] * k, pc)) for g in range(world)]
+
+
+def _at(row_ptr, i: int) -> int:
+    return int(row_ptr[i])
+
+
+def _row_of(row_ptr, g: int) -> int:
+    """format.cpp:42-50 row_of_nonzero on a host or device row_ptr."""
+    m = len(row_ptr) - 1
+    if type(row_ptr).__module__.startswith("torch"):
+        import torch
+        r = int(torch.searchsorted(row_ptr, torch.tensor([g], dtype=row_ptr.dtype,
+                                                          device=row_ptr.device), right=True)) - 1
+    else:
+        r = int(np.searchsorted(row_ptr, g, side="right")) - 1
+    return min(max(r, 0), max(m - 1, 0))
 
 
 def effective_world(pc: int, world: int) -> int:
-    """Ranks that hold at least one tile (a matrix smaller than the box uses
+    """Ranks that hold at least one chunk (a matrix smaller than the box uses
     fewer shards; the extra ranks hold nothing)."""
-    return max(1, min(world, pc))
+    return max(1, min(world, -(-pc // chunk_tiles(pc))))
 
 
 @dataclass
@@ -61,13 +109,13 @@ class ShardView:
     pos_end: int    # one past the last
 
 
-def shard_view(nnz: int, sigma: int, rank: int, world: int) -> ShardView | None:
+def shard_view(nnz: int, sigma: int, rank: int, world: int, row_ptr=None) -> ShardView | None:
     B = 32 * sigma
     pc = nnz // B
     w = effective_world(pc, world)
     if rank >= w:
         return None
-    tb, te = plan_tiles(pc, w)[rank]
+    tb, te = plan_tiles(pc, w, row_ptr, B)[rank]
     last = te == pc
     return ShardView(tb, te, last and nnz % B > 0, tb * B, nnz if last else te * B)
 
@@ -163,7 +211,7 @@ class Csr5Sharded:
         self.torch, self.dist, self.group = torch, dist, group
         self.rank, self.world = rank, world
         self.m, self.n, self.nnz, self.sigma = m, n, nnz, sigma
-        view = shard_view(nnz, sigma, rank, world)
+        view = shard_view(nnz, sigma, rank, world, row_ptr)
         self.active = view is not None
         self.world_eff = effective_world(nnz // (32 * sigma), world)
         dev = row_ptr.device
@@ -257,8 +305,8 @@ class Csr5Sharded:
             self.mailbox = None
 
     @staticmethod
-    def slices_for(nnz: int, sigma: int, rank: int, world: int):
-        v = shard_view(nnz, sigma, rank, world)
+    def slices_for(nnz: int, sigma: int, rank: int, world: int, row_ptr=None):
+        v = shard_view(nnz, sigma, rank, world, row_ptr)
         return (0, 0) if v is None else (v.pos_begin, v.pos_end)
 
     def spmv(self, x, y, events=None):
@@ -372,7 +420,7 @@ def _shards_on_device(a, sigma: int, world: int):
     out = []
     w = effective_world(a.nnz // (32 * sigma), world)
     for g in range(w):
-        v = shard_view(a.nnz, sigma, g, w)
+        v = shard_view(a.nnz, sigma, g, w, a.row_ptr)
         out.append(csr_to_csr5_shard(rp, col[v.pos_begin:], val[v.pos_begin:], a.m, a.n, a.nnz,
                                      TuningParams(sigma=sigma), v.tile_begin, v.tile_end,
                                      v.with_tail))

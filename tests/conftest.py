@@ -55,3 +55,22 @@ def edges():
     import json
     with open(os.path.join(ROOT, "tests", "golden", "ref_edges.json")) as f:
         return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def cpp_build(tmp_path_factory):
+    """The C++ drop-in test programs (tests/cpp) configured through
+    find_package(csr5) and built; returns the build directory."""
+    import shutil
+    if not shutil.which("cmake"):
+        pytest.skip("cmake not on PATH")
+    if not os.path.exists(os.path.join(ROOT, "paper_1503_05032_b200", "libcsr5g.so")):
+        subprocess.run(["make", "-C", ROOT, "lib"], check=True)
+    bdir = str(tmp_path_factory.mktemp("csr5pkg") / "cpp")
+    gen = ["-G", "Ninja"] if shutil.which("ninja") else []
+    subprocess.run(["cmake", "-S", os.path.join(ROOT, "tests", "cpp"), "-B", bdir,
+                    f"-Dcsr5_DIR={os.path.join(ROOT, 'cmake')}", *gen],
+                   check=True, capture_output=True, text=True)
+    r = subprocess.run(["cmake", "--build", bdir, "-j", "4"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    return bdir

@@ -3,11 +3,14 @@
 Run in the build container (needs oracle/_ref/libcsr5ref.so, which is built from
 /root/reference/proj/core/src by oracle/Makefile):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py            # everything
+    python tests/golden/make_golden.py --dumps    # ref_dumps.json.gz only
 
 Writes tests/golden/ref_w32.npz (reference csr_to_csr5 arrays and deterministic
 spmv_csr5 y at omega=32 over a sigma sweep) and tests/golden/ref_edges.json
-(the edge-case metadata dumps listed in SURVEY.md section 8c).  Inputs are
+(the edge-case metadata dumps listed in SURVEY.md section 8c), and
+tests/golden/ref_dumps.json.gz (the reference's dump_format text of every
+ref_w32 case, format.cpp:267-305).  Inputs are
 stored alongside the outputs so the fixtures do not depend on any generator.
 """
 import json
@@ -108,5 +111,25 @@ def main():
     print(f"wrote {len(meta)} w32 cases, {len(edges)} edge dumps")
 
 
+def dumps():
+    """dump_format of the reference's build of every golden case, keyed like
+    ref_w32.npz (the inputs are read back from it)."""
+    import gzip
+    r = Ref()
+    z = np.load(os.path.join(HERE, "ref_w32.npz"))
+    meta = json.loads(str(z["meta"]))
+    out = {}
+    for c in meta:
+        mk = c["mat"]
+        a = Csr(c["m"], c["n"], z[f"{mk}_row_ptr"], z[f"{mk}_col_idx"].astype(np.int64),
+                z[f"{mk}_val"])
+        out[c["key"]] = r.dump_format(a, 32, c["sigma"])
+    with gzip.open(os.path.join(HERE, "ref_dumps.json.gz"), "wt") as f:
+        json.dump(out, f)
+    print(f"wrote {len(out)} reference dumps")
+
+
 if __name__ == "__main__":
-    main()
+    if "--dumps" not in sys.argv:
+        main()
+    dumps()

@@ -32,7 +32,7 @@ def _free_port() -> int:
 def emulate_shard(row_ptr, col, val, x, m, nnz, sigma, rank, world):
     """CPU restatement of one shard's csr5g_spmv + send record (test side)."""
     B = 32 * sigma
-    v = mg.shard_view(nnz, sigma, rank, world)
+    v = mg.shard_view(nnz, sigma, rank, world, row_ptr)
     pc = nnz // B
     lo, hi = v.pos_begin, v.pos_end
     first_row = int(np.searchsorted(row_ptr, lo, side="right") - 1)
@@ -123,13 +123,20 @@ def _case(orc, kind, m, n, nnz, seed, frac, sigma, iters=2):
 
 
 def test_plan_tiles_partition():
-    for pc in (0, 1, 7, 100, 514517):
+    import ctypes as C
+
+    from paper_1503_05032_b200._lib import lib
+    for pc in (0, 1, 7, 100, 131071, 131072, 514517, 4130000):
+        k = mg.chunk_tiles(pc)
+        out = C.c_int64()
+        assert lib().csr5g_chunk_tiles(pc, C.byref(out)) == 0 and out.value == k  # the C rule
         for w in (1, 2, 3, 8):
             r = mg.plan_tiles(pc, w)
             assert r[0][0] == 0 and r[-1][1] == pc
             assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+            assert all(b0 % k == 0 for b0, _ in r)  # shard edges are chunk edges
             sizes = [b - a for a, b in r]
-            assert max(sizes) - min(sizes) <= 1
+            assert max(sizes) - min(sizes) <= k
     assert mg.effective_world(3, 8) == 3 and mg.effective_world(0, 8) == 1
 
 
