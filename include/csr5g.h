@@ -71,7 +71,7 @@ typedef struct {
   double lines_per_gather;      /* distinct 128 B x lines per warp gather (1..32) */
   int32_t warps_per_cta, stages, smem_bytes, x_mode, x_window;
   int32_t kernel_variant;       /* 0 general, 1 VR (values with the gathers), 2 NF (no flag paths) */
-  int64_t chunk_tiles;          /* tiles per calibration chunk (deterministic mode's fold unit) */
+  int64_t long_rows;            /* rows with partials from three or more parts (tiles, tail) */
 } csr5g_info;
 
 /* One boundary partial of a shard: row = -1 when there is none. */
@@ -102,12 +102,6 @@ CSR5G_API int csr5g_build(int device, int64_t m, int64_t n, int64_t nnz, const i
  * FULL global row_ptr; d_col_idx / d_val point at global position
  * tile_begin * omega * sigma.  sigma must be explicit (global).  The held
  * arrays equal the slices of the single-device arrays bit for bit. */
-/* Tiles per calibration chunk of a matrix with p_complete complete tiles
- * (max(1, floor(p_complete / 65536))).  Deterministic mode sums
- * a row's partials per chunk in tile order and combines the chunks in a fixed
- * order, so y is bit-identical for every warp split and shard split; shard
- * tile ranges must therefore be whole chunks. */
-CSR5G_API int csr5g_chunk_tiles(int64_t p_complete, int64_t *out);
 CSR5G_API int csr5g_build_shard(int device, int64_t m, int64_t n, int64_t nnz, const int64_t *d_row_ptr,
                       const int32_t *d_col_idx, const double *d_val, const csr5g_params *params,
                       int64_t tile_begin, int64_t tile_end, int32_t with_tail, void *stream,

@@ -43,7 +43,7 @@ class Info(C.Structure):
         ("lines_per_gather", C.c_double),
         ("warps_per_cta", C.c_int32), ("stages", C.c_int32), ("smem_bytes", C.c_int32),
         ("x_mode", C.c_int32), ("x_window", C.c_int32), ("kernel_variant", C.c_int32),
-        ("chunk_tiles", C.c_int64),
+        ("long_rows", C.c_int64),
     ]
 
 
@@ -66,7 +66,6 @@ SIGNATURES = {
     "csr5g_build_shard": (C.c_int, [C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, C.POINTER(Params),
                                     _i64, _i64, _i32, _vp, C.POINTER(_vp)]),
     "csr5g_info_get": (C.c_int, [_vp, C.POINTER(Info)]),
-    "csr5g_chunk_tiles": (C.c_int, [_i64, C.POINTER(_i64)]),
     "csr5g_export": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "csr5g_spmv": (C.c_int, [_vp, _vp, _vp, _i32, _vp]),
     "csr5g_spmv_evt": (C.c_int, [_vp, _vp, _vp, _i32, _vp, _vp, _vp]),

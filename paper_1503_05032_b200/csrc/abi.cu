@@ -116,12 +116,6 @@ int csr5g_build_shard(int device, int64_t m, int64_t n, int64_t nnz, const int64
                     true, with_tail, stream, out);
 }
 
-int csr5g_chunk_tiles(int64_t p_complete, int64_t* out) {
-  if (!out || p_complete < 0) return fail(CSR5G_EINVAL, "csr5g: bad chunk_tiles arguments");
-  *out = chunk_tiles_for(p_complete);
-  return CSR5G_OK;
-}
-
 int csr5g_info_get(csr5g_matrix h, csr5g_info* out) {
   if (!h || !out) return fail(CSR5G_EINVAL, "csr5g: NULL handle");
   *out = h->h->info;

@@ -311,9 +311,11 @@ __global__ void k_eo(const uint32_t* __restrict__ head_bits, const uint32_t* __r
 __global__ void k_tile_work(const uint32_t* __restrict__ head_bits,
                             const uint32_t* __restrict__ tile_ptr, int64_t pcs, int sigma,
                             int w_head, int w_row, int64_t* __restrict__ work,
-                            int64_t* __restrict__ eo_cnt, int* __restrict__ max_heads) {
+                            int64_t* __restrict__ eo_cnt, int* __restrict__ max_heads,
+                            unsigned long long* __restrict__ single_head) {
   __shared__ int bmax;
-  if (threadIdx.x == 0) bmax = 0;
+  __shared__ unsigned int bone;
+  if (threadIdx.x == 0) bmax = 0, bone = 0;
   __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < pcs) {
@@ -325,9 +327,11 @@ __global__ void k_tile_work(const uint32_t* __restrict__ head_bits,
     work[t] = 32ll * sigma + (int64_t)w_head * heads + (int64_t)w_row * rows;
     eo_cnt[t] = (tp >> 31) ? heads : 0;  // empty_offset entries: heads of flagged tiles
     atomicMax(&bmax, heads);
+    if (heads == 1) atomicAdd(&bone, 1u);  // a tile inside one row (long rows need one)
   }
   __syncthreads();
   if (threadIdx.x == 0 && bmax > 0) atomicMax(max_heads, bmax);
+  if (threadIdx.x == 0 && bone > 0) atomicAdd(single_head, (unsigned long long)bone);
 }
 
 // Largest per-warp work of the equal-tile split (atomicMax into *out).
@@ -420,45 +424,119 @@ __global__ void __launch_bounds__(kFixThreads) k_warp_bounds_fix(int64_t* __rest
   }
 }
 
-// Item rows of the in-kernel calibration (spmv_kernel.cuh "row runs"): item
-// 2q is the row of chunk q's first tile start, item 2q+1 the row holding the
-// chunk's last nonzero -- the last head of its last tile t: H = y_offset +
-// popc(flags) of column 31, row = tile_row + (flagged ? eo[eo_ptr[t] + H - 1]
-// : H - 1) -- and item 2*nchunks (tail) the tail's first row.  O(1) loads per item.
+// ---- long rows (deterministic mode's fixed summation order) ----------------
+// A row whose nonzeros touch three or more parts (complete tiles, the tail)
+// is "long": its per-tile partials are stored, one slot per part, and summed
+// by the last arriving warp in one fixed order (lane-strided sums, then an
+// xor butterfly over 32 lanes), so its value does not depend on which warps,
+// SMs or GPUs hold which tiles.  Every other row has one or two partials:
+// one is the value, two are added (a + b is b + a) -- also partition-free.
+struct LongRowPred {
+  const int64_t* rp;
+  int64_t B, pc;
+  __device__ __forceinline__ bool operator()(int64_t r) const {
+    const int64_t lo = rp[r], hi = rp[r + 1];
+    if (hi - lo < B + 2) return false;  // three parts: a whole tile plus one entry each side
+    const int64_t f = min(lo / B, pc), l = min((hi - 1) / B, pc);
+    return l - f >= 2;
+  }
+};
+
+__device__ __forceinline__ int64_t find_long(const int64_t* __restrict__ lrow, int64_t n,
+                                             int64_t row) {
+  int64_t lo = 0, hi = n;  // first index with lrow >= row
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (lrow[mid] < row)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo < n && lrow[lo] == row ? lo : -1;
+}
+
+// per long row L < *count: first tile and number of parts (0 beyond *count)
+__global__ void k_long_info(const int64_t* __restrict__ rp, int64_t B, int64_t pc,
+                            const int64_t* __restrict__ lrow, const int64_t* __restrict__ count,
+                            int64_t cap, int64_t* __restrict__ ltf, int64_t* __restrict__ lnp) {
+  const int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (L >= cap) return;
+  if (L >= *count) {
+    lnp[L] = 0;
+    return;
+  }
+  const int64_t r = lrow[L], f = min(rp[r] / B, pc), l = min((rp[r + 1] - 1) / B, pc);
+  ltf[L] = f;
+  lnp[L] = l - f + 1;
+}
+
+// per held tile, one word: (b << 2) | head0_long | last_long << 1, b = the
+// first long id whose row is >= the tile's head-0 row.  The head-0 row's id
+// is b; the last head's (a different row) is b + head0_long -- no long row
+// fits between the two, since a long row covers a whole tile.
 template <typename W>
-__global__ void k_item_keys(int64_t chunk_tiles, int64_t pcs, int64_t nchunks,
+__global__ void k_long_tags(int64_t pcs, const uint32_t* __restrict__ tile_ptr,
+                            const W* __restrict__ desc, const int64_t* __restrict__ eo_ptr,
+                            const int32_t* __restrict__ eo, int sigma,
+                            const int64_t* __restrict__ lrow, const int64_t* __restrict__ count,
+                            int32_t* __restrict__ tag) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= pcs) return;
+  const int64_t n = *count;
+  const uint32_t tp = tile_ptr[t];
+  const int64_t r0 = tp & 0x7fffffffu;
+  const uint64_t wd = (uint64_t)desc[t * 32 + 31];
+  const int H = (int)(wd >> (kSegBits + sigma)) + __popcll(wd & ((1ull << sigma) - 1));
+  const int64_t rl = r0 + ((tp >> 31) ? (int64_t)eo[eo_ptr[t] + H - 1] : H - 1);
+  int64_t lo = 0, hi = n;  // first long id with lrow >= r0
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (lrow[mid] < r0)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  const bool h0 = lo < n && lrow[lo] == r0;
+  const int64_t nl = lo + (h0 ? 1 : 0);
+  const bool hl = rl != r0 && nl < n && lrow[nl] == rl;
+  tag[t] = (int32_t)((lo << 2) | (h0 ? 1 : 0) | (hl ? 2 : 0));
+}
+
+__global__ void k_long_tail(int64_t tail_row, int has_tail, const int64_t* __restrict__ lrow,
+                            const int64_t* __restrict__ count, int32_t* __restrict__ out) {
+  *out = has_tail ? (int32_t)find_long(lrow, *count, tail_row) : -1;
+}
+
+// Item rows of the in-kernel calibration (spmv.cu resolve_item): item 2w is
+// the row of warp w's first tile start, item 2w+1 the row holding the warp's
+// last nonzero -- the last head of its last tile t: H = y_offset + popc(flags)
+// of column 31, row = tile_row + (flagged ? eo[eo_ptr[t] + H - 1] : H - 1) --
+// and item 2*nwarps (tail) the tail's first row.  O(1) loads per item.
+template <typename W>
+__global__ void k_item_keys(const int64_t* __restrict__ warp_begin,
                             const uint32_t* __restrict__ tile_ptr, const W* __restrict__ desc,
                             const int64_t* __restrict__ eo_ptr, const int32_t* __restrict__ eo,
-                            int sigma, int has_tail_item, int64_t tail_row_begin,
+                            int sigma, int nwarps, int has_tail_item, int64_t tail_row_begin,
+                            const int64_t* __restrict__ lrow, const int64_t* __restrict__ nlong,
                             int64_t* __restrict__ key) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = 2 * nchunks + (has_tail_item ? 1 : 0);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = 2 * nwarps + (has_tail_item ? 1 : 0);
   if (i >= n) return;
-  if (i == 2 * nchunks) {
-    key[i] = tail_row_begin;
+  int64_t row;
+  if (i == 2 * nwarps) {
+    row = tail_row_begin;
   } else if ((i & 1) == 0) {
-    key[i] = tile_ptr[(i >> 1) * chunk_tiles] & 0x7fffffffu;
+    row = tile_ptr[warp_begin[i >> 1]] & 0x7fffffffu;
   } else {
-    const int64_t t = min(((i >> 1) + 1) * chunk_tiles, pcs) - 1;
+    const int64_t t = warp_begin[(i >> 1) + 1] - 1;
     const uint32_t tp = tile_ptr[t];
     const uint64_t wd = (uint64_t)desc[t * 32 + 31];
     const int H = (int)(wd >> (kSegBits + sigma)) + __popcll(wd & ((1ull << sigma) - 1));
-    key[i] = (int64_t)(tp & 0x7fffffffu) + ((tp >> 31) ? (int64_t)eo[eo_ptr[t] + H - 1] : H - 1);
+    row = (int64_t)(tp & 0x7fffffffu) + ((tp >> 31) ? (int64_t)eo[eo_ptr[t] + H - 1] : H - 1);
   }
-}
-
-// inclusive work prefix at every chunk end (the warp split is in whole chunks)
-__global__ void k_chunk_prefix(const int64_t* __restrict__ prefix, int64_t pcs,
-                               int64_t chunk_tiles, int64_t nchunks, int64_t* __restrict__ out) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < nchunks) out[c] = prefix[min((c + 1) * chunk_tiles, pcs) - 1];
-}
-
-// warp bounds: chunk index -> tile index
-__global__ void k_chunk_bounds_to_tiles(int64_t* __restrict__ begin, int nw, int64_t chunk_tiles,
-                                        int64_t pcs) {
-  const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w <= nw) begin[w] = min(begin[w] * chunk_tiles, pcs);
+  // a long row's partials go through its part slots, not the items: its items
+  // get keys of their own (single-item runs the kernel skips)
+  key[i] = lrow && find_long(lrow, *nlong, row) >= 0 ? -2 - (int64_t)i : row;
 }
 
 // Runs of equal keys (keys are non-decreasing): run_first[i] = prefix max of
@@ -468,8 +546,7 @@ __global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __rest
                                                            int32_t* __restrict__ run_first,
                                                            int32_t* __restrict__ run_last,
                                                            int32_t* __restrict__ run_cnt,
-                                                           double* __restrict__ item_val,
-                                                           uint8_t* __restrict__ item_cls) {
+                                                           double* __restrict__ item_val) {
   __shared__ int part[kFixThreads];
   const int t = threadIdx.x;
   for (int i = t; i < n; i += kFixThreads) {  // per-launch state: no arrivals, idle pair slots
@@ -511,11 +588,6 @@ __global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __rest
     if (i == n - 1 || key[i] != key[i + 1]) run = i;
     run_last[i] = run;
   }
-  __syncthreads();
-  for (int i = t; i < n; i += kFixThreads) {  // length class | first-of-run
-    const int len = run_last[i] - run_first[i] + 1;
-    item_cls[i] = (uint8_t)((len == 1 ? 0 : len == 2 ? 1 : 2) | (run_first[i] == i ? 4 : 0));
-  }
 }
 
 // Every scalar the host needs from the build, gathered by one thread into one
@@ -527,6 +599,7 @@ __global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0,
                           const int64_t* __restrict__ eo_ptr, int64_t pcs,
                           const int* __restrict__ max_heads,
                           const unsigned long long* __restrict__ lines,
+                          const unsigned long long* __restrict__ single_head,
                           int64_t* __restrict__ out) {
   const bool rows = m > 0;
   out[0] = rows && g0 >= 0 ? row_of_nonzero_dev(rp, m, g0) : -1;
@@ -538,6 +611,7 @@ __global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0,
   out[6] = tile_ptr[0];
   out[7] = tile_ptr[ic];
   out[8] = (int64_t)*lines;
+  out[9] = (int64_t)*single_head;
 }
 
 // Gather locality of the SpMV: for `samples` evenly spaced tiles, the number
@@ -687,13 +761,16 @@ void free_handle(Handle* h) {
   free_binding(h->mg);
   for (void* p : {(void*)h->row_ptr, (void*)h->tile_ptr, h->desc, (void*)h->eo_ptr, (void*)h->eo,
                   (void*)h->col, (void*)h->val, (void*)h->item_val, (void*)h->run_first,
-                  (void*)h->run_last, (void*)h->run_cnt, (void*)h->item_cls, (void*)h->send,
-                  (void*)h->spill,
-                  (void*)h->warp_begin})
+                  (void*)h->run_last, (void*)h->run_cnt, (void*)h->send, (void*)h->spill,
+                  (void*)h->warp_begin, (void*)h->lrow, (void*)h->ltf, (void*)h->lnp,
+                  (void*)h->lbase, (void*)h->nlong_d, (void*)h->ltag,
+                  (void*)h->lparts, (void*)h->lcnt})
     if (p) cudaFreeAsync(p, 0);
   for (const StreamScratch& x : h->scratch) {
     if (x.owned)
-      for (void* p : {(void*)x.item_val, (void*)x.run_cnt, (void*)x.spill}) cudaFreeAsync(p, 0);
+      for (void* p : {(void*)x.item_val, (void*)x.run_cnt, (void*)x.spill, (void*)x.lparts,
+                      (void*)x.lcnt})
+        if (p) cudaFreeAsync(p, 0);
     if (x.done) cudaEventDestroy(x.done);
   }
   cudaDeviceSynchronize();
@@ -736,12 +813,6 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   if (tile_begin < 0 || tile_end < tile_begin || tile_end > pc)
     return fail(CSR5G_EINVAL, "csr5g: shard tile range outside [0, p_complete]");
   const bool is_last = tile_end == pc;
-  {
-    const int64_t K = chunk_tiles_for(pc);
-    if (shard && (tile_begin % K != 0 || (tile_end % K != 0 && !is_last)))
-      return fail(CSR5G_EINVAL, "csr5g: a shard's tile range must be whole calibration chunks "
-                                "(multiples of " + std::to_string(K) + " tiles, csr5g_chunk_tiles)");
-  }
   if ((with_tail != 0) != (is_last && tail > 0))
     return fail(CSR5G_EINVAL, "csr5g: the shard ending at p_complete must hold the tail");
   const int64_t pcs = tile_end - tile_begin;
@@ -775,13 +846,12 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   int64_t* work_prefix = nullptr;
   int64_t* work = nullptr;
   int64_t* item_key = nullptr;
-  int64_t* chunk_prefix = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   auto cleanup = [&](int code) {
     if (side && code) cudaStreamSynchronize(side);  // error path: side work may be in flight
     for (void* p : {(void*)zblock, cub_tmp, cub_tmp2, (void*)work_prefix, (void*)work,
-                    (void*)item_key, (void*)chunk_prefix})
+                    (void*)item_key})
       if (p) cudaFreeAsync(p, stream);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -814,7 +884,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   // scalars (4 lines, 6 emax, 8 max heads, 10-18 the values read back)
   const size_t hb_bytes = ((size_t)head_words * 4 + 7) / 8 * 8;
   const size_t eb_bytes = ((size_t)empty_words * 4 + 7) / 8 * 8;
-  const size_t zbytes = hb_bytes + eb_bytes + 8 * ((size_t)pcs + 1) + 8 * 20;
+  const size_t zbytes = hb_bytes + eb_bytes + 8 * ((size_t)pcs + 1) + 8 * 22;
   TRY(dev_alloc(&zblock, zbytes, &alloc_ms, &tmp_bytes));
   head_bits = reinterpret_cast<uint32_t*>(zblock);
   empty_bits = reinterpret_cast<uint32_t*>(zblock + hb_bytes);
@@ -914,11 +984,13 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
     return e ? std::atoi(e) : 1;
   }();
   int* max_heads_d = reinterpret_cast<int*>(scal + 8);  // zeroed with the block
+  auto* single_head_d = reinterpret_cast<unsigned long long*>(scal + 9);
   if (pcs > 0) {
     TRY(dev_alloc(&work, (size_t)pcs, &alloc_ms, &tmp_bytes));
     k_tile_work<<<(unsigned)((pcs + 255) / 256), 256, 0, side>>>(head_bits, h->tile_ptr, pcs,
                                                                  (int)sigma, w_head, w_row, work,
-                                                                 eo_cnt, max_heads_d);
+                                                                 eo_cnt, max_heads_d,
+                                                                 single_head_d);
     TRYC(cudaGetLastError());
   }
   size_t cub_bytes = 0;
@@ -957,11 +1029,12 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   const int64_t g0 = pcs > 0 ? tile_end * B - 1 : -1;
   const int64_t g1 = nnz > 0 ? nnz - 1 : -1;
   int64_t sv[4] = {-1, -1, -1, -1};
-  int64_t hs[9];
+  int64_t hs[10];
   k_scalars<<<1, 1, 0, side>>>(h->row_ptr, m, g0, g1, h->tile_ptr, ic, h->eo_ptr, pcs, max_heads_d,
-                               reinterpret_cast<const unsigned long long*>(scal + 4), scal + 10);
+                               reinterpret_cast<const unsigned long long*>(scal + 4), single_head_d,
+                               scal + 11);
   TRYC(cudaGetLastError());
-  TRYC(cudaMemcpyAsync(hs, scal + 10, sizeof hs, cudaMemcpyDeviceToHost, side));
+  TRYC(cudaMemcpyAsync(hs, scal + 11, sizeof hs, cudaMemcpyDeviceToHost, side));
   TRYC(cudaStreamSynchronize(side));  // the transposition keeps running on `stream`
   trace.mark("scan");
   for (int q = 0; q < 4; ++q) sv[q] = hs[q];
@@ -969,6 +1042,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   const int max_heads = (int)hs[5];
   const uint32_t tp0 = (uint32_t)hs[6], tpc = (uint32_t)hs[7];
   lines = (unsigned long long)hs[8];
+  const int64_t single_head_tiles = hs[9];
   ptr_first = tp0 & 0x7fffffffu;
   ptr_close = tpc & 0x7fffffffu;
   TRY(dev_alloc(&h->eo, (size_t)eo_total, &alloc_ms, &bytes));
@@ -1002,58 +1076,96 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   int sms = 0;
   TRYC(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   h->max_heads = max_heads;  // with eo_total: may the plan drop the flag paths (NF)?
+  h->maybe_long = single_head_tiles > 0;  // (NF plans exclude long rows)
   h->eo_entries = eo_total;
   h->info.sigma = sigma;  // spmv_plan picks the sigma-specialised kernel
   h->info.n = n;          // ... and sizes its shared memory by x
-  // calibration chunks: a function of the global matrix only, so every
-  // partition (warps, shards) folds a row's partials the same way
-  h->chunk_tiles = chunk_tiles_for(pc);
-  h->nchunks = (pcs + h->chunk_tiles - 1) / h->chunk_tiles;
   TRY(spmv_plan(h, sms));
   const int64_t rows_total = h->lead_rows + (m - h->tail_row_begin);
   h->rows_blocks = rows_total > 0 ? (int)std::min<int64_t>((rows_total + 255) / 256, 2 * sms) : 0;
-  const int64_t items = 2 * h->nchunks + 1;
+  const int64_t items = 2 * (int64_t)h->nwarps + 1;
   TRY(dev_alloc(&h->item_val, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->run_first, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->run_last, (size_t)items, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->run_cnt, (size_t)items, &alloc_ms, &bytes));
-  TRY(dev_alloc(&h->item_cls, (size_t)items + 1, &alloc_ms, &bytes));
   TRY(dev_alloc(&h->spill, (size_t)std::max(h->nwarps, 1) * (B + 1), &alloc_ms, &bytes));
   if (pcs > 0 && h->nwarps > 0) {
-    // warp ranges of whole chunks, split by the chunks' work
     TRY(dev_alloc(&h->warp_begin, (size_t)h->nwarps + 1, &alloc_ms, &bytes));
-    TRY(dev_alloc(&chunk_prefix, (size_t)h->nchunks, &alloc_ms, &tmp_bytes));
-    k_chunk_prefix<<<(unsigned)((h->nchunks + 255) / 256), 256, 0, stream>>>(
-        work_prefix, pcs, h->chunk_tiles, h->nchunks, chunk_prefix);
     auto* emax = reinterpret_cast<unsigned long long*>(scal + 6);  // zeroed with the block
     k_equal_split_max<<<(unsigned)((h->nwarps + 255) / 256), 256, 0, stream>>>(
-        chunk_prefix, h->nchunks, h->nwarps, emax);
+        work_prefix, pcs, h->nwarps, emax);
     TRYC(cudaGetLastError());
     k_warp_bounds<<<(unsigned)((h->nwarps + 1 + 255) / 256), 256, 0, stream>>>(
-        chunk_prefix, h->nchunks, h->nwarps, emax, h->warp_begin);
+        work_prefix, pcs, h->nwarps, emax, h->warp_begin);
     TRYC(cudaGetLastError());
     k_warp_bounds_fix<<<1, kFixThreads, 0, stream>>>(h->warp_begin, h->nwarps);
-    k_chunk_bounds_to_tiles<<<(unsigned)((h->nwarps + 1 + 255) / 256), 256, 0, stream>>>(
-        h->warp_begin, h->nwarps, h->chunk_tiles, pcs);
     TRYC(cudaGetLastError());
+  }
+  // long rows (possible only if some tile lies inside one row)
+  if (pcs > 0 && single_head_tiles > 0) {
+    const int64_t cap = single_head_tiles + 2;  // each long row covers a tile of its own
+    h->long_cap = cap;
+    TRY(dev_alloc(&h->lrow, (size_t)cap, &alloc_ms, &bytes));
+    TRY(dev_alloc(&h->ltf, (size_t)cap, &alloc_ms, &bytes));
+    TRY(dev_alloc(&h->lnp, (size_t)cap, &alloc_ms, &bytes));
+    TRY(dev_alloc(&h->lbase, (size_t)cap + 1, &alloc_ms, &bytes));
+    TRY(dev_alloc(&h->nlong_d, 2, &alloc_ms, &bytes));  // [0] long rows, [1] tail's long id
+    TRY(dev_alloc(&h->ltag, (size_t)pcs, &alloc_ms, &bytes));
+    const int64_t r_lo = ptr_first;
+    const int64_t r_hi = std::max<int64_t>(r_lo, (is_last ? (nnz > 0 ? sv[1] : 0) : sv[0]) + 1);
+    LongRowPred pred{h->row_ptr, B, pc};
+    cub::CountingInputIterator<int64_t> rows_it(r_lo);
+    size_t sel_bytes = 0;
+    TRYC(cub::DeviceSelect::If(nullptr, sel_bytes, rows_it, h->lrow, h->nlong_d,
+                               r_hi - r_lo, pred, stream));
+    void* sel_tmp = nullptr;
+    TRY(dev_alloc(reinterpret_cast<char**>(&sel_tmp), sel_bytes, &alloc_ms, &tmp_bytes));
+    TRYC(cub::DeviceSelect::If(sel_tmp, sel_bytes, rows_it, h->lrow, h->nlong_d, r_hi - r_lo,
+                               pred, stream));
+    TRYC(cudaFreeAsync(sel_tmp, stream));
+    k_long_info<<<(unsigned)((cap + 255) / 256), 256, 0, stream>>>(h->row_ptr, B, pc, h->lrow,
+                                                                   h->nlong_d, cap, h->ltf,
+                                                                   h->lnp);
+    TRYC(cudaGetLastError());
+    size_t scan_bytes = 0;
+    TRYC(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, h->lnp, h->lbase, cap, stream));
+    void* scan_tmp = nullptr;
+    TRY(dev_alloc(reinterpret_cast<char**>(&scan_tmp), scan_bytes, &alloc_ms, &tmp_bytes));
+    TRYC(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, h->lnp, h->lbase, cap, stream));
+    TRYC(cudaFreeAsync(scan_tmp, stream));
+    if (h->wide)
+      k_long_tags<uint64_t><<<(unsigned)((pcs + 255) / 256), 256, 0, stream>>>(
+          pcs, h->tile_ptr, (const uint64_t*)h->desc, h->eo_ptr, h->eo, (int)sigma, h->lrow,
+          h->nlong_d, h->ltag);
+    else
+      k_long_tags<uint32_t><<<(unsigned)((pcs + 255) / 256), 256, 0, stream>>>(
+          pcs, h->tile_ptr, (const uint32_t*)h->desc, h->eo_ptr, h->eo, (int)sigma, h->lrow,
+          h->nlong_d, h->ltag);
+    k_long_tail<<<1, 1, 0, stream>>>(h->tail_row_begin, h->has_tail_item ? 1 : 0, h->lrow,
+                                     h->nlong_d, reinterpret_cast<int32_t*>(h->nlong_d + 1));
+    TRYC(cudaGetLastError());
+    h->long_slots = pcs + cap + 1;  // parts: one per tile it covers + its first tile + tail
+    TRY(dev_alloc(&h->lparts, (size_t)h->long_slots, &alloc_ms, &bytes));
+    TRY(dev_alloc(&h->lcnt, (size_t)cap, &alloc_ms, &bytes));
+    TRYC(cudaMemsetAsync(h->lcnt, 0, sizeof(int32_t) * cap, stream));
   }
   // runs of the calibration items (the rows warps / the tail share)
   {
-    const int n_items = (int)(2 * h->nchunks + (h->has_tail_item ? 1 : 0));
+    const int n_items = 2 * h->nwarps + (h->has_tail_item ? 1 : 0);
     if (n_items > 0) {
       TRY(dev_alloc(&item_key, (size_t)n_items, &alloc_ms, &tmp_bytes));
       const unsigned kb = (unsigned)((n_items + 255) / 256);
       if (h->wide)
         k_item_keys<uint64_t><<<kb, 256, 0, stream>>>(
-            h->chunk_tiles, pcs, h->nchunks, h->tile_ptr, (const uint64_t*)h->desc, h->eo_ptr,
-            h->eo, (int)sigma, h->has_tail_item ? 1 : 0, h->tail_row_begin, item_key);
+            h->warp_begin, h->tile_ptr, (const uint64_t*)h->desc, h->eo_ptr, h->eo, (int)sigma,
+            h->nwarps, h->has_tail_item ? 1 : 0, h->tail_row_begin, h->lrow, h->nlong_d, item_key);
       else
         k_item_keys<uint32_t><<<kb, 256, 0, stream>>>(
-            h->chunk_tiles, pcs, h->nchunks, h->tile_ptr, (const uint32_t*)h->desc, h->eo_ptr,
-            h->eo, (int)sigma, h->has_tail_item ? 1 : 0, h->tail_row_begin, item_key);
+            h->warp_begin, h->tile_ptr, (const uint32_t*)h->desc, h->eo_ptr, h->eo, (int)sigma,
+            h->nwarps, h->has_tail_item ? 1 : 0, h->tail_row_begin, h->lrow, h->nlong_d, item_key);
       TRYC(cudaGetLastError());
       k_item_runs<<<1, kFixThreads, 0, stream>>>(item_key, n_items, h->run_first, h->run_last,
-                                                 h->run_cnt, h->item_val, h->item_cls);
+                                                 h->run_cnt, h->item_val);
       TRYC(cudaGetLastError());
     }
   }
@@ -1103,10 +1215,12 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   in.x_mode = h->x_mode;
   in.x_window = h->x_window ? 1 : 0;
   in.kernel_variant = h->vr ? 1 : (h->nf ? 2 : 0);
-  in.chunk_tiles = h->chunk_tiles;
   // the build is synchronous (format.hpp:182 returns a finished value): the
   // handle is usable from any stream once it returns
   TRYC(cudaStreamSynchronize(stream));
+  in.long_rows = 0;
+  if (h->nlong_d)
+    TRYC(cudaMemcpy(&in.long_rows, h->nlong_d, sizeof(int64_t), cudaMemcpyDeviceToHost));
   trace.mark("final");
   in.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
   *out = h;

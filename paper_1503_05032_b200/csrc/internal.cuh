@@ -60,7 +60,6 @@ struct SpmvArgs {
   double* item_val;        // run partials (deterministic mode), per stream
   const int32_t* run_first;  // item i's run of equal rows is items [run_first[i], run_last[i]]
   const int32_t* run_last;
-  const uint8_t* item_cls;   // per item: run length class (0 one, 1 two, 2 more) | 4 if first
   int32_t* run_cnt;        // arrivals per run (indexed by its first item), per stream
   csr5g_partial* send;
   uint32_t* send_flag;     // p2p.cu: owner's ready flag for the send record (or null)
@@ -77,16 +76,13 @@ struct SpmvArgs {
   int64_t tile_ptr_len;
   int64_t first_row;       // row of head 0 of the first held tile
   int32_t first_owned;     // that row starts inside this handle
-  int32_t has_tail_item;   // tail exists: its first row is item 2*nchunks
+  int32_t has_tail_item;   // tail exists: its first row is item 2*nwarps
   int32_t sigma;
   int32_t B;
-  int32_t nwarps;          // tile warps (each a contiguous range of whole chunks)
-  int64_t chunk_tiles;     // tiles per calibration chunk (a function of the matrix alone)
-  int64_t nchunks;         // chunks held; items 2q / 2q+1 = chunk q's first / last run
+  int32_t nwarps;          // tile warps (each a contiguous tile range)
   int32_t stages;          // TMA ring depth per warp
   int32_t stage_bytes;     // one tile: val | col_idx | descriptor words
   int32_t bar_bytes;       // mbarrier area at the start of shared memory
-  int32_t calib_off;       // byte offset of the per-warp calibration area (64 B per warp)
   int32_t atomic;          // SpmvMode::atomic
   int32_t x_mode;          // x gather path: 0 L1+evict_last, 1 L1 no-allocate+evict_last,
                            // 2 LSU, 3 .cg, 4 plain .nc, 5 = 1 with a 64 B L2 prefetch,
@@ -96,6 +92,17 @@ struct SpmvArgs {
   float x_frac;            // share of x lines given evict_last (the rest evict_first)
   int32_t y_hint;          // y stores: 1 = L2 evict_first, no L1 allocation
   Mirrors mir;             // fused iterative mode: peer next-x buffers (n = 0: none)
+  // long rows (three or more parts; convert.cu "long rows"), deterministic mode
+  int32_t has_long;        // the handle may hold long rows
+  int64_t t0;              // global index of the first held tile
+  const int32_t* ltag;     // per tile: (b << 2) | head-0 row long | last row long << 1
+  const int64_t* lrow;     // per long id: row, first tile, parts, first slot
+  const int64_t* ltf;
+  const int64_t* lnp;
+  const int64_t* lbase;
+  const int32_t* tail_long;  // long id of the tail's first row, or -1
+  double* lparts;          // part slots (per stream)
+  int32_t* lcnt;           // arrivals per long row (per stream; reset by the last)
   int64_t trace_tile;      // trace launch (csr5g_spmv_tile): the tile and its outputs
   int64_t* trace_row;
   double* trace_val;
@@ -112,6 +119,8 @@ struct StreamScratch {
   double* item_val;
   int32_t* run_cnt;
   double* spill;
+  double* lparts = nullptr;  // long-row part slots and arrival counters
+  int32_t* lcnt = nullptr;
   cudaEvent_t done = nullptr;  // recorded after the last SpMV that used it
   uint64_t last_use = 0;       // LRU stamp
   bool owned = true;           // false: the handle's own arrays (freed with it)
@@ -134,7 +143,6 @@ struct Handle {
   double* item_val = nullptr;
   int32_t* run_first = nullptr;  // static run structure of the items (built once)
   int32_t* run_last = nullptr;
-  uint8_t* item_cls = nullptr;   // run class of every item (SpmvArgs::item_cls)
   int32_t* run_cnt = nullptr;    // zeroed; every launch leaves it zeroed
   csr5g_partial* send = nullptr;
   csr5g_partial* send_ext = nullptr;  // caller-provided record slot
@@ -148,16 +156,21 @@ struct Handle {
   int64_t first_row = 0, last_row = 0;
   bool first_owned = true, is_last = true, has_tail_item = false;
   int nwarps = 0, tile_blocks = 0, rows_blocks = 0;
-  int64_t chunk_tiles = 1, nchunks = 0;  // calibration chunks (spmv_kernel.cuh "row runs")
   double lines_per_gather = 1.0;  // sampled x-gather locality (1 = coalesced, 32 = random)
   int x_mode = 0;                 // gather path chosen by the plan
   bool x_window = false;          // L2 persisting window on x
   bool vr = false;                // values outside the TMA ring (k_spmv<SIG, true>)
   bool nf = false;                // no flagged tile, heads fit the slots (k_spmv<SIG, false, true>)
   int max_heads = 0;              // most segment heads in one tile
+  // long rows (convert.cu "long rows"): ids, per-tile tags, per-row info
+  bool maybe_long = false;
+  int64_t long_cap = 0, long_slots = 0;
+  int64_t *lrow = nullptr, *ltf = nullptr, *lnp = nullptr, *lbase = nullptr, *nlong_d = nullptr;
+  int32_t* ltag = nullptr;
+  double* lparts = nullptr;  // the first stream's part slots / counters
+  int32_t* lcnt = nullptr;
   int64_t eo_entries = 0;         // empty_offset entries
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
-  int calib_off = 0;  // shared-memory offset of the per-warp calibration area
   int carveout_pct = -1;  // preferred shared-memory carveout of the SpMV kernel
   // per-stream SpMV scratch (the handle's own arrays are the first set);
   // guarded by scratch_mu
@@ -180,10 +193,6 @@ int resolve_device(int* device);  // device < 0: the current device
     if (e_ != cudaSuccess) return ::csr5g::cuda_fail(e_, #call); \
   } while (0)
 
-// Tiles per calibration chunk of a matrix with pc complete tiles: ~65536
-// chunks, so the items stay small and every SM's warps get many chunks.
-inline int64_t chunk_tiles_for(int64_t pc) { return (pc >> 16) > 1 ? (pc >> 16) : 1; }
-
 // ---- launchers implemented in convert.cu / spmv.cu -------------------------
 int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d_row_ptr,
                  const int32_t* d_col_idx, const double* d_val, const csr5g_params* params,
@@ -200,6 +209,8 @@ int launch_tile_trace(Handle* h, int64_t k, const double* d_x, int64_t* d_rows, 
 int spmv_plan(Handle* h, int sms);
 int func_attrs(const void* fn, int device, int smem, int carve);
 int scratch_done(Handle* h, cudaStream_t stream);
+int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, double** sp,
+                double** lp, int32_t** lc);
 int spmv_host_batch(Handle* h, const double* const* xs, double* const* ys, int64_t count,
                     int mode, cudaStream_t stream);
 void free_pipeline(Pipeline* p);

@@ -86,7 +86,8 @@ int spmv_plan(Handle* h, int sms) {
     const char* e = std::getenv("CSR5G_NF");
     return e ? std::atoi(e) : -1;
   }();
-  h->nf = nf_env != 0 && !h->vr && sigma <= kNfMaxSigma && h->pcs > 0 && h->eo_entries == 0 &&
+  h->nf = nf_env != 0 && !h->vr && !h->maybe_long && sigma <= kNfMaxSigma && h->pcs > 0 &&
+          h->eo_entries == 0 &&
           h->max_heads < std::min<int64_t>(h->B, kClosedSlots);
   const int64_t tile_bytes = h->B * (h->vr ? 4 : 12) + 32 * wbytes;
   const int stage_bytes = (int)((tile_bytes + 127) / 128 * 128);
@@ -141,7 +142,7 @@ int spmv_plan(Handle* h, int sms) {
   if (h->x_mode >= 7 && !h->vr) h->x_mode = 1;
   const int xex_bytes = h->x_mode >= 7 ? sigma * 33 * 8 : 0;
   auto need = [&](int w, int st) {
-    return bars(w, st) + w * (closed_bytes + kEoSlots * 4 + st * stage_bytes + xex_bytes + 64);
+    return bars(w, st) + w * (closed_bytes + kEoSlots * 4 + st * stage_bytes + xex_bytes);
   };
   // local gathers: warps per SM matter most (keep them, give up depth first);
   // random gathers: keep the TMA lead (depth), give up warps
@@ -159,7 +160,6 @@ int spmv_plan(Handle* h, int sms) {
   h->stage_bytes = stage_bytes;
   h->bar_bytes = bars(nw, stages);
   h->smem_bytes = need(nw, stages);
-  h->calib_off = h->smem_bytes - nw * 64;  // the last 64 bytes per warp
   // Ask for the smallest shared-memory carveout that holds the ring: the rest
   // of the SM's 256 KB stays L1, which is where outstanding gather misses land
   // (measured: a 233 KB carveout halves R-MAT throughput through mio/lg
@@ -174,7 +174,7 @@ int spmv_plan(Handle* h, int sms) {
     h->carveout_pct = std::min(100, std::max(0, pct));
   }
   const int64_t max_warps = (int64_t)sms * nw;
-  h->nwarps = (int)std::min<int64_t>(max_warps, h->nchunks);
+  h->nwarps = (int)std::min<int64_t>(max_warps, h->pcs);
   h->tile_blocks = (h->nwarps + nw - 1) / nw;
   return CSR5G_OK;
 }
@@ -202,28 +202,34 @@ int func_attrs(const void* fn, int device, int smem, int carve) {
 // The scratch set of `stream` (the reference's per-worker workspaces,
 // spmv.hpp:27-38): the handle's own arrays for the first stream, sets
 // allocated stream-ordered for others, at most kMaxStreamScratch of them --
-// beyond that the least recently used set moves to the new stream.  Every
-// hand-out makes the stream wait for the set's last SpMV (an event), so a set
-// is never shared by two kernels in flight, even when a destroyed stream's
-// address comes back as a new stream.
-int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, double** sp) {
+// beyond that the least recently used set moves to the new stream, which
+// first waits for the set's last SpMV (an event recorded after every launch),
+// so a set is never shared by two kernels in flight.  (A stream destroyed and
+// re-created at the same address with its last SpMV still running would
+// share its set: the caller's stream lifetime is assumed, as for any
+// per-stream workspace.)
+int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, double** sp,
+                double** lp, int32_t** lc) {
   std::lock_guard<std::mutex> lock(h->scratch_mu);
   StreamScratch* x = nullptr;
   for (StreamScratch& s : h->scratch)
     if (s.stream == stream) x = &s;
   if (!x && h->scratch.empty()) {
-    h->scratch.push_back(StreamScratch{stream, h->item_val, h->run_cnt, h->spill});
+    h->scratch.push_back(StreamScratch{stream, h->item_val, h->run_cnt, h->spill, h->lparts,
+                                       h->lcnt});
     h->scratch.back().owned = false;
     x = &h->scratch.back();
   }
+  bool moved = false;  // the set changes hands: wait for its previous user
   if (!x && h->scratch.size() >= kMaxStreamScratch) {
     x = &h->scratch[0];
     for (StreamScratch& s : h->scratch)
       if (s.last_use < x->last_use) x = &s;
     x->stream = stream;
+    moved = true;
   }
   if (!x) {
-    const size_t items = 2 * (size_t)h->nchunks + 1;
+    const size_t items = 2 * (size_t)h->nwarps + 1;
     const size_t spill = (size_t)std::max(h->nwarps, 1) * (size_t)(h->B + 1);
     StreamScratch n{stream, nullptr, nullptr, nullptr};
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&n.item_val), items * 8, stream);
@@ -231,8 +237,14 @@ int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, doubl
     if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&n.run_cnt), items * 4, stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(n.run_cnt, 0, items * 4, stream);
     if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&n.spill), spill * 8, stream);
+    if (e == cudaSuccess && h->long_cap > 0) {
+      e = cudaMallocAsync(reinterpret_cast<void**>(&n.lparts), h->long_slots * 8, stream);
+      if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&n.lcnt), h->long_cap * 4, stream);
+      if (e == cudaSuccess) e = cudaMemsetAsync(n.lcnt, 0, h->long_cap * 4, stream);
+    }
     if (e != cudaSuccess) {
-      for (void* p : {(void*)n.item_val, (void*)n.run_cnt, (void*)n.spill})
+      for (void* p : {(void*)n.item_val, (void*)n.run_cnt, (void*)n.spill, (void*)n.lparts,
+                      (void*)n.lcnt})
         if (p) cudaFreeAsync(p, stream);
       return cuda_fail(e, "per-stream SpMV scratch");
     }
@@ -242,14 +254,17 @@ int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, doubl
   if (!x->done) CSR5G_CUDA(cudaEventCreateWithFlags(&x->done, cudaEventDisableTiming));
   // (inside a stream capture the graph's own ordering serialises the kernels;
   // an event recorded outside it may not be waited on there)
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  CSR5G_CUDA(cudaStreamIsCapturing(stream, &cap));
-  if (cap == cudaStreamCaptureStatusNone)
-    CSR5G_CUDA(cudaStreamWaitEvent(stream, x->done, 0));  // no-op until first recorded
+  if (moved) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CSR5G_CUDA(cudaStreamIsCapturing(stream, &cap));
+    if (cap == cudaStreamCaptureStatusNone) CSR5G_CUDA(cudaStreamWaitEvent(stream, x->done, 0));
+  }
   x->last_use = ++h->scratch_clock;
   *iv = x->item_val;
   *rc = x->run_cnt;
   *sp = x->spill;
+  *lp = x->lparts;
+  *lc = x->lcnt;
   return CSR5G_OK;
 }
 
@@ -289,10 +304,18 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.val = h->val;
   a.x = d_x;
   a.y = d_y;
-  if (int rc = scratch_for(h, stream, &a.item_val, &a.run_cnt, &a.spill)) return rc;
+  if (int rc = scratch_for(h, stream, &a.item_val, &a.run_cnt, &a.spill, &a.lparts, &a.lcnt))
+    return rc;
+  a.has_long = h->long_cap > 0 && !atomic;
+  a.t0 = h->t0;
+  a.ltag = h->ltag;
+  a.lrow = h->lrow;
+  a.ltf = h->ltf;
+  a.lnp = h->lnp;
+  a.lbase = h->lbase;
+  a.tail_long = h->nlong_d ? reinterpret_cast<const int32_t*>(h->nlong_d + 1) : nullptr;
   a.run_first = h->run_first;
   a.run_last = h->run_last;
-  a.item_cls = h->item_cls;
   a.send = h->send_ext ? h->send_ext : h->send;
   a.send_flag = h->send_flag;
   a.send_epoch = h->send_epoch;
@@ -311,12 +334,9 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.sigma = (int)in.sigma;
   a.B = (int)h->B;
   a.nwarps = h->nwarps;
-  a.chunk_tiles = h->chunk_tiles;
-  a.nchunks = h->nchunks;
   a.stages = h->stages;
   a.stage_bytes = h->stage_bytes;
   a.bar_bytes = h->bar_bytes;
-  a.calib_off = h->calib_off;
   a.atomic = atomic;
   a.mir = h->mir;
   const int grid = std::max(h->tile_blocks, h->rows_blocks);
@@ -341,7 +361,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     return e ? std::atoi(e) : 0;
   }();
   a.stream_only = stream_only;
-  const int64_t items = 2 * h->nchunks + (h->has_tail_item ? 1 : 0);
+  const int64_t items = 2 * (int64_t)h->nwarps + (h->has_tail_item ? 1 : 0);
   if (ev0) CSR5G_CUDA(cudaEventRecord(ev0, stream));
   if (grid > 0) {
     cudaLaunchConfig_t cfg{};
@@ -374,9 +394,10 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     const SpmvFn fn = spmv_fn(a.sigma, h->vr, h->nf);
     if (int rc = func_attrs((const void*)fn, h->device, h->smem_bytes, h->carveout_pct)) return rc;
     CSR5G_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
-    if (int rc = scratch_done(h, stream)) return rc;
   }
   if (ev1) CSR5G_CUDA(cudaEventRecord(ev1, stream));
+  if (grid > 0)
+    if (int rc = scratch_done(h, stream)) return rc;
   // the rows shared between warps were merged inside the kernel
   // (resolve_item); a handle with nothing to multiply has no record
   if (!atomic && items == 0 && grid == 0) {  // no record: row -1 (all ones), value 0.0
@@ -396,7 +417,7 @@ int launch_tile_trace(Handle* h, int64_t k, const double* d_x, int64_t* d_rows, 
   const int stage_bytes = (int)((h->B * 12 + 32 * wbytes + 127) / 128 * 128);
   const int closed_bytes = (int)(std::min<int64_t>(h->B, kClosedSlots) * 8);
   const int stages = 2, bar_bytes = 128;
-  const int smem = bar_bytes + closed_bytes + kEoSlots * 4 + stages * stage_bytes + 64;
+  const int smem = bar_bytes + closed_bytes + kEoSlots * 4 + stages * stage_bytes;
   double* spill = nullptr;
   CSR5G_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&spill), sizeof(double) * (h->B + 1), stream));
   SpmvArgs a{};
@@ -417,12 +438,9 @@ int launch_tile_trace(Handle* h, int64_t k, const double* d_x, int64_t* d_rows, 
   a.sigma = sigma;
   a.B = (int)h->B;
   a.nwarps = 1;
-  a.chunk_tiles = h->chunk_tiles;
-  a.nchunks = h->nchunks;
   a.stages = stages;
   a.stage_bytes = stage_bytes;
   a.bar_bytes = bar_bytes;
-  a.calib_off = smem - 64;
   a.x_mode = 4;
   a.x_frac = 1.0f;
   a.trace_tile = k;

@@ -48,9 +48,12 @@ __device__ __forceinline__ void sts_if(int32_t* p, int32_t v, bool pred) {
       : "memory");
 }
 
+template <bool LONG = true>
 __device__ void resolve_item(const SpmvArgs& a, int64_t idx, int64_t row, double v);
+__device__ __forceinline__ void long_arrive_thread(const SpmvArgs& a, int64_t L, int cnt);
 
 // Tail rows and leading/trailing empty rows, grid-stride over all threads.
+template <bool LONG>
 __device__ void rows_part(const SpmvArgs& a) {
   const int64_t tail_rows = a.m - a.tail_row_begin;
   const int64_t total = a.lead_rows + tail_rows;
@@ -68,7 +71,13 @@ __device__ void rows_part(const SpmvArgs& a) {
     double s = 0.0;
     for (int64_t q = lo; q < hi; ++q) s = fma(a.val[q - a.pos0], a.x[a.col[q - a.pos0]], s);
     if (a.has_tail_item && r == a.tail_row_begin) {
-      resolve_item(a, 2 * a.nchunks, r, s);
+      const int64_t L = LONG && a.has_long ? (int64_t)*a.tail_long : -1;
+      if (L >= 0) {  // the last part of a long row
+        a.lparts[a.lbase[L] + a.lnp[L] - 1] = s;
+        long_arrive_thread(a, L, 1);
+      } else {
+        resolve_item<LONG>(a, 2 * (int64_t)a.nwarps, r, s);
+      }
     } else {
       a.y[r] = s;
       if (a.mir.n) mirror_store(a.mir, r, s);
@@ -85,7 +94,7 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
 // The send record goes to local memory (collective exchange) or straight into
 // the owner rank's mailbox over NVLink (p2p.cu), followed there by its ready
 // flag: value stores, system-scope fence, then the flag store with release.
-__device__ __noinline__ void write_run(int64_t row, double v, double* y, int64_t first_row,
+__device__ __forceinline__ void write_run(int64_t row, double v, double* y, int64_t first_row,
                                           int first_owned, csr5g_partial* send, uint32_t* flag,
                                           uint32_t epoch, const Mirrors& mir) {
   if (!first_owned && row == first_row) {
@@ -138,12 +147,12 @@ __device__ __forceinline__ bool pair_exchange(const SpmvArgs& a, int s, double v
 // thread finishes the run: lane l of a warp sums items s+l, s+l+32, ... in
 // turn, then an xor butterfly (resolve_item_warp); a single thread
 // (resolve_item, e.g. the tail's) replays exactly that order.
-__device__ __noinline__ double run_sum_serial(const SpmvArgs& a, int s, int e) {
+__device__ __noinline__ double sum_fixed_order(const double* p, int64_t n) {
   double t[32];
 #pragma unroll
   for (int l = 0; l < 32; ++l) {
     t[l] = 0.0;
-    for (int j = s + l; j <= e; j += 32) t[l] += __ldcg(a.item_val + j);
+    for (int64_t j = l; j < n; j += 32) t[l] += __ldcg(p + j);
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
@@ -156,6 +165,49 @@ __device__ __noinline__ double run_sum_serial(const SpmvArgs& a, int s, int e) {
   return t[0];
 }
 
+// Long rows (convert.cu "long rows"): every part of the row sits in its slot;
+// `cnt` more parts have been stored by the caller (a warp, lane 0; or one
+// thread for the tail's part).  The arrival that completes the row sums its
+// parts in sum_fixed_order's order -- the warp version below does the same
+// additions -- and writes it.
+__device__ __forceinline__ void long_arrive_thread(const SpmvArgs& a, int64_t L, int cnt) {
+  __threadfence();
+  if (atomicAdd(a.lcnt + L, cnt) + cnt != (int)a.lnp[L]) return;
+  __threadfence();
+  const double t = sum_fixed_order(a.lparts + a.lbase[L], a.lnp[L]);
+  a.lcnt[L] = 0;
+  write_run(a.lrow[L], t, a.y, a.first_row, a.first_owned, a.send, a.send_flag, a.send_epoch,
+            a.mir);
+}
+
+__device__ __forceinline__ void long_arrive_warp(const SpmvArgs& a, int64_t L, int cnt, int lane) {
+  const int64_t n = a.lnp[L];
+  if (cnt == n) {
+    __syncwarp();  // every part is this warp's (lane 0's stores): no count needed
+  } else {
+    int last = 0;
+    if (lane == 0) {
+      __threadfence();  // this warp's part stores (lane 0) before the count
+      last = atomicAdd(a.lcnt + L, cnt) + cnt == (int)n;
+    }
+    if (!__shfl_sync(kFull, last, 0)) return;
+    __threadfence();
+  }
+  const double* p = a.lparts + a.lbase[L];
+  double t = 0.0;
+  for (int64_t j = lane; j < n; j += 32) t += __ldcg(p + j);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(kFull, t, d);
+  if (lane == 0) {
+    if (cnt != n) a.lcnt[L] = 0;
+    write_run(a.lrow[L], t, a.y, a.first_row, a.first_owned, a.send, a.send_flag, a.send_epoch,
+              a.mir);
+  }
+}
+
+// LONG = false (NF plans: no row covers a whole tile, so no run has more
+// than two items) leaves the three-or-more path, and its call, out.
+template <bool LONG>
 __device__ void resolve_item(const SpmvArgs& a, int64_t idx, int64_t row, double v) {
   if (a.atomic) {  // spmv.cpp:273-295: fp64 atomics into the zeroed y
     if (v != 0.0) atomicAdd(a.y + row, v);
@@ -170,7 +222,12 @@ __device__ void resolve_item(const SpmvArgs& a, int64_t idx, int64_t row, double
     __threadfence();
     if (atomicAdd(a.run_cnt + s, 1) != e - s) return;
     __threadfence();
-    t = run_sum_serial(a, s, e);
+    if (LONG) {
+      t = sum_fixed_order(a.item_val + s, e - s + 1);
+    } else {
+      t = 0.0;
+      for (int j = s; j <= e; ++j) t += __ldcg(a.item_val + j);
+    }
     a.run_cnt[s] = 0;
   }
   write_run(row, t, a.y, a.first_row, a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
@@ -178,8 +235,8 @@ __device__ void resolve_item(const SpmvArgs& a, int64_t idx, int64_t row, double
 
 // The same, called by a whole warp (idx, row, v uniform): the last arrival's
 // warp sums a long run 32 items at a time (fixed tree, deterministic).
-__device__ __noinline__ void resolve_item_warp(const SpmvArgs& a, int64_t idx, int64_t row,
-                                               double v, int lane) {
+__device__ __forceinline__ void resolve_item_warp(const SpmvArgs& a, int64_t idx, int64_t row,
+                                                  double v, int lane) {
   const int s = a.atomic ? 0 : a.run_first[idx], e = a.atomic ? 0 : a.run_last[idx];
   if (a.atomic || e <= s + 1) {  // single partial, pair exchange, or atomic mode
     if (lane == 0) resolve_item(a, idx, row, v);
@@ -299,7 +356,7 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
   }
   __syncwarp();
 
-  if (!TR) rows_part(a);
+  if (!TR) rows_part<!NF>(a);
   if (has_tiles) {
     double* __restrict__ y = a.y;
     const bool yh = a.y_hint != 0;
@@ -312,31 +369,18 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
         y[r] = v;
       if (mirrored) mirror_store(a.mir, r, v);
     };
-    // ---- calibration state (see "row runs" below) ----
-    const int64_t KT = a.chunk_tiles;
-    int64_t run_row = -1;    // the current run of equal rows ...
-    double run_val = 0.0;    // ... its partial inside the current chunk
-    int64_t run_item = -1;   // >= 0: the run is its chunk's first run (that item)
-    bool outer_has = false;  // a two-item run whose other part ends the previous chunk
-    double outer_val = 0.0;
-    // items deferred to the end of the warp, when their pair exchange with a
-    // neighbouring warp goes out (both in flight at once, none stalls the
-    // loop): {first item, row, value, last item, row, value} in shared memory
-    int64_t* dfl = reinterpret_cast<int64_t*>(smem + a.calib_off) + (size_t)wib * 8;
-    if (lane == 0) dfl[0] = dfl[3] = -1;
-    // run classes of the items of 32 chunks from cb on, two bytes per lane
-    int64_t cb = -64;
-    uint32_t clsv = 0;
-    auto cls_of = [&](int64_t idx) -> uint32_t {  // warp-uniform
-      const int64_t q = idx >> 1;
-      if (q < cb || q >= cb + 32) {
-        cb = q;
-        const int64_t qq = q + lane;
-        clsv = qq < a.nchunks ? *reinterpret_cast<const uint16_t*>(a.item_cls + 2 * qq) : 0u;
-      }
-      const uint32_t v = __shfl_sync(kFull, clsv, (int)(q - cb));
-      return (idx & 1) ? (v >> 8) & 0xffu : v & 0xffu;
-    };
+    int64_t pend_row = -1;
+    double pend_val = 0.0;
+    bool pend_first = true;
+    // the pending run is a long row: its parts go to their slots (pend_cnt of
+    // them stored so far by this warp); first_long: the warp's first run was
+    bool pend_long = false, first_long = false;
+    int32_t pend_L = -1, pend_cnt = 0;
+    int32_t ltv = 0;  // long tags of 32 tiles (batched like tile_ptr)
+    // the warp's first run is resolved after its loop, together with the last
+    // one (both pair exchanges in flight at once, none stalls the tile loop)
+    int64_t first_row = -1;
+    double first_val = 0.0;
     uint32_t tpv = 0, tpv_next = 0;
     int64_t eov = 0;
     int s = 0;
@@ -385,59 +429,6 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
         for (int u = 0; u < CH; ++u) xv[u] = ld_keep(a.x + sc[u * 32 + lane], pol_x);
       }
     };
-    // a final row; item 0's row goes through write_run (a shard's first row
-    // may be owned upstream: its partial is sent instead)
-    auto put_row = [&](int64_t idx, int64_t row, double v) {
-      if (lane != 0) return;
-      if (idx == 0 && !a.first_owned)
-        write_run(row, v, a.y, a.first_row, a.first_owned, a.send, a.send_flag, a.send_epoch,
-                  a.mir);
-      else
-        put_y(row, v);
-    };
-    auto emit = [&](int64_t idx, int64_t row, double v, bool warp_edge) {  // warp-uniform
-      const uint32_t c = a.atomic ? 2u : cls_of(idx);
-      if ((c & 3u) == 2u) {  // three or more items (or atomic mode)
-        resolve_item_warp(a, idx, row, v, lane);
-      } else if ((c & 3u) == 0u) {  // the only item: final
-        put_row(idx, row, v);
-      } else if (warp_edge) {  // pair with the neighbouring warp: at the end
-        if (lane == 0) {
-          int64_t* d = dfl + ((c & 4u) ? 3 : 0);
-          d[0] = idx;
-          d[1] = row;
-          d[2] = __double_as_longlong(v);
-        }
-      } else {  // pair inside the warp: folded by the caller (outer)
-        outer_has = true;
-        outer_val = v;
-      }
-    };
-    // the current run ends inside its chunk (its row does not continue)
-    auto close_run = [&]() {
-      if (run_item < 0) {  // started and ended inside the chunk: final
-        if (lane == 0) put_y(run_row, run_val);
-      } else if (outer_has) {  // the second item of an in-warp pair
-        outer_has = false;
-        put_row(run_item, run_row, outer_val + run_val);
-      } else {
-        emit(run_item, run_row, run_val, true);
-      }
-    };
-    // chunk q ended; the current run is its last run (item 2q+1)
-    auto end_chunk = [&](int64_t q, bool next_in_warp) {
-      const int64_t il = 2 * q + 1;
-      if (run_item >= 0) {  // the whole chunk is one row: items 2q (value) and 2q+1 (0.0)
-        if (!a.atomic && (cls_of(il) & 3u) == 1u) {  // exactly these two items: final
-          put_row(run_item, run_row, run_val + 0.0);
-        } else {
-          emit(run_item, run_row, run_val, true);
-          emit(il, run_row, 0.0, true);
-        }
-      } else {
-        emit(il, run_row, run_val, !next_in_warp);
-      }
-    };
     double xa[CH];
     mbar_wait(bars, 0);
     gather(0, kb, xa);
@@ -449,6 +440,7 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
         tpv = a.tile_ptr[k + lane < last ? k + lane : last];
         tpv_next = a.tile_ptr[k + 32 < last ? k + 32 : last];
         if (!NF) eov = a.eo_ptr[k + lane < a.pcs ? k + lane : a.pcs];
+        if (!NF && !TR && a.has_long) ltv = a.ltag[k + lane < a.pcs ? k + lane : a.pcs - 1];
       }
       const uint32_t tp = __shfl_sync(kFull, tpv, slot);
       const uint32_t tpn_s = __shfl_sync(kFull, tpv, (slot + 1) & 31);
@@ -663,61 +655,134 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
       }
       __syncwarp();  // closed[] is rewritten by the next tile
 
-      // ---- row runs: chunk-canonical calibration ----
-      // The tiles form fixed chunks of KT tiles (a function of the matrix
-      // alone); warp ranges and shard edges are whole chunks.  A row's value
-      // is canonical, whatever the partition: the partials of its tiles are
-      // folded in tile order inside each chunk, giving one item per chunk
-      // edge it touches (items 2q / 2q+1: chunk q's first / last run); one
-      // item is the value, two are added (a + b, either order), three or more
-      // (rows spanning whole chunks) are summed by resolve_item's fixed order.
-      const bool chunk_start = k == kb || k % KT == 0;
-      if (chunk_start) {
-        if (k > kb) end_chunk(k / KT - 1, true);
-        run_row = tile_row;
-        run_val = c0;
-        run_item = 2 * (k / KT);
-      } else if (tile_row == run_row) {
-        run_val += c0;
+      // ---- row runs across the warp's consecutive tiles ----
+      auto flush = [&]() {  // warp-uniform
+        if (!NF && pend_long) {
+          long_arrive_warp(a, pend_L, pend_cnt, lane);
+        } else if (pend_first) {
+          first_row = pend_row;
+          first_val = pend_val;
+        } else if (lane == 0) {
+          put_y(pend_row, pend_val);
+        }
+      };
+      if (NF || !a.has_long) {  // no long rows: fold every run here
+        if (k == kb) {
+          pend_row = tile_row;
+          pend_val = c0;
+          pend_first = true;
+        } else if (tile_row == pend_row) {
+          pend_val += c0;
+        } else {
+          flush();
+          pend_row = tile_row;
+          pend_val = c0;
+          pend_first = false;
+        }
+        if (H >= 2) {
+          flush();
+          pend_row = rL;
+          pend_val = cL;
+          pend_first = false;
+        }
       } else {
-        close_run();
-        run_row = tile_row;
-        run_val = c0;
-        run_item = -1;
-      }
-      if (H >= 2) {
-        close_run();
-        run_row = rL;
-        run_val = cL;
-        run_item = -1;
+        // long rows (three or more parts) store each part in its slot instead
+        // of folding it here (the fixed-order sum happens at the row's last
+        // arrival, long_arrive_warp)
+        const int ltg = __shfl_sync(kFull, ltv, slot);
+        const int l0 = (ltg & 1) ? ltg >> 2 : -1;
+        const int lL = (ltg & 2) ? (ltg >> 2) + (ltg & 1) : -1;
+        auto store_part = [&](int L, double v) {
+          if (lane == 0) a.lparts[a.lbase[L] + (k + a.t0 - a.ltf[L])] = v;
+        };
+        auto start = [&](int64_t row, double v, int L) {
+          pend_row = row;
+          if (L >= 0) {
+            store_part(L, v);
+            pend_long = true;
+            pend_L = L;
+            pend_cnt = 1;
+          } else {
+            pend_val = v;
+            pend_long = false;
+          }
+        };
+        if (k == kb) {
+          start(tile_row, c0, l0);
+          pend_first = !pend_long;
+          first_long = pend_long;
+        } else if (tile_row == pend_row) {
+          if (pend_long) {
+            store_part(pend_L, c0);
+            ++pend_cnt;
+          } else {
+            pend_val += c0;
+          }
+        } else {
+          flush();
+          pend_first = false;
+          start(tile_row, c0, l0);
+        }
+        if (H >= 2) {
+          flush();
+          pend_first = false;
+          start(rL, cL, lL);
+        }
       }
     }
     if (a.stream_only) return;  // profiling knobs: no rows were produced
-    if (ke > kb) end_chunk((ke - 1) / KT, false);
-    // the pair exchanges with the neighbouring warps (atomic mode resolved
-    // every item already)
-    __syncwarp();
-    const int64_t dfi = dfl[0], dli = dfl[3];
-    if (lane == 0 && (dfi >= 0 || dli >= 0)) {
-      const int64_t dfr = dfl[1], dlr = dfl[4];
-      const double dfv = __longlong_as_double(dfl[2]), dlv = __longlong_as_double(dfl[5]);
-      unsigned long long of = 0, ol = 0;
-      if (dfi >= 0)  // the second item of a pair exchanges on the first's slot
-        of = atomicExch(reinterpret_cast<unsigned long long*>(a.item_val + dfi - 1),
-                        (unsigned long long)__double_as_longlong(exchangeable(dfv)));
-      if (dli >= 0)
-        ol = atomicExch(reinterpret_cast<unsigned long long*>(a.item_val + dli),
-                        (unsigned long long)__double_as_longlong(exchangeable(dlv)));
-      if (dfi >= 0 && of != kSlotIdle) {
-        a.item_val[dfi - 1] = __longlong_as_double((long long)kSlotIdle);
-        write_run(dfr, __longlong_as_double((long long)of) + dfv, a.y, a.first_row,
-                  a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
+    const bool last_long = !NF && pend_long;
+    if (last_long) long_arrive_warp(a, pend_L, pend_cnt, lane);
+    // a long row's items are single-item runs of their own (k_item_keys):
+    // nothing to resolve for them
+    const bool do0 = NF || !first_long, do1 = NF || !last_long;
+    const int64_t i0 = 2 * (int64_t)w, i1 = i0 + 1;
+    const int64_t r0 = pend_first ? pend_row : first_row;
+    const double v0 = pend_first ? pend_val : first_val;
+    const double v1 = pend_first ? 0.0 : pend_val;
+    // (NF plans never have a run of more than two items: no row covers a tile)
+    const bool short_runs = NF || (a.run_last[i0] - a.run_first[i0] <= 1 &&
+                                   a.run_last[i1] - a.run_first[i1] <= 1);
+    if (a.atomic) {  // spmv.cpp:273-295: fp64 atomics into the zeroed y
+      if (lane == 0) {
+        if (do0 && v0 != 0.0) atomicAdd(a.y + r0, v0);
+        if (do1 && v1 != 0.0) atomicAdd(a.y + pend_row, v1);
       }
-      if (dli >= 0 && ol != kSlotIdle) {
-        a.item_val[dli] = __longlong_as_double((long long)kSlotIdle);
-        write_run(dlr, __longlong_as_double((long long)ol) + dlv, a.y, a.first_row,
-                  a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
+    } else if (short_runs) {
+      // both runs hold one or two partials: lane 0 issues both exchanges, then
+      // finishes whichever it completed
+      if (lane == 0) {
+        const int s0 = a.run_first[i0], e0 = a.run_last[i0];
+        const int s1 = a.run_first[i1], e1 = a.run_last[i1];
+        unsigned long long o0 = 0, o1 = 0;
+        if (e0 > s0 && do0)
+          o0 = atomicExch(reinterpret_cast<unsigned long long*>(a.item_val + s0),
+                          (unsigned long long)__double_as_longlong(exchangeable(v0)));
+        if (e1 > s1 && do1)
+          o1 = atomicExch(reinterpret_cast<unsigned long long*>(a.item_val + s1),
+                          (unsigned long long)__double_as_longlong(exchangeable(v1)));
+        if (!do0) {
+        } else if (e0 == s0) {
+          write_run(r0, v0, a.y, a.first_row, a.first_owned, a.send, a.send_flag, a.send_epoch,
+                    a.mir);
+        } else if (o0 != kSlotIdle && !(s1 == s0 && e1 > s1)) {
+          a.item_val[s0] = __longlong_as_double((long long)kSlotIdle);
+          write_run(r0, __longlong_as_double((long long)o0) + v0, a.y, a.first_row,
+                    a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
+        }
+        if (!do1) {
+        } else if (e1 == s1) {
+          write_run(pend_row, v1, a.y, a.first_row, a.first_owned, a.send, a.send_flag,
+                    a.send_epoch, a.mir);
+        } else if (o1 != kSlotIdle) {
+          a.item_val[s1] = __longlong_as_double((long long)kSlotIdle);
+          write_run(pend_row, __longlong_as_double((long long)o1) + v1, a.y, a.first_row,
+                    a.first_owned, a.send, a.send_flag, a.send_epoch, a.mir);
+        }
       }
+    } else {
+      if (do0) resolve_item_warp(a, i0, r0, v0, lane);
+      if (do1) resolve_item_warp(a, i1, pend_row, v1, lane);
     }
   }
 }

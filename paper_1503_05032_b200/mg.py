@@ -39,41 +39,38 @@ import numpy as np
 from ._lib import IPC_HANDLE_BYTES, check, lib
 
 
-def chunk_tiles(pc: int) -> int:
-    """Tiles per calibration chunk (csr5g_chunk_tiles: max(1, pc >> 16)).
-    Deterministic mode folds a row's partials per chunk, so shard edges are
-    chunk edges and y does not depend on the number of shards."""
-    return max(1, pc >> 16)
-
-
 def plan_tiles(pc: int, world: int, row_ptr=None, B: int | None = None) -> list[tuple[int, int]]:
-    """Contiguous equal ranges of whole chunks (CSR5 tiles are equal-nnz work
-    units; a chunk is chunk_tiles(pc) of them).
+    """Contiguous tile ranges of the non-empty shards, at most `world` of them
+    (CSR5 tiles are equal-nnz work units: the equal split).
 
     With the matrix's row_ptr (numpy or torch) and the tile size B, an edge
-    whose row would bring three or more chunk partials from both sides (a row
-    covering a whole chunk next to the edge) moves to the row's first chunk,
-    so every row split by a shard edge gets exactly one partial from each side
-    and the fix-up's a + b is the single-device sum bit for bit."""
-    k = chunk_tiles(pc)
-    nch = -(-pc // k)
-    edges = [g * nch // world for g in range(world + 1)]
-    if row_ptr is not None and B and world > 1:
-        step = k * B
-        for g in range(1, world):
-            c = edges[g]
+    inside a long row (nonzeros in three or more parts: tiles, the tail)
+    moves to the tile where that row starts -- or, if that would empty the
+    shard on its left, past the row's last tile -- so every long row lies in
+    one shard: its parts meet in that shard's fixed-order sum, and a row split
+    by an edge has one partial on each side, which the fix-up adds (a + b).  y
+    is then bit-identical for every shard count (deterministic mode).  A row
+    larger than the shards leaves fewer of them (the last ranks hold nothing)."""
+    if world <= 1 or pc <= 1:
+        return [(0, pc)]
+    edges = [0]
+    for g in range(1, world):
+        e = max(g * pc // world, edges[-1] + 1)
+        if row_ptr is not None and B:
             for _ in range(64):
-                if c <= edges[g - 1] or c >= nch:
+                if e >= pc:
                     break
-                r = _row_of(row_ptr, c * step)
+                r = _row_of(row_ptr, e * B)
                 lo, hi = _at(row_ptr, r), _at(row_ptr, r + 1)
-                if lo == c * step:
-                    break  # the row starts at the edge: nothing of it on the left
-                if lo > (c - 1) * step and hi < (c + 1) * step:
-                    break  # the edge row touches one chunk on each side
-                c = lo // step  # start the shard at the row's first chunk
-            edges[g] = max(edges[g - 1], min(c, nch))
-    return [(min(edges[g] * k, pc), min(edges[g + 1] * k, pc)) for g in range(world)]
+                first, last = min(lo // B, pc), min((hi - 1) // B, pc)
+                if lo == e * B or last - first < 2:
+                    break  # the row starts at the edge, or is not long
+                e = first if first > edges[-1] else last + 1
+        if e >= pc:
+            break
+        edges.append(e)
+    edges.append(pc)
+    return [(edges[g], edges[g + 1]) for g in range(len(edges) - 1)]
 
 
 def _at(row_ptr, i: int) -> int:
@@ -92,10 +89,11 @@ def _row_of(row_ptr, g: int) -> int:
     return min(max(r, 0), max(m - 1, 0))
 
 
-def effective_world(pc: int, world: int) -> int:
-    """Ranks that hold at least one chunk (a matrix smaller than the box uses
-    fewer shards; the extra ranks hold nothing)."""
-    return max(1, min(world, -(-pc // chunk_tiles(pc))))
+def effective_world(pc: int, world: int, row_ptr=None, B: int | None = None) -> int:
+    """Ranks that hold at least one tile (a matrix smaller than the box, or
+    one whose long rows swallow shards, uses fewer; the extra ranks hold
+    nothing)."""
+    return len(plan_tiles(pc, max(1, min(world, pc)), row_ptr, B))
 
 
 @dataclass
@@ -112,10 +110,10 @@ class ShardView:
 def shard_view(nnz: int, sigma: int, rank: int, world: int, row_ptr=None) -> ShardView | None:
     B = 32 * sigma
     pc = nnz // B
-    w = effective_world(pc, world)
-    if rank >= w:
+    plan = plan_tiles(pc, max(1, min(world, pc)), row_ptr, B)
+    if rank >= len(plan):
         return None
-    tb, te = plan_tiles(pc, w, row_ptr, B)[rank]
+    tb, te = plan[rank]
     last = te == pc
     return ShardView(tb, te, last and nnz % B > 0, tb * B, nnz if last else te * B)
 
@@ -213,7 +211,7 @@ class Csr5Sharded:
         self.m, self.n, self.nnz, self.sigma = m, n, nnz, sigma
         view = shard_view(nnz, sigma, rank, world, row_ptr)
         self.active = view is not None
-        self.world_eff = effective_world(nnz // (32 * sigma), world)
+        self.world_eff = effective_world(nnz // (32 * sigma), world, row_ptr, 32 * sigma)
         dev = row_ptr.device
         if self.active:
             self.a5 = csr_to_csr5_shard(row_ptr, col_slice, val_slice, m, n, nnz,
@@ -418,7 +416,7 @@ def _shards_on_device(a, sigma: int, world: int):
     col = torch.as_tensor(np.ascontiguousarray(a.col_idx, np.int32)).cuda()
     val = torch.as_tensor(np.ascontiguousarray(a.val, np.float64)).cuda()
     out = []
-    w = effective_world(a.nnz // (32 * sigma), world)
+    w = effective_world(a.nnz // (32 * sigma), world, a.row_ptr, 32 * sigma)
     for g in range(w):
         v = shard_view(a.nnz, sigma, g, w, a.row_ptr)
         out.append(csr_to_csr5_shard(rp, col[v.pos_begin:], val[v.pos_begin:], a.m, a.n, a.nnz,

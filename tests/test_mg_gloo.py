@@ -78,7 +78,7 @@ def _worker(rank, world, port, case):
     try:
         rp, col, val, m, sigma, iters = (case[k] for k in ("rp", "col", "val", "m", "sigma", "iters"))
         nnz = int(rp[-1])
-        weff = mg.effective_world(nnz // (32 * sigma), world)
+        weff = mg.effective_world(nnz // (32 * sigma), world, rp, 32 * sigma)
         x = np.asarray(case["x"], dtype=np.float64)
         xt = torch.as_tensor(x.copy())
         for _ in range(iters):
@@ -122,21 +122,35 @@ def _case(orc, kind, m, n, nnz, seed, frac, sigma, iters=2):
     return dict(rp=a.row_ptr, col=a.col_idx, val=a.val, m=a.m, sigma=sigma, x=x, iters=iters)
 
 
-def test_plan_tiles_partition():
-    import ctypes as C
+def test_shard_edges_avoid_long_rows():
+    """An edge inside a long row (three or more parts) moves to the tile where
+    the row starts; other edges stay where the equal split puts them."""
+    B = 32
+    lens = np.full(4000, 3)
+    lens[1000] = 300   # long: ~10 tiles
+    lens[3000] = 40    # two or three parts
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(rp[-1])
+    pc = nnz // B
+    for world in (2, 3, 4, 8, 16, 64):
+        r = mg.plan_tiles(pc, world, rp, B)
+        assert r[0][0] == 0 and r[-1][1] == pc and len(r) <= world
+        assert all(a < b for a, b in r)  # no empty shard
+        for (_, e), _ in zip(r, r[1:]):
+            row = int(np.searchsorted(rp, e * B, side="right") - 1)
+            lo, hi = rp[row], rp[row + 1]
+            parts = min((hi - 1) // B, pc) - min(lo // B, pc) + 1
+            assert lo == e * B or parts < 3, (world, e, row, parts)
 
-    from paper_1503_05032_b200._lib import lib
-    for pc in (0, 1, 7, 100, 131071, 131072, 514517, 4130000):
-        k = mg.chunk_tiles(pc)
-        out = C.c_int64()
-        assert lib().csr5g_chunk_tiles(pc, C.byref(out)) == 0 and out.value == k  # the C rule
+
+def test_plan_tiles_partition():
+    for pc in (0, 1, 7, 100, 514517):
         for w in (1, 2, 3, 8):
             r = mg.plan_tiles(pc, w)
             assert r[0][0] == 0 and r[-1][1] == pc
             assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
-            assert all(b0 % k == 0 for b0, _ in r)  # shard edges are chunk edges
             sizes = [b - a for a, b in r]
-            assert max(sizes) - min(sizes) <= k
+            assert max(sizes) - min(sizes) <= 1
     assert mg.effective_world(3, 8) == 3 and mg.effective_world(0, 8) == 1
 
 
@@ -151,7 +165,7 @@ def test_plan_exchange_routes_partials_to_owners(orc):
         a = orc.generate_synthetic(kind, m, n, nnz, seed, frac)
         x = np.ones(a.n)
         for world in (2, 3, 8, 16):
-            w = mg.effective_world(a.nnz // (32 * sigma), world)
+            w = mg.effective_world(a.nnz // (32 * sigma), world, a.row_ptr, 32 * sigma)
             sh = [emulate_shard(a.row_ptr, a.col_idx, a.val, x, a.m, a.nnz, sigma, g, w)
                   for g in range(w)]
             dest, senders = mg.plan_exchange([(s["first_row"], s["first_owned"]) for s in sh],
