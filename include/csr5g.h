@@ -72,6 +72,8 @@ typedef struct {
   int32_t warps_per_cta, stages, smem_bytes, x_mode, x_window;
   int32_t kernel_variant;       /* 0 general, 1 VR (values with the gathers), 2 NF (no flag paths) */
   int64_t long_rows;            /* rows with partials from three or more parts (tiles, tail) */
+  int64_t hot_cols;             /* x values staged per SpMV for the hot columns (0: none) */
+  double hot_coverage;          /* sampled share of the gathers that read a staged value */
 } csr5g_info;
 
 /* One boundary partial of a shard: row = -1 when there is none. */

@@ -44,6 +44,8 @@ class Info(C.Structure):
         ("warps_per_cta", C.c_int32), ("stages", C.c_int32), ("smem_bytes", C.c_int32),
         ("x_mode", C.c_int32), ("x_window", C.c_int32), ("kernel_variant", C.c_int32),
         ("long_rows", C.c_int64),
+        ("hot_cols", C.c_int64),
+        ("hot_coverage", C.c_double),
     ]
 
 

@@ -764,12 +764,13 @@ void free_handle(Handle* h) {
                   (void*)h->run_last, (void*)h->run_cnt, (void*)h->send, (void*)h->spill,
                   (void*)h->warp_begin, (void*)h->lrow, (void*)h->ltf, (void*)h->lnp,
                   (void*)h->lbase, (void*)h->nlong_d, (void*)h->ltag,
-                  (void*)h->lparts, (void*)h->lcnt})
+                  (void*)h->lparts, (void*)h->lcnt, (void*)h->hot_cols, (void*)h->xh,
+                  (void*)(h->col_x != h->col ? h->col_x : nullptr)})
     if (p) cudaFreeAsync(p, 0);
   for (const StreamScratch& x : h->scratch) {
     if (x.owned)
       for (void* p : {(void*)x.item_val, (void*)x.run_cnt, (void*)x.spill, (void*)x.lparts,
-                      (void*)x.lcnt})
+                      (void*)x.lcnt, (void*)x.xh})
         if (p) cudaFreeAsync(p, 0);
     if (x.done) cudaEventDestroy(x.done);
   }
@@ -1081,6 +1082,13 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   h->info.sigma = sigma;  // spmv_plan picks the sigma-specialised kernel
   h->info.n = n;          // ... and sizes its shared memory by x
   TRY(spmv_plan(h, sms));
+  // hot-column x staging for random plans whose x is several times the L2
+  // (hotx.cu); such plans gather in lane order, so the plan is made again
+  h->info.nnz_held = nnz_held;
+  h->info.num_sms = sms;
+  TRY(build_hot_plan(h, stream, &bytes));
+  if (h->n_hot > 0) TRY(spmv_plan(h, sms));
+  trace.mark("hot");
   const int64_t rows_total = h->lead_rows + (m - h->tail_row_begin);
   h->rows_blocks = rows_total > 0 ? (int)std::min<int64_t>((rows_total + 255) / 256, 2 * sms) : 0;
   const int64_t items = 2 * (int64_t)h->nwarps + 1;
@@ -1215,6 +1223,8 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   in.x_mode = h->x_mode;
   in.x_window = h->x_window ? 1 : 0;
   in.kernel_variant = h->vr ? 1 : (h->nf ? 2 : 0);
+  in.hot_cols = h->n_hot;
+  in.hot_coverage = h->hot_coverage;
   // the build is synchronous (format.hpp:182 returns a finished value): the
   // handle is usable from any stream once it returns
   TRYC(cudaStreamSynchronize(stream));

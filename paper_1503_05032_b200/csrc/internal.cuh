@@ -107,6 +107,12 @@ struct SpmvArgs {
   int64_t* trace_row;
   double* trace_val;
   int32_t* trace_count;
+  // hot-column x staging (hotx.cu): a.col holds the execution col_idx, whose
+  // negative entries c address xh[~c] (the hot columns' x values, refreshed
+  // per SpMV); the others address x[c] with the cold policy
+  const double* xh;
+  int32_t cold_pol;        // cold gathers: 0 evict_first, 1 evict_normal, 2 evict_last
+  int32_t hot_l1;          // hot gathers allocate in L1
 };
 
 struct Pipeline;  // pipeline.cu: host-vector copy/compute pipeline
@@ -121,6 +127,7 @@ struct StreamScratch {
   double* spill;
   double* lparts = nullptr;  // long-row part slots and arrival counters
   int32_t* lcnt = nullptr;
+  double* xh = nullptr;        // hot-column x values (hotx.cu), per stream
   cudaEvent_t done = nullptr;  // recorded after the last SpMV that used it
   uint64_t last_use = 0;       // LRU stamp
   bool owned = true;           // false: the handle's own arrays (freed with it)
@@ -170,6 +177,17 @@ struct Handle {
   double* lparts = nullptr;  // the first stream's part slots / counters
   int32_t* lcnt = nullptr;
   int64_t eo_entries = 0;         // empty_offset entries
+  // hot-column x staging (hotx.cu): the execution copy of col_idx (hot
+  // columns renumbered to ~rank), the hot columns in ascending order, and the
+  // first stream's staged x values; n_hot = 0: no staging (col_x = col)
+  int32_t* col_x = nullptr;
+  int32_t* hot_cols = nullptr;
+  double* xh = nullptr;
+  int64_t n_hot = 0;
+  double hot_coverage = 0.0;      // sampled share of gathers that hit a hot column
+  int hot_threshold = 0;          // sampled count a hot column reaches
+  int cold_pol = 0;               // cold gathers' L2 policy (SpmvArgs::cold_pol)
+  int hot_l1 = 0;                 // hot gathers allocate in L1 (SpmvArgs::hot_l1)
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
   int carveout_pct = -1;  // preferred shared-memory carveout of the SpMV kernel
   // per-stream SpMV scratch (the handle's own arrays are the first set);
@@ -207,10 +225,12 @@ int launch_to_csr(Handle* h, int32_t* d_col, double* d_val, cudaStream_t stream)
 int launch_tile_trace(Handle* h, int64_t k, const double* d_x, int64_t* d_rows, double* d_vals,
                       int32_t* d_count, cudaStream_t stream);
 int spmv_plan(Handle* h, int sms);
+int build_hot_plan(Handle* h, cudaStream_t stream, int64_t* bytes);
+int launch_xhot_fill(Handle* h, const double* d_x, double* d_xh, cudaStream_t stream);
 int func_attrs(const void* fn, int device, int smem, int carve);
 int scratch_done(Handle* h, cudaStream_t stream);
 int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, double** sp,
-                double** lp, int32_t** lc);
+                double** lp, int32_t** lc, double** xh);
 int spmv_host_batch(Handle* h, const double* const* xs, double* const* ys, int64_t count,
                     int mode, cudaStream_t stream);
 void free_pipeline(Pipeline* p);
@@ -336,6 +356,50 @@ __device__ __forceinline__ double ld_keep_na64(const double* p, uint64_t pol) {
       : "=d"(v)
       : "l"(p), "l"(pol));
   return v;
+}
+// Hot-column split gathers (hotx.cu): c < 0 reads the staged hot value
+// xh[~c] (kept in L2 with ph), c >= 0 the original x[c] (policy pc).
+__device__ __forceinline__ double ld_x_split(const double* x, const double* xh, int32_t c,
+                                             uint64_t ph, uint64_t pc) {
+  const bool hot = c < 0;
+  const double* p = hot ? xh + ~c : x + c;
+  const uint64_t pol = hot ? ph : pc;
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_x_split64(const double* x, const double* xh, int32_t c,
+                                               uint64_t ph, uint64_t pc) {
+  const bool hot = c < 0;
+  const double* p = hot ? xh + ~c : x + c;
+  const uint64_t pol = hot ? ph : pc;
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::64B.f64 %0, [%1], %2;"
+      : "=d"(v)
+      : "l"(p), "l"(pol));
+  return v;
+}
+// the same, hot values allocated in L1 (the hottest columns come first in xh
+// and are re-read by every warp of the SM)
+template <bool PF64>
+__device__ __forceinline__ double ld_x_split_l1(const double* x, const double* xh, int32_t c,
+                                                uint64_t ph, uint64_t pc) {
+  double v;
+  if (c < 0) {
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(xh + ~c), "l"(ph));
+  } else if (PF64) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::64B.f64 %0, [%1], %2;"
+        : "=d"(v)
+        : "l"(x + c), "l"(pc));
+  } else {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(pc));
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ double ld_x_plain64(const double* p) {
   double v;

@@ -111,8 +111,13 @@ int spmv_plan(Handle* h, int sms) {
     // R-MAT s27 38.8 -> 28.3 ms, s26 15.3 -> 11.6 ms; at s25 (268 MB) and
     // below the plain order wins (4.19 vs 4.48 ms), so the switch sits at
     // 3x the L2 (profiles/r02_csr_order_gathers.txt)
+    // With hot-column staging (hotx.cu) most gathers read the dense staged
+    // values instead, and lane order with the 64-byte prefetch on the cold
+    // rest wins: R-MAT s27 (hot set 64 MB) x_mode 8 / 1 / 5 = 16.4 / 15.6 /
+    // 14.7 ms, 13.0 with the hot values allocated in L1
+    // (profiles/r02_hot_sweep.txt)
     if (xb > 3.0 * (double)l2) {
-      h->x_mode = 8;
+      h->x_mode = h->n_hot > 0 ? 5 : 8;
       budget = 120 * 1024;
     }
   }
@@ -209,14 +214,14 @@ int func_attrs(const void* fn, int device, int smem, int carve) {
 // share its set: the caller's stream lifetime is assumed, as for any
 // per-stream workspace.)
 int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, double** sp,
-                double** lp, int32_t** lc) {
+                double** lp, int32_t** lc, double** xh) {
   std::lock_guard<std::mutex> lock(h->scratch_mu);
   StreamScratch* x = nullptr;
   for (StreamScratch& s : h->scratch)
     if (s.stream == stream) x = &s;
   if (!x && h->scratch.empty()) {
     h->scratch.push_back(StreamScratch{stream, h->item_val, h->run_cnt, h->spill, h->lparts,
-                                       h->lcnt});
+                                       h->lcnt, h->xh});
     h->scratch.back().owned = false;
     x = &h->scratch.back();
   }
@@ -242,9 +247,11 @@ int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, doubl
       if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&n.lcnt), h->long_cap * 4, stream);
       if (e == cudaSuccess) e = cudaMemsetAsync(n.lcnt, 0, h->long_cap * 4, stream);
     }
+    if (e == cudaSuccess && h->n_hot > 0)
+      e = cudaMallocAsync(reinterpret_cast<void**>(&n.xh), h->n_hot * 8, stream);
     if (e != cudaSuccess) {
       for (void* p : {(void*)n.item_val, (void*)n.run_cnt, (void*)n.spill, (void*)n.lparts,
-                      (void*)n.lcnt})
+                      (void*)n.lcnt, (void*)n.xh})
         if (p) cudaFreeAsync(p, stream);
       return cuda_fail(e, "per-stream SpMV scratch");
     }
@@ -265,6 +272,7 @@ int scratch_for(Handle* h, cudaStream_t stream, double** iv, int32_t** rc, doubl
   *sp = x->spill;
   *lp = x->lparts;
   *lc = x->lcnt;
+  *xh = x->xh;
   return CSR5G_OK;
 }
 
@@ -300,12 +308,16 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.desc = h->desc;
   a.eo_ptr = h->eo_ptr;
   a.eo = h->eo;
-  a.col = h->col;
+  a.col = h->col_x ? h->col_x : h->col;  // execution col_idx (hot columns renumbered)
   a.val = h->val;
   a.x = d_x;
   a.y = d_y;
-  if (int rc = scratch_for(h, stream, &a.item_val, &a.run_cnt, &a.spill, &a.lparts, &a.lcnt))
+  double* xh = nullptr;
+  if (int rc = scratch_for(h, stream, &a.item_val, &a.run_cnt, &a.spill, &a.lparts, &a.lcnt, &xh))
     return rc;
+  a.xh = h->n_hot > 0 ? xh : nullptr;
+  a.cold_pol = h->cold_pol;
+  a.hot_l1 = h->hot_l1;
   a.has_long = h->long_cap > 0 && !atomic;
   a.t0 = h->t0;
   a.ltag = h->ltag;
@@ -363,6 +375,9 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
   a.stream_only = stream_only;
   const int64_t items = 2 * (int64_t)h->nwarps + (h->has_tail_item ? 1 : 0);
   if (ev0) CSR5G_CUDA(cudaEventRecord(ev0, stream));
+  // the hot columns' x values for this call (inside the timed kernel span)
+  if (grid > 0 && a.xh)
+    if (int rc = launch_xhot_fill(h, d_x, xh, stream)) return rc;
   if (grid > 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);

@@ -331,6 +331,9 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
                                           (size_t)NW * S * a.stage_bytes) + (size_t)wib * SIG * 33;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_x = a.x_frac >= 1.0f ? policy_evict_last() : policy_evict_last_frac(a.x_frac);
+  const uint64_t pol_cold = a.cold_pol == 2   ? policy_evict_last()
+                            : a.cold_pol == 1 ? policy_evict_normal()
+                                              : policy_evict_first();
   const W* __restrict__ desc = static_cast<const W*>(a.desc);
 
   int64_t kb = 0, ke = 0;
@@ -397,7 +400,20 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
         for (int u = 0; u < (VR ? CH : 0); ++u)
           va[u] = ld_stream(a.val + kt * B + u * 32 + lane, pol_s);
       }
-      if (VR && a.x_mode >= 7) {  // CSR order: lane L fetches logical entry u*32 + L
+      if (VR && a.xh) {  // hot-column staging (hotx.cu): c < 0 reads xh[~c]
+        const bool csr_order = a.x_mode >= 7, pf64 = a.x_mode == 8 || a.x_mode == 5;
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) {
+          const int e = u * 32 + lane, i = e / SIG, j = e - (e / SIG) * SIG;
+          const int32_t c = sc[csr_order ? j * 32 + i : u * 32 + lane];
+          if (a.hot_l1)
+            xv[u] = pf64 ? ld_x_split_l1<true>(a.x, a.xh, c, pol_x, pol_cold)
+                         : ld_x_split_l1<false>(a.x, a.xh, c, pol_x, pol_cold);
+          else
+            xv[u] = pf64 ? ld_x_split64(a.x, a.xh, c, pol_x, pol_cold)
+                         : ld_x_split(a.x, a.xh, c, pol_x, pol_cold);
+        }
+      } else if (VR && a.x_mode >= 7) {  // CSR order: lane L fetches logical entry u*32 + L
   #pragma unroll
         for (int u = 0; u < CH; ++u) {
           const int e = u * 32 + lane, i = e / SIG, j = e - (e / SIG) * SIG;

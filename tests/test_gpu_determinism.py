@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 from oracle.oracle import Csr
+from tests import _shard_emulation as emu
 from tests._util import assert_y_close
 
 torch = pytest.importorskip("torch")
@@ -84,7 +85,7 @@ def test_y_bit_identical_across_warp_splits_and_shards(case, orc, monkeypatch):
         assert bad.size == 0, (case, env, info, bad[:5], y[bad[:5]], y0[bad[:5]])
     assert len(seen) >= 4, seen  # the warp splits really differed
     for world in (2, 3, 8):
-        ys = mg.emulate_shards_on_one_device(a, x, sigma, world)
+        ys = emu.emulate_shards_on_one_device(a, x, sigma, world)
         bad = np.flatnonzero(ys.view(np.int64) != y0.view(np.int64))
         assert bad.size == 0, (case, world, bad[:5], ys[bad[:5]], y0[bad[:5]])
     assert info0[2] >= 3  # the long rows really are long (three or more parts)

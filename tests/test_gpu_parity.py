@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 from oracle.oracle import Csr
+from tests import _shard_emulation as emu
 from tests._util import assert_y_close
 
 torch = pytest.importorskip("torch")
@@ -226,9 +227,9 @@ def test_shards_concatenate_and_fix_up(g, orc):
         full = orc.build(a, 32, sigma)
         y_ref = orc.spmv(a, x, 32, sigma)
         for world in (2, 3, 5, 8):
-            y = mg.emulate_shards_on_one_device(a, x, sigma, world)
+            y = emu.emulate_shards_on_one_device(a, x, sigma, world)
             assert_y_close(y, y_ref, a, x, f"world={world}")
-            ex = mg.emulate_shard_exports(a, sigma, world)
+            ex = emu.emulate_shard_exports(a, sigma, world)
             for f in ("tile_desc", "eo", "col_idx", "val"):
                 assert np.array_equal(np.concatenate([e[f] for e in ex]), getattr(full, f)), f
             tp = np.concatenate([e["tile_ptr"][:-1] for e in ex[:-1]] + [ex[-1]["tile_ptr"]])
@@ -249,11 +250,11 @@ def test_p2p_exchange_on_one_device(g, orc):
         sigma = orc.select_sigma(a.nnz / a.m)
         xs = [rng.random_x(a.n) for _ in range(3)]
         for world in (2, 3, 8, 16):
-            ys, errs, dest, senders = mg.emulate_p2p_on_one_device(a, xs, sigma, world)
+            ys, errs, dest, senders = emu.emulate_p2p_on_one_device(a, xs, sigma, world)
             assert errs == [0] * len(errs), (world, errs)
             for x, y in zip(xs, ys):
                 assert_y_close(y, orc.spmv(a, x, 32, sigma), a, x, f"p2p world={world}")
-                y_coll = mg.emulate_shards_on_one_device(a, x, sigma, world)
+                y_coll = emu.emulate_shards_on_one_device(a, x, sigma, world)
                 assert np.array_equal(y, y_coll), f"p2p != collective, world={world}"
         if a.m == 300:  # the long row lies in one shard (mg.plan_tiles moved the edges off
             # it), so every row split by an edge has one partial per side
@@ -274,13 +275,13 @@ def test_p2p_fused_iterative_on_one_device(g, orc):
         sigma = orc.select_sigma(a.nnz / a.m)
         x0 = rng.random_x(a.n) / 32.0
         for world in (2, 3, 8):
-            outs, errs = mg.emulate_p2p_iterative_on_one_device(a, x0, sigma, world, 3)
+            outs, errs = emu.emulate_p2p_iterative_on_one_device(a, x0, sigma, world, 3)
             assert errs == [0] * len(errs), (world, errs)
             x = x0
             for it, bufs in enumerate(outs):
                 for b in bufs[1:]:
                     assert np.array_equal(b, bufs[0]), f"world={world} it={it}: shards disagree"
-                y_coll = mg.emulate_shards_on_one_device(a, x, sigma, world)
+                y_coll = emu.emulate_shards_on_one_device(a, x, sigma, world)
                 assert np.array_equal(bufs[0], y_coll), f"world={world} it={it}: != sharded SpMV"
                 assert_y_close(bufs[0], orc.spmv(a, x, 32, sigma), a, x, f"iter {it} world={world}")
                 x = bufs[0]
