@@ -50,7 +50,24 @@ __global__ void k_fixup(const csr5g_partial* __restrict__ all, int world, int ra
   y[row] = acc;
 }
 
-SpmvFn spmv_fn(int sigma, bool vr, bool nf = false) {
+// The plan's kernel: the compile-time gather mode when the plan's x path has
+// one (spmv_kernel.cuh, GM), else the runtime-switch variant.  CSR5G_GM=0
+// forces the runtime variant (A/B).
+int gather_mode(const Handle* h) {
+  const char* e = std::getenv("CSR5G_GM");
+  if (e && std::atoi(e) == 0) return 0;
+  if (h->vr) {
+    if (h->n_hot > 0) return h->x_mode == 5 && h->hot_l1 ? 3 : 0;
+    return h->x_mode == 1 ? 1 : h->x_mode == 8 ? 2 : 0;
+  }
+  return h->x_mode == 4 ? 4 : 0;
+}
+
+SpmvFn spmv_fn(int sigma, bool vr, bool nf, int gm) {
+  SpmvFn f = nullptr;
+  if (gm >= 1 && gm <= 3 && vr) f = spmv_fn_vr_gm(sigma, gm);
+  if (gm == 4 && !vr) f = spmv_fn_local_gm4(sigma, nf && sigma <= kNfMaxSigma);
+  if (f) return f;
   if (nf && !vr && sigma <= kNfMaxSigma) return spmv_fn_nf(sigma);
   if (vr) return spmv_fn_vr(sigma);
   return spmv_fn_general(sigma);
@@ -178,6 +195,7 @@ int spmv_plan(Handle* h, int sms) {
     int pct = (int)((100LL * need_bytes + max_smem - 1) / max_smem);
     h->carveout_pct = std::min(100, std::max(0, pct));
   }
+  h->gm = gather_mode(h);
   const int64_t max_warps = (int64_t)sms * nw;
   h->nwarps = (int)std::min<int64_t>(max_warps, h->pcs);
   h->tile_blocks = (h->nwarps + nw - 1) / nw;
@@ -406,7 +424,7 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
       cfg.attrs = attr;
       cfg.numAttrs = 1;
     }
-    const SpmvFn fn = spmv_fn(a.sigma, h->vr, h->nf);
+    const SpmvFn fn = spmv_fn(a.sigma, h->vr, h->nf, h->gm);
     if (int rc = func_attrs((const void*)fn, h->device, h->smem_bytes, h->carveout_pct)) return rc;
     CSR5G_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
   }

@@ -290,7 +290,13 @@ constexpr int kVrMaxSigma = 24;  // VR variants are instantiated up to this sigm
 // TR ("trace", test hook csr5g_spmv_tile): one warp runs the general kernel on
 // the single tile a.trace_tile and records every head's final value (its
 // contribution, spmv.cpp:211-222) instead of writing y.
-template <int SIG, bool VR, bool NF = false, bool TR = false>
+// GM (gather mode) fixes the plan's x load path at compile time, so the tile
+// loop carries no per-tile mode branches: 1 = VR lane order, no L1 allocation
+// (x_mode 1); 2 = VR CSR order with the 64-byte prefetch (x_mode 8); 3 = VR
+// hot-column staging, hot values L1-allocated, cold ones 64-byte prefetched
+// (x_mode 5 + hot_l1); 4 = plain read-only loads (x_mode 4, local plans).
+// GM = 0 keeps the runtime switch over every x_mode (experiments, trace).
+template <int SIG, bool VR, bool NF = false, bool TR = false, int GM = 0>
 __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG), 1)
     k_spmv(SpmvArgs a) {
   using W = typename std::conditional<(SIG <= 17), uint32_t, uint64_t>::type;
@@ -400,7 +406,23 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
         for (int u = 0; u < (VR ? CH : 0); ++u)
           va[u] = ld_stream(a.val + kt * B + u * 32 + lane, pol_s);
       }
-      if (VR && a.xh) {  // hot-column staging (hotx.cu): c < 0 reads xh[~c]
+      if constexpr (GM == 1) {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) xv[u] = ld_keep_na(a.x + sc[u * 32 + lane], pol_x);
+      } else if constexpr (GM == 2) {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) {
+          const int e = u * 32 + lane, i = e / SIG, j = e - (e / SIG) * SIG;
+          xv[u] = ld_keep_na64(a.x + sc[j * 32 + i], pol_x);
+        }
+      } else if constexpr (GM == 3) {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u)
+          xv[u] = ld_x_split_l1<true>(a.x, a.xh, sc[u * 32 + lane], pol_x, pol_cold);
+      } else if constexpr (GM == 4) {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) xv[u] = ld_x_plain(a.x + sc[u * 32 + lane]);
+      } else if (VR && a.xh) {  // hot-column staging (hotx.cu): c < 0 reads xh[~c]
         const bool csr_order = a.x_mode >= 7, pf64 = a.x_mode == 8 || a.x_mode == 5;
   #pragma unroll
         for (int u = 0; u < CH; ++u) {
@@ -523,7 +545,7 @@ __global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG),
   #pragma unroll
         for (int j0 = 0; j0 < SIG; j0 += CH) {
           double xv[CH];
-          if (j0 == 0 && VR && a.x_mode >= 7) {
+          if (j0 == 0 && VR && (GM == 2 || (GM == 0 && a.x_mode >= 7))) {
             constexpr int rs = 33;  // row stride 33: no bank conflicts
   #pragma unroll
             for (int u = 0; u < CH; ++u) {
@@ -811,5 +833,17 @@ SpmvFn spmv_fn_general(int sigma);
 SpmvFn spmv_fn_vr(int sigma);
 SpmvFn spmv_fn_nf(int sigma);
 SpmvFn spmv_fn_trace(int sigma);
+SpmvFn spmv_fn_vr_gm(int sigma, int gm);  // GM 1..3 (spmv_inst_vr_gm*.cu)
+SpmvFn spmv_fn_local_gm4(int sigma, bool nf);  // GM 4, general / NF (spmv_inst_gm4.cu)
+
+// k_spmv<S..MAX, ...> as a sigma switch, instantiated where it is called
+template <int S, int MAX, bool VR, bool NF, bool TR, int GM>
+SpmvFn pick_sigma(int sigma) {
+  if constexpr (S > MAX) {
+    return nullptr;
+  } else {
+    return sigma == S ? k_spmv<S, VR, NF, TR, GM> : pick_sigma<S + 1, MAX, VR, NF, TR, GM>(sigma);
+  }
+}
 
 }  // namespace csr5g
