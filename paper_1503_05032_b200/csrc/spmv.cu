@@ -156,7 +156,8 @@ int spmv_plan(Handle* h, int sms) {
   // NF plans (short tiles, sigma <= 8): two stages too -- the 2 KB tile
   // arrives well within one tile's work, and the smaller ring leaves more L1
   // (Laplacian 1000^2 at 24 warps: 2 / 3 stages 25.1 / 26.0 us mean)
-  int nw = (h->nf ? spmv_threads_nf(sigma) : spmv_threads(sigma)) / 32,
+  h->gm = gather_mode(h);
+  int nw = spmv_threads_of(sigma, h->vr, h->nf, h->gm) / 32,
       stages = random || h->nf ? 2 : 4;
   // one mbarrier per warp and stage at the start, 128-byte aligned
   auto bars = [](int w, int st) { return (w * st * 8 + 127) / 128 * 128; };
@@ -195,7 +196,6 @@ int spmv_plan(Handle* h, int sms) {
     int pct = (int)((100LL * need_bytes + max_smem - 1) / max_smem);
     h->carveout_pct = std::min(100, std::max(0, pct));
   }
-  h->gm = gather_mode(h);
   const int64_t max_warps = (int64_t)sms * nw;
   h->nwarps = (int)std::min<int64_t>(max_warps, h->pcs);
   h->tile_blocks = (h->nwarps + nw - 1) / nw;

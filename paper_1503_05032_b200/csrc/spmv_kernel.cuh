@@ -272,6 +272,17 @@ __host__ __device__ constexpr int spmv_threads(int sigma) {
 __host__ __device__ constexpr int spmv_threads_nf(int sigma) {
   return sigma <= 5 ? 768 : spmv_threads(sigma);  // 80 registers suffice without the flag paths
 }
+#ifndef CSR5G_VR_GM_THREADS16
+#define CSR5G_VR_GM_THREADS16 512
+#endif
+// VR kernels with a compile-time gather mode (fewer registers than the
+// runtime switch)
+__host__ __device__ constexpr int spmv_threads_vr_gm(int sigma) {
+  return sigma <= 16 && sigma > 13 ? CSR5G_VR_GM_THREADS16 : spmv_threads(sigma);
+}
+__host__ __device__ constexpr int spmv_threads_of(int sigma, bool vr, bool nf, int gm) {
+  return nf ? spmv_threads_nf(sigma) : (vr && gm != 0) ? spmv_threads_vr_gm(sigma) : spmv_threads(sigma);
+}
 // closed-segment slots per warp in shared memory (tiles rarely have more heads)
 constexpr int kClosedSlots = 128;
 constexpr int kEoSlots = 128;  // >= kClosedSlots - 1 heads of a shared-slot tile
@@ -297,7 +308,7 @@ constexpr int kVrMaxSigma = 24;  // VR variants are instantiated up to this sigm
 // (x_mode 5 + hot_l1); 4 = plain read-only loads (x_mode 4, local plans).
 // GM = 0 keeps the runtime switch over every x_mode (experiments, trace).
 template <int SIG, bool VR, bool NF = false, bool TR = false, int GM = 0>
-__global__ void __launch_bounds__(NF ? spmv_threads_nf(SIG) : spmv_threads(SIG), 1)
+__global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
     k_spmv(SpmvArgs a) {
   using W = typename std::conditional<(SIG <= 17), uint32_t, uint64_t>::type;
   constexpr int B = 32 * SIG;
