@@ -788,7 +788,7 @@ def measure_sharded(args, name, workload, dev, local, dist, rank, world):
     peak, peak_src = peaks()
     line = None
     if rank == 0:
-        launches = 1
+        launches = 1 + (1 if info is not None and info.hot_cols > 0 else 0)  # + hot-x staging
         if sh.active:
             if sh.exchange == "p2p":
                 sb, se = sh.senders[sh.rank]
@@ -809,6 +809,12 @@ def measure_sharded(args, name, workload, dev, local, dist, rank, world):
                                  "iterative: SpMV + y->x all-gather") if args.iterative else
                                 "SpMV + boundary exchange"),
                        "exchange": os.environ.get("CSR5G_EXCHANGE", "p2p"),
+                       # NVLink bytes each GPU sends per step (DESIGN §6 model):
+                       # the boundary partial (16 B + flags) per shard edge, and in
+                       # the fused iterative mode its owned rows of y to every peer
+                       "nvlink_out_bytes_per_step_per_gpu": (
+                           8 * (own[1] - own[0]) * (world - 1)
+                           if args.iterative and sh.iterative else 16 + 8),
                        "parallelism": f"tile-range shards x{world}, x replicated",
                        "l2": f"L2 flushed between timed calls ({2 * l2_bytes / 1e6:.0f} MB read)",
                        "x": "mt19937_64(1), 0.5 + (rng()>>11)*2^-53 (bench.cpp:103-105)"},

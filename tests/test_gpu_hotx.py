@@ -63,5 +63,13 @@ def test_hot_staging_is_bit_identical(scale, stride, orc, monkeypatch):
     rp = d.row_ptr.cpu().numpy()
     a = Csr(m, n, rp, d.col_idx.cpu().numpy().astype(np.int64), d.val.cpu().numpy())
     assert_y_close(y0, orc.spmv(a, x, 32, int(plain.info.sigma)), a, x, f"rmat{scale}")
+    # tile-range shards build their own hot sets; deterministic y is partition
+    # invariant, so every shard count gives the single-device bits
+    yd = csr5.spmv_csr5(plain, xd).cpu().numpy()
+    sigma = int(plain.info.sigma)
     plain.release()
     hot.release()
+    from tests import _shard_emulation as emu
+    for world in (2, 3):
+        ys = emu.emulate_shards_on_one_device(a, x, sigma, world)
+        assert np.array_equal(ys.view(np.int64), yd.view(np.int64)), world

@@ -30,11 +30,12 @@ for cfg in configs:
         os.environ[k] = v
     a5 = csr5.csr_to_csr5(a, csr5.TuningParams(sigma=sigma))
     evs = [(csr5.Event(), csr5.Event()) for _ in range(10)]
+    mode = os.environ.get("PROBE_MODE", "deterministic")
     for _ in range(3):
-        csr5.spmv_csr5(a5, x, y)
+        csr5.spmv_csr5(a5, x, y, mode=mode)
     for e0, e1 in evs:
         scrub.sum()
-        csr5.spmv_csr5_evt(a5, x, y, e0, e1)
+        csr5.spmv_csr5_evt(a5, x, y, e0, e1, mode=mode)
     ts = sorted(e0.elapsed_ms(e1) for e0, e1 in evs)
     ms = sum(ts) / len(ts)
     same = "-"
@@ -45,5 +46,5 @@ for cfg in configs:
     i = a5.info
     print(f"{name} [{cfg}] {ms:.4f} ms (min {ts[0]:.4f}) frac {i.spmv_bytes / ms / 1e6 / 6458.4:.3f} "
           f"hot {i.hot_cols} cov {i.hot_coverage:.3f} build {i.build_ms:.1f} ms warps {i.warps_per_cta} "
-          f"xmode {i.x_mode} y_same {same}", flush=True)
+          f"xmode {i.x_mode} long {i.long_rows} y_same {same}", flush=True)
     a5.release()
