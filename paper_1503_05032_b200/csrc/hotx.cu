@@ -137,14 +137,14 @@ int64_t env_i64(const char* name, int64_t dflt) {
 }  // namespace
 
 // Decides and builds the staging (h->vr plans only; CSR5G_HOT = 0 off, 1 on
-// whatever x's size, unset: on when 8n exceeds 3x the L2 and the hot set
+// whatever x's size, unset: on when 8n exceeds 3/4 of the L2 and the hot set
 // takes >= 30% of the sampled gathers).  Out of memory for the execution copy
 // is not an error: the handle keeps the plain gathers.
 int build_hot_plan(Handle* h, cudaStream_t stream, int64_t* bytes) {
   h->col_x = h->col;
   h->n_hot = 0;
   h->cold_pol = (int)env_i64("CSR5G_HOT_COLD_POL", 0);
-  h->hot_l1 = (int)env_i64("CSR5G_HOT_L1", 1);
+
   const int64_t mode = env_i64("CSR5G_HOT", -1);
   const int64_t n = h->info.n;
   const int64_t tiled = h->pcs * h->B;
@@ -152,14 +152,18 @@ int build_hot_plan(Handle* h, cudaStream_t stream, int64_t* bytes) {
   int l2 = 0, sms = 0;
   CSR5G_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device));
   CSR5G_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-  // (x within 3x the L2, e.g. R-MAT s24 at 134 MB: staging measured slower,
-  // 1.69-2.28 vs 1.56 ms, profiles/r02_hot_sweep.txt)
-  if (mode < 0 && (double)n * 8.0 <= 3.0 * (double)l2) return CSR5G_OK;
+  if (mode < 0 && (double)n * 8.0 <= 0.75 * (double)l2) return CSR5G_OK;
+  // x several times the L2 (R-MAT s27): hottest first and L1-allocated hot
+  // gathers; x around the L2 (R-MAT s24): ascending column order, no L1
+  // allocation (the other way round measured slower on each,
+  // profiles/r02_hot_sweep.txt)
+  const bool big = (double)n * 8.0 > 3.0 * (double)l2;
+  h->hot_l1 = (int)env_i64("CSR5G_HOT_L1", big ? 1 : 0);
   const int64_t hmax = env_i64("CSR5G_HOT_COLS", env_i64("CSR5G_HOT_MB", 64) * (1 << 20) / 8);
   // sample: every entry up to 2^28 of them, then every stride-th
   const int stride = (int)std::max<int64_t>(
       1, env_i64("CSR5G_HOT_STRIDE", (tiled + (int64_t(1) << 28) - 1) >> 28));
-  const bool by_count = env_i64("CSR5G_HOT_ORDER", 1) != 0;
+  const bool by_count = env_i64("CSR5G_HOT_ORDER", big ? 1 : 0) != 0;
 
   uint32_t* cnt = nullptr;
   unsigned long long* hist = nullptr;

@@ -57,7 +57,7 @@ int gather_mode(const Handle* h) {
   const char* e = std::getenv("CSR5G_GM");
   if (e && std::atoi(e) == 0) return 0;
   if (h->vr) {
-    if (h->n_hot > 0) return h->x_mode == 5 && h->hot_l1 ? 3 : 0;
+    if (h->n_hot > 0) return h->x_mode == 5 && h->hot_l1 ? 3 : h->x_mode == 1 && !h->hot_l1 ? 5 : 0;
     return h->x_mode == 1 ? 1 : h->x_mode == 8 ? 2 : 0;
   }
   return h->x_mode == 4 ? 4 : 0;
@@ -65,7 +65,7 @@ int gather_mode(const Handle* h) {
 
 SpmvFn spmv_fn(int sigma, bool vr, bool nf, int gm) {
   SpmvFn f = nullptr;
-  if (gm >= 1 && gm <= 3 && vr) f = spmv_fn_vr_gm(sigma, gm);
+  if ((gm >= 1 && gm <= 3 || gm == 5) && vr) f = spmv_fn_vr_gm(sigma, gm);
   if (gm == 4 && !vr) f = spmv_fn_local_gm4(sigma, nf && sigma <= kNfMaxSigma);
   if (f) return f;
   if (nf && !vr && sigma <= kNfMaxSigma) return spmv_fn_nf(sigma);
@@ -121,6 +121,10 @@ int spmv_plan(Handle* h, int sms) {
     CSR5G_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device));
     const double xb = (double)h->info.n * 8.0;
     budget = xb > 0.75 * (double)l2 ? 60 * 1024 : 72 * 1024;
+    // with hot-column staging most gathers hit the dense staged values in L2
+    // and more warps win again: R-MAT s24 10 / 13 / 16 warps (budget 60 / 80 /
+    // 100 KB) -> 1.45 / 1.37 / 1.28 ms
+    if (h->n_hot > 0) budget = 100 * 1024;
     // x several times the L2 (R-MAT s26/s27: 537 MB / 1.07 GB): the gathers
     // are DRAM-random-access bound.  Issued in CSR order (lane L fetches the
     // tile's logical entry u*32 + L, exchanged into the lane-per-column order

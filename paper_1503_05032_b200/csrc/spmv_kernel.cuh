@@ -305,7 +305,9 @@ constexpr int kVrMaxSigma = 24;  // VR variants are instantiated up to this sigm
 // loop carries no per-tile mode branches: 1 = VR lane order, no L1 allocation
 // (x_mode 1); 2 = VR CSR order with the 64-byte prefetch (x_mode 8); 3 = VR
 // hot-column staging, hot values L1-allocated, cold ones 64-byte prefetched
-// (x_mode 5 + hot_l1); 4 = plain read-only loads (x_mode 4, local plans).
+// (x_mode 5 + hot_l1); 4 = plain read-only loads (x_mode 4, local plans);
+// 5 = VR hot-column staging, lane order, no L1 allocation, no prefetch
+// (x_mode 1 without hot_l1).
 // GM = 0 keeps the runtime switch over every x_mode (experiments, trace).
 template <int SIG, bool VR, bool NF = false, bool TR = false, int GM = 0>
 __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
@@ -430,6 +432,10 @@ __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
   #pragma unroll
         for (int u = 0; u < CH; ++u)
           xv[u] = ld_x_split_l1<true>(a.x, a.xh, sc[u * 32 + lane], pol_x, pol_cold);
+      } else if constexpr (GM == 5) {
+  #pragma unroll
+        for (int u = 0; u < CH; ++u)
+          xv[u] = ld_x_split(a.x, a.xh, sc[u * 32 + lane], pol_x, pol_cold);
       } else if constexpr (GM == 4) {
   #pragma unroll
         for (int u = 0; u < CH; ++u) xv[u] = ld_x_plain(a.x + sc[u * 32 + lane]);
@@ -844,7 +850,7 @@ SpmvFn spmv_fn_general(int sigma);
 SpmvFn spmv_fn_vr(int sigma);
 SpmvFn spmv_fn_nf(int sigma);
 SpmvFn spmv_fn_trace(int sigma);
-SpmvFn spmv_fn_vr_gm(int sigma, int gm);  // GM 1..3 (spmv_inst_vr_gm*.cu)
+SpmvFn spmv_fn_vr_gm(int sigma, int gm);  // GM 1..3, 5 (spmv_inst_vr_gm*.cu)
 SpmvFn spmv_fn_local_gm4(int sigma, bool nf);  // GM 4, general / NF (spmv_inst_gm4.cu)
 
 // k_spmv<S..MAX, ...> as a sigma switch, instantiated where it is called
