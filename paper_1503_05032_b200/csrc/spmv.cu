@@ -56,6 +56,9 @@ __global__ void k_fixup(const csr5g_partial* __restrict__ all, int world, int ra
 int gather_mode(const Handle* h) {
   const char* e = std::getenv("CSR5G_GM");
   if (e && std::atoi(e) == 0) return 0;
+  // the profiling / experiment knobs GM 4 compiles out
+  for (const char* k : {"CSR5G_STREAM_ONLY", "CSR5G_YHINT", "CSR5G_EARLY"})
+    if (std::getenv(k) && !h->vr) return 0;
   if (h->vr) {
     if (h->n_hot > 0) return h->x_mode == 5 && h->hot_l1 ? 3 : h->x_mode == 1 && !h->hot_l1 ? 5 : 0;
     return h->x_mode == 1 ? 1 : h->x_mode == 8 ? 2 : 0;

@@ -318,7 +318,13 @@ __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
   static_assert(!VR || CH == SIG, "VR needs the whole tile's gathers in one batch");
   constexpr int CAPC = B < kClosedSlots ? B : kClosedSlots;
   constexpr uint64_t FMASK = (1ull << SIG) - 1;
-  constexpr bool EARLY_OK = !VR && SIG <= 18;  // a second x array fits in registers
+  // GM 4 (local plans) compiles the profiling knobs (stream_only, y_hint)
+  // out, and early gathers, which only random non-VR plans use: Laplacian
+  // 24.8 -> 22.7 us, st27 0.442 -> 0.435 ms.  The VR kernels keep them --
+  // without them R-MAT s24 measured slower (1.42 vs 1.27 ms, GM 5), an
+  // effect of the compiler's schedule, not of the knobs' work.
+  constexpr bool KNOBS = GM != 4;
+  constexpr bool EARLY_OK = !VR && SIG <= 18 && GM != 4;  // a second x array fits in registers
   constexpr uint32_t COL_OFF = VR ? 0 : B * 8, DESC_OFF = COL_OFF + B * 4;
   constexpr uint32_t TILE_BYTES = DESC_OFF + 32 * sizeof(W);
 
@@ -381,7 +387,7 @@ __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
   if (!TR) rows_part<!NF>(a);
   if (has_tiles) {
     double* __restrict__ y = a.y;
-    const bool yh = a.y_hint != 0;
+    const bool yh = KNOBS && a.y_hint != 0;
     const bool mirrored = a.mir.n != 0;
     auto put_y = [&](int64_t r, double v) {
       if (TR) return;
@@ -508,10 +514,10 @@ __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
 
       // profiling knob 2: compute only -- every tile re-reads the resident
       // stage 0, no TMA traffic after the prologue (y is garbage)
-      const bool compute_only = a.stream_only == 2;
+      const bool compute_only = KNOBS && a.stream_only == 2;
       const int sn = compute_only ? 0 : (s + 1 == S ? 0 : s + 1);
       const uint32_t pn = compute_only ? 0u : (s + 1 == S ? phase ^ 1u : phase);
-      if (a.stream_only == 1) {  // profiling knob 1: the TMA ring alone (y is garbage)
+      if (KNOBS && a.stream_only == 1) {  // profiling knob 1: the TMA ring alone (y is garbage)
         mbar_wait(bars + s, phase);
         __syncwarp();
         if (lane == 0 && k + S < ke) issue(k + S, s);
@@ -785,7 +791,7 @@ __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
         }
       }
     }
-    if (a.stream_only) return;  // profiling knobs: no rows were produced
+    if (KNOBS && a.stream_only) return;  // profiling knobs: no rows were produced
     const bool last_long = !NF && pend_long;
     if (last_long) long_arrive_warp(a, pend_L, pend_cnt, lane);
     // a long row's items are single-item runs of their own (k_item_keys):
