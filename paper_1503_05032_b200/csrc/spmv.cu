@@ -169,8 +169,8 @@ int spmv_plan(Handle* h, int sms) {
   // one mbarrier per warp and stage at the start, 128-byte aligned
   auto bars = [](int w, int st) { return (w * st * 8 + 127) / 128 * 128; };
   // x_mode 7/8 (CSR-order gathers, VR only) need a sigma x 33 exchange buffer per warp
-  if (h->x_mode >= 7 && !h->vr) h->x_mode = 1;
-  const int xex_bytes = h->x_mode >= 7 ? sigma * 33 * 8 : 0;
+  if ((h->x_mode == 7 || h->x_mode == 8) && !h->vr) h->x_mode = 1;
+  const int xex_bytes = (h->x_mode == 7 || h->x_mode == 8) ? sigma * 33 * 8 : 0;
   auto need = [&](int w, int st) {
     return bars(w, st) + w * (closed_bytes + kEoSlots * 4 + st * stage_bytes + xex_bytes);
   };

@@ -445,8 +445,14 @@ __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
       } else if constexpr (GM == 4) {
   #pragma unroll
         for (int u = 0; u < CH; ++u) xv[u] = ld_x_plain(a.x + sc[u * 32 + lane]);
+      } else if (a.x_mode == 9) {  // profiling: no gathers (x taken as the column's parity)
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) xv[u] = (double)(sc[u * 32 + lane] & 1);
+      } else if (a.x_mode == 10) {  // profiling: every gather reads x[0] (an L1 hit)
+  #pragma unroll
+        for (int u = 0; u < CH; ++u) xv[u] = ld_keep(a.x + (sc[u * 32 + lane] & 0), pol_x);
       } else if (VR && a.xh) {  // hot-column staging (hotx.cu): c < 0 reads xh[~c]
-        const bool csr_order = a.x_mode >= 7, pf64 = a.x_mode == 8 || a.x_mode == 5;
+        const bool csr_order = a.x_mode == 7 || a.x_mode == 8, pf64 = a.x_mode == 8 || a.x_mode == 5;
   #pragma unroll
         for (int u = 0; u < CH; ++u) {
           const int e = u * 32 + lane, i = e / SIG, j = e - (e / SIG) * SIG;
@@ -458,7 +464,7 @@ __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
             xv[u] = pf64 ? ld_x_split64(a.x, a.xh, c, pol_x, pol_cold)
                          : ld_x_split(a.x, a.xh, c, pol_x, pol_cold);
         }
-      } else if (VR && a.x_mode >= 7) {  // CSR order: lane L fetches logical entry u*32 + L
+      } else if (VR && (a.x_mode == 7 || a.x_mode == 8)) {  // CSR order: lane L fetches entry u*32 + L
   #pragma unroll
         for (int u = 0; u < CH; ++u) {
           const int e = u * 32 + lane, i = e / SIG, j = e - (e / SIG) * SIG;
@@ -568,7 +574,7 @@ __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
   #pragma unroll
         for (int j0 = 0; j0 < SIG; j0 += CH) {
           double xv[CH];
-          if (j0 == 0 && VR && (GM == 2 || (GM == 0 && a.x_mode >= 7))) {
+          if (j0 == 0 && VR && (GM == 2 || (GM == 0 && (a.x_mode == 7 || a.x_mode == 8)))) {
             constexpr int rs = 33;  // row stride 33: no bank conflicts
   #pragma unroll
             for (int u = 0; u < CH; ++u) {
