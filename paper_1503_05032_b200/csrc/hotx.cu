@@ -171,14 +171,32 @@ int build_hot_plan(Handle* h, cudaStream_t stream, int64_t* bytes) {
   int32_t *wc = nullptr, *wpre = nullptr, *hot = nullptr, *colx = nullptr;
   double* xh = nullptr;
   void* cub_tmp = nullptr;
+  uint32_t *key = nullptr, *key2 = nullptr;  // count-order sort temporaries
+  int32_t *idx = nullptr, *order = nullptr, *sorted = nullptr, *perm = nullptr;
+  void* st = nullptr;
   const int64_t nwords = (n + 31) / 32;
+  // keep = true: the staging survives (hot, colx, xh); every temporary goes
   auto release = [&](bool keep) {
-    for (void* p : {(void*)cnt, (void*)hist, (void*)bm, (void*)wc, (void*)wpre, cub_tmp})
+    for (void* p : {(void*)cnt, (void*)hist, (void*)bm, (void*)wc, (void*)wpre, cub_tmp,
+                    (void*)key, (void*)key2, (void*)idx, (void*)order, (void*)perm, st})
       if (p) cudaFreeAsync(p, stream);
-    if (!keep)
-      for (void* p : {(void*)hot, (void*)colx, (void*)xh})
+    cnt = nullptr, hist = nullptr, bm = nullptr, wc = wpre = nullptr, cub_tmp = nullptr;
+    key = key2 = nullptr, idx = order = perm = nullptr, st = nullptr;
+    if (!keep) {
+      for (void* p : {(void*)hot, (void*)colx, (void*)xh, (void*)sorted})
         if (p) cudaFreeAsync(p, stream);
+      hot = colx = sorted = nullptr, xh = nullptr;
+    }
   };
+  // a CUDA failure after the first allocation frees everything before it returns
+#define HTRY(call)                                   \
+  do {                                               \
+    const cudaError_t e_ = (call);                   \
+    if (e_ != cudaSuccess) {                         \
+      release(false);                                \
+      return cuda_fail(e_, #call);                   \
+    }                                                \
+  } while (0)
   auto alloc = [&](auto** p, size_t nb) {
     const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(nb, 16), stream);
     if (e != cudaSuccess) cudaGetLastError();
@@ -189,16 +207,16 @@ int build_hot_plan(Handle* h, cudaStream_t stream, int64_t* bytes) {
     release(false);
     return CSR5G_OK;
   }
-  CSR5G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * n, stream));
-  CSR5G_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * kHotBins, stream));
+  HTRY(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * n, stream));
+  HTRY(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * kHotBins, stream));
   k_hot_count<<<sms * 8, 256, 0, stream>>>(h->col, tiled, stride, cnt);
-  CSR5G_CUDA(cudaGetLastError());
+  HTRY(cudaGetLastError());
   k_hot_hist<<<sms * 4, 256, 0, stream>>>(cnt, n, hist);
-  CSR5G_CUDA(cudaGetLastError());
+  HTRY(cudaGetLastError());
   std::vector<unsigned long long> hh(kHotBins);
-  CSR5G_CUDA(cudaMemcpyAsync(hh.data(), hist, sizeof(unsigned long long) * kHotBins,
+  HTRY(cudaMemcpyAsync(hh.data(), hist, sizeof(unsigned long long) * kHotBins,
                              cudaMemcpyDeviceToHost, stream));
-  CSR5G_CUDA(cudaStreamSynchronize(stream));
+  HTRY(cudaStreamSynchronize(stream));
   // threshold: the smallest sampled count whose columns fit the budget
   std::vector<double> cols(kHotBins + 1, 0.0), mass(kHotBins + 1, 0.0);
   for (int b = kHotBins - 1; b >= 0; --b) {
@@ -214,7 +232,7 @@ int build_hot_plan(Handle* h, cudaStream_t stream, int64_t* bytes) {
     return CSR5G_OK;
   }
   size_t cub_bytes = 0;
-  CSR5G_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (int32_t*)nullptr, (int32_t*)nullptr,
+  HTRY(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (int32_t*)nullptr, (int32_t*)nullptr,
                                            (int)nwords, stream));
   if (!alloc(&bm, sizeof(uint32_t) * nwords) || !alloc(&wc, sizeof(int32_t) * nwords) ||
       !alloc(&wpre, sizeof(int32_t) * nwords) || !alloc(&cub_tmp, cub_bytes) ||
@@ -225,45 +243,39 @@ int build_hot_plan(Handle* h, cudaStream_t stream, int64_t* bytes) {
   }
   const unsigned cb = (unsigned)((nwords * 32 + 255) / 256);
   k_hot_bits<<<cb, 256, 0, stream>>>(cnt, n, (uint32_t)thr, bm, wc);
-  CSR5G_CUDA(cudaGetLastError());
-  CSR5G_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, wc, wpre, (int)nwords, stream));
+  HTRY(cudaGetLastError());
+  HTRY(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, wc, wpre, (int)nwords, stream));
   k_hot_list<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(bm, wpre, n, hot);
-  CSR5G_CUDA(cudaGetLastError());
+  HTRY(cudaGetLastError());
   // hottest first (stable: equal counts keep column order), so the most
   // gathered values share the fewest lines
-  int32_t* perm = nullptr;
   if (by_count) {
-    uint32_t *key = nullptr, *key2 = nullptr;
-    int32_t *idx = nullptr, *order = nullptr, *sorted = nullptr;
-    void* st = nullptr;
     size_t sb = 0;
-    CSR5G_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, key, key2, idx, order, (int)H,
+    HTRY(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, key, key2, idx, order, (int)H,
                                                          0, 32, stream));
     if (!alloc(&key, 4 * H) || !alloc(&key2, 4 * H) || !alloc(&idx, 4 * H) ||
         !alloc(&order, 4 * H) || !alloc(&sorted, 4 * H) || !alloc(&perm, 4 * H) || !alloc(&st, sb)) {
-      for (void* p : {(void*)key, (void*)key2, (void*)idx, (void*)order, (void*)sorted, (void*)perm, st})
-        if (p) cudaFreeAsync(p, stream);
       release(false);
       return CSR5G_OK;
     }
     const unsigned hb = (unsigned)((H + 255) / 256);
     k_hot_keys<<<hb, 256, 0, stream>>>(hot, cnt, H, key, idx);
-    CSR5G_CUDA(cudaGetLastError());
-    CSR5G_CUDA(cub::DeviceRadixSort::SortPairsDescending(st, sb, key, key2, idx, order, (int)H, 0, 32,
+    HTRY(cudaGetLastError());
+    HTRY(cub::DeviceRadixSort::SortPairsDescending(st, sb, key, key2, idx, order, (int)H, 0, 32,
                                                          stream));
     k_hot_perm<<<hb, 256, 0, stream>>>(order, hot, H, perm, sorted);
-    CSR5G_CUDA(cudaGetLastError());
-    for (void* p : {(void*)key, (void*)key2, (void*)idx, (void*)order, (void*)hot, st})
-      cudaFreeAsync(p, stream);
+    HTRY(cudaGetLastError());
+    int32_t* ascending = hot;
     hot = sorted;
+    sorted = nullptr;
+    HTRY(cudaFreeAsync(ascending, stream));
   }
   k_col_exec<<<sms * 8, 256, 0, stream>>>(reinterpret_cast<const int4*>(h->col), tiled / 4, bm, wpre,
                                           perm, reinterpret_cast<int4*>(colx));
-  CSR5G_CUDA(cudaGetLastError());
-  if (perm) CSR5G_CUDA(cudaFreeAsync(perm, stream));
+  HTRY(cudaGetLastError());
   const int64_t rest = h->info.nnz_held - tiled;  // the CSR tail keeps its columns
   if (rest > 0)
-    CSR5G_CUDA(cudaMemcpyAsync(colx + tiled, h->col + tiled, sizeof(int32_t) * rest,
+    HTRY(cudaMemcpyAsync(colx + tiled, h->col + tiled, sizeof(int32_t) * rest,
                                cudaMemcpyDeviceToDevice, stream));
   release(true);
   h->col_x = colx;
@@ -274,6 +286,7 @@ int build_hot_plan(Handle* h, cudaStream_t stream, int64_t* bytes) {
   h->hot_threshold = thr;
   *bytes += (int64_t)(sizeof(int32_t) * (H + h->info.nnz_held) + sizeof(double) * H);
   return CSR5G_OK;
+#undef HTRY
 }
 
 int launch_xhot_fill(Handle* h, const double* d_x, double* d_xh, cudaStream_t stream) {
