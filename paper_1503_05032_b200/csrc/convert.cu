@@ -381,24 +381,81 @@ __global__ void k_warp_bounds(const int64_t* __restrict__ prefix, int64_t pcs, i
 // are b'[w] = w + max_{j<=w}(b[j] - j) and b''[w] = w + min_{j>=w}(b'[j] - j):
 // a prefix max and a suffix min, done by one CTA (nw <= 32 * 1024).
 constexpr int kFixThreads = 1024;
+// Block-wide exclusive scans for the one-CTA plan kernels (kFixThreads
+// threads): warp shuffles, then one pass over the warp totals -- three
+// barriers instead of a log-step shared-memory scan's twenty.  fwd: the op
+// over threads < t; bwd: the op over threads > t.
+template <typename T, typename Op>
+__device__ __forceinline__ T block_excl_fwd(T v, T ident, Op op, T* wtot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const T o = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v = op(v, o);
+  }
+  T x = __shfl_up_sync(kFull, v, 1);
+  if (lane == 0) x = ident;
+  if (lane == 31) wtot[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    T t = lane < nw ? wtot[lane] : ident;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const T o = __shfl_up_sync(kFull, t, d);
+      if (lane >= d) t = op(t, o);
+    }
+    wtot[lane] = t;
+  }
+  __syncthreads();
+  const T before = w > 0 ? wtot[w - 1] : ident;
+  __syncthreads();  // wtot is reused by the next scan
+  return op(x, before);
+}
+template <typename T, typename Op>
+__device__ __forceinline__ T block_excl_bwd(T v, T ident, Op op, T* wtot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const T o = __shfl_down_sync(kFull, v, d);
+    if (lane + d < 32) v = op(v, o);
+  }
+  T x = __shfl_down_sync(kFull, v, 1);
+  if (lane == 31) x = ident;
+  if (lane == 0) wtot[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    T t = lane < nw ? wtot[lane] : ident;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const T o = __shfl_down_sync(kFull, t, d);
+      if (lane + d < 32) t = op(t, o);
+    }
+    wtot[lane] = t;
+  }
+  __syncthreads();
+  const T after = w + 1 < nw ? wtot[w + 1] : ident;
+  __syncthreads();
+  return op(x, after);
+}
+struct MaxOp {
+  template <typename T>
+  __device__ T operator()(T a, T b) const { return a > b ? a : b; }
+};
+struct MinOp {
+  template <typename T>
+  __device__ T operator()(T a, T b) const { return a < b ? a : b; }
+};
+
 __global__ void __launch_bounds__(kFixThreads) k_warp_bounds_fix(int64_t* __restrict__ begin,
                                                                   int nw) {
-  __shared__ int64_t part[kFixThreads];
+  __shared__ int64_t wtot[32];
   const int t = threadIdx.x;
   const int per = (nw + kFixThreads - 1) / kFixThreads;
   // forward over j in [0, nw): inclusive prefix max of begin[j] - j
   int lo = min(nw, t * per), hi = min(nw, lo + per);
   int64_t m = LLONG_MIN;
   for (int j = lo; j < hi; ++j) m = max(m, begin[j] - j);
-  part[t] = m;
-  __syncthreads();
-  for (int d = 1; d < kFixThreads; d <<= 1) {
-    const int64_t o = t >= d ? part[t - d] : LLONG_MIN;
-    __syncthreads();
-    part[t] = max(part[t], o);
-    __syncthreads();
-  }
-  int64_t run = t > 0 ? part[t - 1] : LLONG_MIN;
+  int64_t run = block_excl_fwd<int64_t>(m, LLONG_MIN, MaxOp{}, wtot);
   for (int j = lo; j < hi; ++j) {
     run = max(run, begin[j] - j);
     if (j >= 1) begin[j] = j + run;
@@ -409,15 +466,7 @@ __global__ void __launch_bounds__(kFixThreads) k_warp_bounds_fix(int64_t* __rest
   hi = 1 + min(nw, t * per + per);
   m = LLONG_MAX;
   for (int j = lo; j < hi; ++j) m = min(m, begin[j] - j);
-  part[t] = m;
-  __syncthreads();
-  for (int d = 1; d < kFixThreads; d <<= 1) {
-    const int64_t o = t + d < kFixThreads ? part[t + d] : LLONG_MAX;
-    __syncthreads();
-    part[t] = min(part[t], o);
-    __syncthreads();
-  }
-  run = t + 1 < kFixThreads ? part[t + 1] : LLONG_MAX;
+  run = block_excl_bwd<int64_t>(m, LLONG_MAX, MinOp{}, wtot);
   for (int j = hi - 1; j >= lo; --j) {
     run = min(run, begin[j] - j);
     if (j < nw) begin[j] = j + run;
@@ -547,7 +596,7 @@ __global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __rest
                                                            int32_t* __restrict__ run_last,
                                                            int32_t* __restrict__ run_cnt,
                                                            double* __restrict__ item_val) {
-  __shared__ int part[kFixThreads];
+  __shared__ int wtot[32];
   const int t = threadIdx.x;
   for (int i = t; i < n; i += kFixThreads) {  // per-launch state: no arrivals, idle pair slots
     run_cnt[i] = 0;
@@ -558,32 +607,15 @@ __global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __rest
   int m = -1;
   for (int i = lo; i < hi; ++i)
     if (i == 0 || key[i] != key[i - 1]) m = i;
-  part[t] = m;
-  __syncthreads();
-  for (int d = 1; d < kFixThreads; d <<= 1) {
-    const int o = t >= d ? part[t - d] : -1;
-    __syncthreads();
-    part[t] = max(part[t], o);
-    __syncthreads();
-  }
-  int run = t > 0 ? part[t - 1] : -1;
+  int run = block_excl_fwd<int>(m, -1, MaxOp{}, wtot);
   for (int i = lo; i < hi; ++i) {
     if (i == 0 || key[i] != key[i - 1]) run = i;
     run_first[i] = run;
   }
-  __syncthreads();
   m = INT_MAX;
   for (int i = hi - 1; i >= lo; --i)
     if (i == n - 1 || key[i] != key[i + 1]) m = i;
-  part[t] = m;
-  __syncthreads();
-  for (int d = 1; d < kFixThreads; d <<= 1) {
-    const int o = t + d < kFixThreads ? part[t + d] : INT_MAX;
-    __syncthreads();
-    part[t] = min(part[t], o);
-    __syncthreads();
-  }
-  run = t + 1 < kFixThreads ? part[t + 1] : INT_MAX;
+  run = block_excl_bwd<int>(m, INT_MAX, MinOp{}, wtot);
   for (int i = hi - 1; i >= lo; --i) {
     if (i == n - 1 || key[i] != key[i + 1]) run = i;
     run_last[i] = run;
@@ -594,6 +626,34 @@ __global__ void __launch_bounds__(kFixThreads) k_item_runs(const int64_t* __rest
 // block for a single read-back: row_of_nonzero at two positions (negative
 // query = skip), row_ptr at the first and the closing row, the empty_offset
 // total, the largest head count, the two tile_ptr words, the locality count.
+// format.cpp:42-50 row_of_nonzero by one warp: a 32-ary upper_bound over
+// row_ptr[0, m] (4 rounds of coalesced probes for a million rows instead of
+// 20 dependent loads)
+__device__ int64_t row_of_nonzero_warp(const int64_t* __restrict__ rp, int64_t m, int64_t g) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = m + 1;  // first index in [lo, hi) with rp[idx] > g
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = min(lo + (int64_t)(lane + 1) * step - 1, hi - 1);
+    const uint32_t b = __ballot_sync(kFull, rp[p] > g);
+    if (b == 0) {
+      lo = min(lo + 32 * step, hi);
+    } else {
+      const int f = __ffs(b) - 1;
+      const int64_t nlo = lo + (int64_t)f * step, nhi = min(lo + (int64_t)(f + 1) * step, hi);
+      lo = nlo;
+      hi = nhi;
+    }
+  }
+  const int64_t q = lo + lane;
+  const uint32_t b = __ballot_sync(kFull, q < hi && rp[q] > g);
+  const int64_t idx = b ? lo + __ffs(b) - 1 : hi;
+  int64_t r = idx - 1;
+  r = r < 0 ? 0 : r;
+  return r > m - 1 ? m - 1 : r;
+}
+
+// one CTA of 64 threads: warp 0 and warp 1 find the two rows, thread 0 the rest
 __global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0, int64_t g1,
                           const uint32_t* __restrict__ tile_ptr, int64_t ic,
                           const int64_t* __restrict__ eo_ptr, int64_t pcs,
@@ -602,8 +662,13 @@ __global__ void k_scalars(const int64_t* __restrict__ rp, int64_t m, int64_t g0,
                           const unsigned long long* __restrict__ single_head,
                           int64_t* __restrict__ out) {
   const bool rows = m > 0;
-  out[0] = rows && g0 >= 0 ? row_of_nonzero_dev(rp, m, g0) : -1;
-  out[1] = rows && g1 >= 0 ? row_of_nonzero_dev(rp, m, g1) : -1;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w < 2) {
+    const int64_t g = w == 0 ? g0 : g1;
+    const int64_t r = rows && g >= 0 ? row_of_nonzero_warp(rp, m, g) : -1;
+    if (lane == 0) out[w] = r;
+  }
+  if (threadIdx.x != 0) return;
   out[2] = rows ? rp[tile_ptr[0] & 0x7fffffffu] : -1;
   out[3] = rows ? rp[tile_ptr[ic] & 0x7fffffffu] : -1;
   out[4] = eo_ptr[pcs];
@@ -1031,7 +1096,7 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   const int64_t g1 = nnz > 0 ? nnz - 1 : -1;
   int64_t sv[4] = {-1, -1, -1, -1};
   int64_t hs[10];
-  k_scalars<<<1, 1, 0, side>>>(h->row_ptr, m, g0, g1, h->tile_ptr, ic, h->eo_ptr, pcs, max_heads_d,
+  k_scalars<<<1, 64, 0, side>>>(h->row_ptr, m, g0, g1, h->tile_ptr, ic, h->eo_ptr, pcs, max_heads_d,
                                reinterpret_cast<const unsigned long long*>(scal + 4), single_head_d,
                                scal + 11);
   TRYC(cudaGetLastError());
