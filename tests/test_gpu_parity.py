@@ -488,3 +488,27 @@ def test_gather_orders_give_identical_y(g, orc, sigma, monkeypatch):
     for mode, y in ys.items():
         assert np.array_equal(y.view(np.int64), ys["1"].view(np.int64)), mode
     assert_y_close(ys["8"], orc.spmv(a, x, 32, sigma), a, x, "csr-order gathers")
+
+
+def test_nf_kernel_multi_tile_warps(g, orc, monkeypatch):
+    """The NF kernel's lean write-back and run merge (every NF tile has >= 2
+    heads; only the last head carries over) with many tiles per warp: a
+    200^2 Laplacian (1,245 tiles) on 1, 2 and 5 warps per CTA -- y against
+    the oracle, and bit-identical across the warp splits (partition-invariant
+    deterministic mode)."""
+    from oracle.oracle import stencil
+    a = stencil(orc, 0, 200, 200)
+    sigma = orc.select_sigma(a.nnz / a.m)
+    x = orc.rng(8).random_x(a.n)
+    y_ref = orc.spmv(a, x, 32, sigma)
+    ys = []
+    for nw in (1, 2, 5):
+        monkeypatch.setenv("CSR5G_NW", str(nw))
+        a5 = gpu_build(g, a, sigma)
+        assert a5.info.kernel_variant == 2 and a5.info.warps_per_cta == nw
+        y = gpu_y(g, a5, x)
+        assert_y_close(y, y_ref, a, x, f"nf nw={nw}")
+        ys.append(y)
+        a5.release()
+    for y in ys[1:]:
+        assert np.array_equal(y.view(np.int64), ys[0].view(np.int64))
