@@ -761,18 +761,21 @@ int dev_alloc(T** p, size_t count, double* alloc_ms, int64_t* bytes) {
 }
 
 // CSR5G_TRACE=1: synchronise after each build phase and print the phase times
-// to stderr (a profiling aid; off by default, no syncs added when off).
+// to stderr (a profiling aid; off by default, no syncs added when off);
+// CSR5G_TRACE=2: the host-side time of each phase, without the syncs.
 struct BuildTrace {
   bool on;
   cudaStream_t st;
   std::chrono::steady_clock::time_point last;
   std::string log;
+  bool host_only = false;  // CSR5G_TRACE=2: host (enqueue) time per phase, no syncs
   explicit BuildTrace(cudaStream_t s) : on(std::getenv("CSR5G_TRACE") != nullptr), st(s) {
+    host_only = on && std::atoi(std::getenv("CSR5G_TRACE")) == 2;
     last = std::chrono::steady_clock::now();
   }
   void mark(const char* what) {
     if (!on) return;
-    cudaStreamSynchronize(st);
+    if (!host_only) cudaStreamSynchronize(st);
     const auto t = std::chrono::steady_clock::now();
     char buf[96];
     std::snprintf(buf, sizeof buf, " %s=%.3fms", what,

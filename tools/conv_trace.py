@@ -26,7 +26,8 @@ for name in sys.argv[1:]:
         a5.release()
     ts.sort()
     print(f"{name} build ms: min {ts[0]:.3f} median {ts[len(ts) // 2]:.3f}", flush=True)
-    os.environ["CSR5G_TRACE"] = "1"
-    for _ in range(3):
-        csr5.csr_to_csr5(a, csr5.TuningParams(sigma=sigma)).release()
-    del os.environ["CSR5G_TRACE"]
+    for mode in ("1", "2"):
+        os.environ["CSR5G_TRACE"] = mode
+        for _ in range(3):
+            csr5.csr_to_csr5(a, csr5.TuningParams(sigma=sigma)).release()
+        del os.environ["CSR5G_TRACE"]
