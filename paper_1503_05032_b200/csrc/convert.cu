@@ -301,38 +301,13 @@ __global__ void k_eo(const uint32_t* __restrict__ head_bits, const uint32_t* __r
   }
 }
 
-// Per-tile SpMV work in nonzero-equivalents, for the warps' tile ranges:
+// Per-tile SpMV work in nonzero-equivalents, for the warps' tile ranges (k_tile_scan):
 // B (stream + gathers) + w_head * heads + w_row * rows spanned (y stores,
 // empty rows zeroed).  Tiles spanning many short and empty rows cost several
 // times a tile of long rows; an equal-tile split gives the warps holding them
 // (unpermuted power-law matrices: the whole tail) most of the work.  Measured
 // on R-MAT s24 unpermuted: equal split 4.42 ms; weights (head, row) = (1,0)
 // 3.90, (0,1) 1.91, (1,1) 1.87, (4,2) 1.79 ms.
-__global__ void k_tile_work(const uint32_t* __restrict__ head_bits,
-                            const uint32_t* __restrict__ tile_ptr, int64_t pcs, int sigma,
-                            int w_head, int w_row, int64_t* __restrict__ work,
-                            int64_t* __restrict__ eo_cnt, int* __restrict__ max_heads,
-                            unsigned long long* __restrict__ single_head) {
-  __shared__ int bmax;
-  __shared__ unsigned int bone;
-  if (threadIdx.x == 0) bmax = 0, bone = 0;
-  __syncthreads();
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < pcs) {
-    const uint32_t* wd = head_bits + t * sigma;  // a tile is sigma 32-bit words
-    int heads = (wd[0] & 1u) ? 0 : 1;           // bf[0] is forced
-    for (int i = 0; i < sigma; ++i) heads += __popc(wd[i]);
-    const uint32_t tp = tile_ptr[t];
-    const int64_t rows = (int64_t)(tile_ptr[t + 1] & 0x7fffffffu) - (tp & 0x7fffffffu) + 1;
-    work[t] = 32ll * sigma + (int64_t)w_head * heads + (int64_t)w_row * rows;
-    eo_cnt[t] = (tp >> 31) ? heads : 0;  // empty_offset entries: heads of flagged tiles
-    atomicMax(&bmax, heads);
-    if (heads == 1) atomicAdd(&bone, 1u);  // a tile inside one row (long rows need one)
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && bmax > 0) atomicMax(max_heads, bmax);
-  if (threadIdx.x == 0 && bone > 0) atomicAdd(single_head, (unsigned long long)bone);
-}
 
 // Largest per-warp work of the equal-tile split (atomicMax into *out).
 __global__ void k_equal_split_max(const int64_t* __restrict__ prefix, int64_t pcs, int nw,
@@ -445,6 +420,121 @@ struct MinOp {
   template <typename T>
   __device__ T operator()(T a, T b) const { return a < b ? a : b; }
 };
+
+struct AddOp {
+  template <typename T>
+  __device__ T operator()(T a, T b) const { return a + b; }
+};
+
+// ---- per-tile work and both prefix sums in one pass --------------------------
+// k_tile_scan replaces k_tile_work and the two CUB scans (empty_offset_ptr,
+// exclusive, format.cpp:213-217; the warp split's work prefix, inclusive):
+// a single-pass chained scan with decoupled look-back.  Each CTA takes the
+// next chunk of kScanTiles tiles (a dynamic chunk index, so every predecessor
+// of a chunk has started), publishes its aggregate, sums its predecessors'
+// published values back to the first inclusive prefix, and writes its tiles'
+// prefixes -- one launch instead of five on the converter's critical path.
+constexpr int kScanThreads = 256, kScanPer = 4, kScanTiles = kScanThreads * kScanPer;
+struct ScanStatus {  // flag 0 nothing yet, 1 aggregate published, 2 inclusive prefix published
+  unsigned long long flag;
+  long long agg_e, agg_w;  // written once, before flag 1 (never changed afterwards)
+  long long inc_e, inc_w;  // written once, before flag 2
+};
+
+__global__ void __launch_bounds__(kScanThreads) k_tile_scan(
+    const uint32_t* __restrict__ head_bits, const uint32_t* __restrict__ tile_ptr, int64_t pcs,
+    int sigma, int w_head, int w_row, ScanStatus* status, unsigned int* chunk_ctr,
+    int64_t* __restrict__ eo_ptr, int64_t* __restrict__ work_prefix, int* __restrict__ max_heads,
+    unsigned long long* __restrict__ single_head) {
+  __shared__ int64_t wtot[32];
+  __shared__ int64_t pre_e, pre_w;
+  __shared__ unsigned int chunk;
+  __shared__ int bmax;
+  __shared__ unsigned int bone;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    chunk = atomicAdd(chunk_ctr, 1u);
+    bmax = 0, bone = 0;
+  }
+  __syncthreads();
+  const int64_t b = chunk;
+  const int64_t k0 = b * kScanTiles + (int64_t)t * kScanPer;
+  int64_t ec[kScanPer], wk[kScanPer], se = 0, sw = 0;
+  int mh = 0;
+  unsigned one = 0;
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i) {
+    const int64_t k = k0 + i;
+    ec[i] = wk[i] = 0;
+    if (k < pcs) {
+      const uint32_t* wd = head_bits + k * sigma;  // a tile is sigma 32-bit words
+      int h = (wd[0] & 1u) ? 0 : 1;                // bf[0] is forced
+      for (int j = 0; j < sigma; ++j) h += __popc(wd[j]);
+      const uint32_t tp = tile_ptr[k];
+      const int64_t rows = (int64_t)(tile_ptr[k + 1] & 0x7fffffffu) - (tp & 0x7fffffffu) + 1;
+      wk[i] = 32ll * sigma + (int64_t)w_head * h + (int64_t)w_row * rows;
+      ec[i] = (tp >> 31) ? h : 0;  // empty_offset entries: heads of flagged tiles
+      mh = max(mh, h);
+      one += h == 1;  // a tile inside one row (long rows need one)
+    }
+    se += ec[i];
+    sw += wk[i];
+  }
+  if (mh) atomicMax(&bmax, mh);
+  if (one) atomicAdd(&bone, one);
+  int64_t xe = block_excl_fwd<int64_t>(se, 0, AddOp{}, wtot);
+  int64_t xw = block_excl_fwd<int64_t>(sw, 0, AddOp{}, wtot);
+  if (t == kScanThreads - 1) {  // the chunk's aggregate: publish, then look back
+    const int64_t ae = xe + se, aw = xw + sw;
+    volatile ScanStatus* st = status + b;
+    int64_t pe = 0, pw = 0;
+    if (b == 0) {
+      st->inc_e = ae, st->inc_w = aw;
+      __threadfence();
+      st->flag = 2;
+    } else {
+      st->agg_e = ae, st->agg_w = aw;
+      __threadfence();
+      st->flag = 1;
+      // a predecessor's flag may move from 1 to 2 at any time: read the field
+      // pair that the flag seen names (each is written once, before its flag)
+      for (int64_t j = b - 1; j >= 0; --j) {
+        volatile ScanStatus* q = status + j;
+        unsigned long long f;
+        while ((f = q->flag) == 0) {
+        }
+        __threadfence();
+        if (f == 2) {
+          pe += q->inc_e;
+          pw += q->inc_w;
+          break;
+        }
+        pe += q->agg_e;
+        pw += q->agg_w;
+      }
+      st->inc_e = pe + ae, st->inc_w = pw + aw;
+      __threadfence();
+      st->flag = 2;
+    }
+    pre_e = pe, pre_w = pw;
+    if (b == (pcs - 1) / kScanTiles) eo_ptr[pcs] = pe + ae;  // the last chunk closes eo_ptr
+  }
+  __syncthreads();
+  xe += pre_e;
+  xw += pre_w;
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i) {
+    const int64_t k = k0 + i;
+    if (k < pcs) {
+      eo_ptr[k] = xe;
+      xe += ec[i];
+      xw += wk[i];
+      work_prefix[k] = xw;
+    }
+  }
+  if (t == 0 && bmax > 0) atomicMax(max_heads, bmax);
+  if (t == 0 && bone > 0) atomicAdd(single_head, (unsigned long long)bone);
+}
 
 __global__ void __launch_bounds__(kFixThreads) k_warp_bounds_fix(int64_t* __restrict__ begin,
                                                                   int nw) {
@@ -910,16 +1000,13 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   int64_t* eo_cnt = nullptr;
   int64_t* scal = nullptr;
   char* zblock = nullptr;  // head_bits | empty_bits | eo_cnt | scal, zeroed by one memset
-  void* cub_tmp = nullptr;
-  void* cub_tmp2 = nullptr;
   int64_t* work_prefix = nullptr;
-  int64_t* work = nullptr;
   int64_t* item_key = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   auto cleanup = [&](int code) {
     if (side && code) cudaStreamSynchronize(side);  // error path: side work may be in flight
-    for (void* p : {(void*)zblock, cub_tmp, cub_tmp2, (void*)work_prefix, (void*)work,
+    for (void* p : {(void*)zblock, (void*)work_prefix,
                     (void*)item_key})
       if (p) cudaFreeAsync(p, stream);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -953,7 +1040,10 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   // scalars (4 lines, 6 emax, 8 max heads, 10-18 the values read back)
   const size_t hb_bytes = ((size_t)head_words * 4 + 7) / 8 * 8;
   const size_t eb_bytes = ((size_t)empty_words * 4 + 7) / 8 * 8;
-  const size_t zbytes = hb_bytes + eb_bytes + 8 * ((size_t)pcs + 1) + 8 * 22;
+  // + the chained scan's per-chunk status and chunk counter (k_tile_scan)
+  const int64_t scan_chunks = (pcs + kScanTiles - 1) / kScanTiles;
+  const size_t zbytes = hb_bytes + eb_bytes + 8 * ((size_t)pcs + 1) + 8 * 22 +
+                        sizeof(ScanStatus) * (size_t)scan_chunks + 16;
   TRY(dev_alloc(&zblock, zbytes, &alloc_ms, &tmp_bytes));
   head_bits = reinterpret_cast<uint32_t*>(zblock);
   empty_bits = reinterpret_cast<uint32_t*>(zblock + hb_bytes);
@@ -1055,27 +1145,15 @@ int build_handle(int device, int64_t m, int64_t n, int64_t nnz, const int64_t* d
   int* max_heads_d = reinterpret_cast<int*>(scal + 8);  // zeroed with the block
   auto* single_head_d = reinterpret_cast<unsigned long long*>(scal + 9);
   if (pcs > 0) {
-    TRY(dev_alloc(&work, (size_t)pcs, &alloc_ms, &tmp_bytes));
-    k_tile_work<<<(unsigned)((pcs + 255) / 256), 256, 0, side>>>(head_bits, h->tile_ptr, pcs,
-                                                                 (int)sigma, w_head, w_row, work,
-                                                                 eo_cnt, max_heads_d,
-                                                                 single_head_d);
-    TRYC(cudaGetLastError());
-  }
-  size_t cub_bytes = 0;
-  TRYC(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, eo_cnt, h->eo_ptr, (int)(pcs + 1), side));
-  TRY(dev_alloc(reinterpret_cast<char**>(&cub_tmp), cub_bytes, &alloc_ms, &tmp_bytes));
-  TRYC(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, eo_cnt, h->eo_ptr, (int)(pcs + 1), side));
-  if (pcs > 0) {
     TRY(dev_alloc(&work_prefix, (size_t)pcs, &alloc_ms, &tmp_bytes));
-    size_t need = 0;
-    TRYC(cub::DeviceScan::InclusiveSum(nullptr, need, work, work_prefix, (int)pcs, side));
-    void* t2 = cub_tmp;
-    if (need > cub_bytes) {
-      TRY(dev_alloc(reinterpret_cast<char**>(&cub_tmp2), need, &alloc_ms, &tmp_bytes));
-      t2 = cub_tmp2;
-    }
-    TRYC(cub::DeviceScan::InclusiveSum(t2, need, work, work_prefix, (int)pcs, side));
+    auto* status = reinterpret_cast<ScanStatus*>(scal + 22);  // zeroed with the block
+    auto* chunk_ctr = reinterpret_cast<unsigned int*>(status + scan_chunks);
+    k_tile_scan<<<(unsigned)scan_chunks, kScanThreads, 0, side>>>(
+        head_bits, h->tile_ptr, pcs, (int)sigma, w_head, w_row, status, chunk_ctr, h->eo_ptr,
+        work_prefix, max_heads_d, single_head_d);
+    TRYC(cudaGetLastError());
+  } else {
+    TRYC(cudaMemsetAsync(h->eo_ptr, 0, sizeof(int64_t), side));  // eo_ptr = {0}
   }
 
   // gather locality over up to 4096 sampled tiles (drives the SpMV plan), from
