@@ -819,8 +819,12 @@ def measure_sharded(args, name, workload, dev, local, dist, rank, world):
                        # NVLink bytes each GPU sends per step (DESIGN §6 model):
                        # the boundary partial (16 B + flags) per shard edge, and in
                        # the fused iterative mode its owned rows of y to every peer
+                       # (NVLS multicast: one multimem store per value, replicated
+                       # by the switch -- 8 bytes per owned row leave the GPU)
+                       "nvls_multicast": bool(getattr(sh, "mcast", False)),
                        "nvlink_out_bytes_per_step_per_gpu": (
-                           8 * (own[1] - own[0]) * (world - 1)
+                           (8 * (own[1] - own[0]) * (1 if getattr(sh, "mcast", False)
+                                                     else world - 1))
                            if args.iterative and sh.iterative else 16 + 8),
                        "parallelism": f"tile-range shards x{world}, x replicated",
                        "l2": f"L2 flushed between timed calls ({2 * l2_bytes / 1e6:.0f} MB read)",

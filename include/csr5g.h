@@ -171,6 +171,24 @@ CSR5G_API int csr5g_mailbox_link_local(csr5g_mailbox mb, int32_t peer, csr5g_mai
 CSR5G_API int csr5g_mailbox_errors(csr5g_mailbox mb, uint32_t *errors);
 CSR5G_API int csr5g_mailbox_release(csr5g_mailbox mb);
 /* active_world: ranks holding tiles (0 .. active_world-1) */
+/* NVSwitch multicast (NVLS) for the fused iterative mode: every rank's x
+ * ping-pong bound to one multicast object, so each mirror store is one
+ * multimem.st the switch replicates (instead of G-1 peer stores).  Order:
+ * rank 0 _create (exports a 64-byte fabric handle when ndev > 1), the others
+ * _import it, every rank _add (its device), a barrier, every rank _bind, a
+ * barrier.  After _bind, csr5g_mailbox_vector returns the bound buffers.
+ * Any failure leaves the peer-store path; _release drops the object.
+ * (No reference counterpart: the reference has no distributed backend.) */
+CSR5G_API int csr5g_mcast_supported(int device, int32_t *out);
+CSR5G_API int csr5g_mailbox_mcast_create(csr5g_mailbox mb, int32_t ndev, void *handle64);
+CSR5G_API int csr5g_mailbox_mcast_import(csr5g_mailbox mb, int32_t ndev, const void *handle64);
+CSR5G_API int csr5g_mailbox_mcast_add(csr5g_mailbox mb);
+CSR5G_API int csr5g_mailbox_mcast_bind(csr5g_mailbox mb);
+CSR5G_API int csr5g_mailbox_mcast_release(csr5g_mailbox mb);
+/* test hook: multimem stores into x buffer 1's multicast mapping, then the
+ * values that did not land in this rank's bound copy */
+CSR5G_API int csr5g_mailbox_mcast_selftest(csr5g_mailbox mb, int64_t *mismatches);
+
 CSR5G_API int csr5g_mg_bind(csr5g_matrix h, csr5g_mailbox mb, int32_t dest, int32_t sender_begin,
                             int32_t sender_end, int32_t active_world);
 CSR5G_API int csr5g_mg_spmv_post(csr5g_matrix h, const double *d_x, double *d_y, void *stream,

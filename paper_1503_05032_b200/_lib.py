@@ -81,6 +81,13 @@ SIGNATURES = {
     "csr5g_mailbox_link_local": (C.c_int, [_vp, _i32, _vp]),
     "csr5g_mailbox_errors": (C.c_int, [_vp, C.POINTER(C.c_uint32)]),
     "csr5g_mailbox_release": (C.c_int, [_vp]),
+    "csr5g_mcast_supported": (C.c_int, [C.c_int, C.POINTER(C.c_int32)]),
+    "csr5g_mailbox_mcast_create": (C.c_int, [_vp, _i32, _vp]),
+    "csr5g_mailbox_mcast_import": (C.c_int, [_vp, _i32, _vp]),
+    "csr5g_mailbox_mcast_add": (C.c_int, [_vp]),
+    "csr5g_mailbox_mcast_bind": (C.c_int, [_vp]),
+    "csr5g_mailbox_mcast_release": (C.c_int, [_vp]),
+    "csr5g_mailbox_mcast_selftest": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "csr5g_mg_bind": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32]),
     "csr5g_mg_spmv_post": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "csr5g_mg_spmv_fixup": (C.c_int, [_vp, _vp, _vp]),

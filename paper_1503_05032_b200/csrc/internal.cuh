@@ -34,13 +34,23 @@ constexpr uint32_t kFull = 0xffffffffu;
 // whose value here is still partial (an owner's boundary row before the
 // fix-up, which mirrors the total itself).
 constexpr int kMaxMirror = 7;  // one NVSwitch box: 8 GPUs
+// mc: the NVLS multicast mapping of every rank's next-x buffer (p2p.cu): one
+// multimem store reaches all of them through the switch, instead of n peer
+// stores over NVLink.
 struct Mirrors {
   double* p[kMaxMirror];
   int32_t n;
   int64_t skip_row;
+  double* mc;
 };
 
+__host__ __device__ __forceinline__ bool mir_on(const Mirrors& m) { return m.n != 0 || m.mc != nullptr; }
+
 __device__ __forceinline__ void mirror_store(const Mirrors& m, int64_t r, double v) {
+  if (m.mc) {
+    asm volatile("multimem.st.global.f64 [%0], %1;" ::"l"(m.mc + r), "d"(v) : "memory");
+    return;
+  }
 #pragma unroll
   for (int g = 0; g < kMaxMirror; ++g)
     if (g < m.n) m.p[g][r] = v;

@@ -29,6 +29,13 @@
 // then separates the two phases with a host barrier, so every wait is already
 // satisfied when it is enqueued (B200_PROFILING: no cross-rank waits on one GPU).
 //
+// NVLS variant of the fused mode (csr5g_mailbox_mcast_*): the x ping-pong of
+// every rank is bound to one NVSwitch multicast object; a kernel's mirror
+// store is a single multimem.st to the multicast mapping, which the switch
+// replicates to every rank's copy -- 8 bytes out per value instead of
+// 8 * (G - 1).  The flags stay peer-to-peer.  Built only where the device
+// reports multicast support; any failure leaves the peer-store path.
+//
 // Fused iterative mode (y -> x, square A).  Instead of an all-gather of the
 // owned y ranges after the SpMV, every kernel that stores a final y value
 // (tile write-back, tail rows, calibration, fix-up) also stores it into each
@@ -43,8 +50,10 @@
 //   xready[r] = k + 1 on every peer.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "internal.cuh"
 
@@ -62,20 +71,28 @@ struct MailboxDev {
 constexpr size_t kVecOffset = 4096;  // x buffers follow the header in one allocation
 static_assert(sizeof(MailboxDev) <= kVecOffset, "mailbox header");
 
+struct Mcast;  // NVSwitch multicast of the x ping-pong (end of this file)
+
 struct Mailbox {
   int device = 0, world = 0, rank = 0;
   int64_t vec_len = 0;                    // x buffers (iterative mode), 0 = none
+  Mcast* mc = nullptr;                    // multicast x buffers (end of this file), or none
+  double* mc_local = nullptr;             // ... their unicast mapping here
+  double* mc_multi = nullptr;             // ... and the multicast mapping (every rank's copy)
   MailboxDev* local = nullptr;            // this rank's mailbox (own HBM)
   MailboxDev* peer[kMaxWorld] = {};       // every rank's mailbox, mapped here
   bool ipc_opened[kMaxWorld] = {};
   uint32_t** d_peer_ack = nullptr;        // device table: &peer[g]->ack
   uint32_t** d_peer_xready = nullptr;     // device table: &peer[g]->xready[rank]
   double* vec(const MailboxDev* d, int64_t which) const {
+    if (d == local && mc_local) return mc_local + (which & 1) * vec_len;
     return reinterpret_cast<double*>(reinterpret_cast<char*>(const_cast<MailboxDev*>(d)) +
                                      kVecOffset) +
            (which & 1) * vec_len;
   }
 };
+
+void mcast_free(Mailbox* m);  // multicast teardown (end of this file)
 
 struct Binding {
   Mailbox* mb = nullptr;
@@ -213,8 +230,12 @@ Mirrors iter_mirrors(Handle* h, int64_t it) {
   Binding* b = h->mg;
   Mailbox* m = b->mb;
   Mirrors mir{};
-  for (int g = 0; g < b->active; ++g)
-    if (g != m->rank) mir.p[mir.n++] = m->vec(m->peer[g], it + 1);
+  if (m->mc_multi) {  // one multimem store per value reaches every rank's copy
+    mir.mc = m->mc_multi + ((it + 1) & 1) * m->vec_len;
+  } else {
+    for (int g = 0; g < b->active; ++g)
+      if (g != m->rank) mir.p[mir.n++] = m->vec(m->peer[g], it + 1);
+  }
   mir.skip_row = b->se > b->sb ? h->last_row : -1;
   return mir;
 }
@@ -397,6 +418,7 @@ int csr5g_mailbox_release(csr5g_mailbox mb) {
   Mailbox* m = mb->m;
   cudaSetDevice(m->device);
   cudaDeviceSynchronize();
+  mcast_free(m);
   for (int g = 0; g < m->world; ++g)
     if (m->ipc_opened[g]) cudaIpcCloseMemHandle(m->peer[g]);
   cudaFree(m->d_peer_ack);
@@ -472,3 +494,303 @@ int csr5g_mg_iter(csr5g_matrix h, int64_t it, void* stream, void* ev0, void* ev1
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// NVSwitch multicast (NVLS) of the x ping-pong, fused iterative mode
+// ---------------------------------------------------------------------------
+namespace csr5g {
+
+struct Mcast {
+  CUmemGenericAllocationHandle mc = 0, mem = 0;
+  CUmemAllocationHandleType ht = CU_MEM_HANDLE_TYPE_NONE;  // shareable type of both
+  CUdeviceptr local_va = 0, mc_va = 0;
+  size_t bytes = 0;
+  int ndev = 0;
+  bool have_mc = false, have_mem = false, local_mapped = false, mc_mapped = false, bound = false;
+};
+
+namespace {
+
+// driver entry points (no -lcuda: the runtime hands them out)
+struct Drv {
+  CUresult (*mc_create)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+  CUresult (*mc_add)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+  CUresult (*mc_bind)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t,
+                      size_t, unsigned long long) = nullptr;
+  CUresult (*mc_unbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+  CUresult (*mc_gran)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) = nullptr;
+  CUresult (*mem_create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*,
+                         unsigned long long) = nullptr;
+  CUresult (*mem_gran)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*mem_release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*va_reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*va_free)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*export_h)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType,
+                       unsigned long long) = nullptr;
+  CUresult (*import_h)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType) = nullptr;
+  CUresult (*dev_get)(CUdevice*, int) = nullptr;
+  CUresult (*dev_attr)(int*, CUdevice_attribute, CUdevice) = nullptr;
+};
+
+int drv(const Drv** out) {
+  static Drv d;
+  static cudaError_t rc = [] {
+    auto get = [](const char* name, auto** fn) {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q{};
+      cudaError_t e = cudaGetDriverEntryPointByVersion(name, &p, CUDA_VERSION, cudaEnableDefault, &q);
+      if (e == cudaSuccess && q != cudaDriverEntryPointSuccess) e = cudaErrorNotSupported;
+      *fn = reinterpret_cast<std::remove_pointer_t<decltype(fn)>>(p);
+      return e;
+    };
+    cudaError_t e = cudaSuccess;
+    for (cudaError_t r : {get("cuMulticastCreate", &d.mc_create), get("cuMulticastAddDevice", &d.mc_add),
+                          get("cuMulticastBindMem", &d.mc_bind), get("cuMulticastUnbind", &d.mc_unbind),
+                          get("cuMulticastGetGranularity", &d.mc_gran), get("cuMemCreate", &d.mem_create),
+                          get("cuMemGetAllocationGranularity", &d.mem_gran),
+                          get("cuMemRelease", &d.mem_release), get("cuMemAddressReserve", &d.va_reserve),
+                          get("cuMemAddressFree", &d.va_free), get("cuMemMap", &d.map),
+                          get("cuMemUnmap", &d.unmap), get("cuMemSetAccess", &d.set_access),
+                          get("cuMemExportToShareableHandle", &d.export_h),
+                          get("cuMemImportFromShareableHandle", &d.import_h),
+                          get("cuDeviceGet", &d.dev_get), get("cuDeviceGetAttribute", &d.dev_attr)})
+      if (r != cudaSuccess) e = r;
+    return e;
+  }();
+  if (rc != cudaSuccess) return cuda_fail(rc, "cudaGetDriverEntryPoint (multicast / VMM)");
+  *out = &d;
+  return CSR5G_OK;
+}
+
+int cu_fail(CUresult r, const char* what) {
+  return fail(CSR5G_ECUDA, std::string(what) + " failed (CUresult " + std::to_string((int)r) + ")");
+}
+#define CSR5G_CU(call)                              \
+  do {                                              \
+    const CUresult r_ = (call);                     \
+    if (r_ != CUDA_SUCCESS) return cu_fail(r_, #call); \
+  } while (0)
+
+CUmulticastObjectProp mc_prop(int ndev, size_t bytes, CUmemAllocationHandleType ht) {
+  CUmulticastObjectProp p{};
+  p.numDevices = (unsigned)ndev;
+  p.size = bytes;
+  p.handleTypes = (unsigned long long)ht;
+  p.flags = 0;
+  return p;
+}
+
+// the x ping-pong's size rounded to both granularities
+int mc_size(const Drv* d, int device, int ndev, int64_t vec_len, CUmemAllocationHandleType ht,
+            size_t* bytes) {
+  CUmulticastObjectProp mp = mc_prop(ndev, 1, ht);
+  size_t g1 = 0, g2 = 0;
+  CSR5G_CU(d->mc_gran(&g1, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = device;
+  ap.requestedHandleTypes = ht;
+  CSR5G_CU(d->mem_gran(&g2, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  const size_t g = std::max<size_t>(std::max<size_t>(g1, g2), 1);
+  const size_t want = sizeof(double) * 2 * (size_t)vec_len;
+  *bytes = (want + g - 1) / g * g;
+  return CSR5G_OK;
+}
+
+int map_rw(const Drv* d, int device, CUmemGenericAllocationHandle h, size_t bytes, CUdeviceptr* va) {
+  CSR5G_CU(d->va_reserve(va, bytes, 0, 0, 0));
+  CUresult r = d->map(*va, bytes, 0, h, 0);
+  if (r == CUDA_SUCCESS) {
+    CUmemAccessDesc a{};
+    a.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    a.location.id = device;
+    a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    r = d->set_access(*va, bytes, &a, 1);
+    if (r != CUDA_SUCCESS) d->unmap(*va, bytes);
+  }
+  if (r != CUDA_SUCCESS) {
+    d->va_free(*va, bytes);
+    *va = 0;
+    return cu_fail(r, "cuMemMap / cuMemSetAccess");
+  }
+  return CSR5G_OK;
+}
+
+}  // namespace
+
+void mcast_free(Mailbox* m) {
+  Mcast* c = m->mc;
+  if (!c) return;
+  const Drv* d = nullptr;
+  if (drv(&d) == CSR5G_OK) {
+    CUdevice dev = 0;
+    d->dev_get(&dev, m->device);
+    if (c->mc_mapped) d->unmap(c->mc_va, c->bytes), d->va_free(c->mc_va, c->bytes);
+    if (c->local_mapped) d->unmap(c->local_va, c->bytes), d->va_free(c->local_va, c->bytes);
+    if (c->bound) d->mc_unbind(c->mc, dev, 0, c->bytes);
+    if (c->have_mem) d->mem_release(c->mem);
+    if (c->have_mc) d->mem_release(c->mc);
+  }
+  m->mc_local = m->mc_multi = nullptr;
+  delete c;
+  m->mc = nullptr;
+}
+
+}  // namespace csr5g
+
+int csr5g_mcast_supported(int device, int32_t* out) {
+  if (!out) return fail(CSR5G_EINVAL, "csr5g: out is NULL");
+  *out = 0;
+  const Drv* d = nullptr;
+  if (int rc = drv(&d)) return rc;
+  CUdevice dev = 0;
+  CSR5G_CU(d->dev_get(&dev, device));
+  int v = 0;
+  CSR5G_CU(d->dev_attr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev));
+  *out = v;
+  return CSR5G_OK;
+}
+
+int csr5g_mailbox_mcast_create(csr5g_mailbox mb, int32_t ndev, void* handle64) {
+  if (!mb || ndev < 1) return fail(CSR5G_EINVAL, "csr5g: bad multicast arguments");
+  Mailbox* m = mb->m;
+  if (m->mc) return fail(CSR5G_EINVAL, "csr5g: the mailbox already has a multicast object");
+  if (m->vec_len <= 0) return fail(CSR5G_EINVAL, "csr5g: mailbox has no x buffers");
+  const Drv* d = nullptr;
+  if (int rc = drv(&d)) return rc;
+  CSR5G_CUDA(cudaSetDevice(m->device));
+  auto* c = new Mcast;
+  c->ndev = ndev;
+  m->mc = c;
+  // several processes need a fabric handle; one process takes the first
+  // handle type the driver accepts
+  CUresult r = CUDA_ERROR_NOT_SUPPORTED;
+  for (CUmemAllocationHandleType ht :
+       {CU_MEM_HANDLE_TYPE_FABRIC, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, CU_MEM_HANDLE_TYPE_NONE}) {
+    if (ndev > 1 && ht != CU_MEM_HANDLE_TYPE_FABRIC) break;
+    if (mc_size(d, m->device, ndev, m->vec_len, ht, &c->bytes) != CSR5G_OK) continue;
+    const CUmulticastObjectProp p = mc_prop(ndev, c->bytes, ht);
+    r = d->mc_create(&c->mc, &p);
+    if (r == CUDA_SUCCESS) {
+      c->ht = ht;
+      break;
+    }
+  }
+  if (r != CUDA_SUCCESS) return mcast_free(m), cu_fail(r, "cuMulticastCreate");
+  c->have_mc = true;
+  if (ndev > 1) {
+    if (!handle64) return mcast_free(m), fail(CSR5G_EINVAL, "csr5g: handle64 is NULL");
+    r = d->export_h(handle64, c->mc, CU_MEM_HANDLE_TYPE_FABRIC, 0);
+    if (r != CUDA_SUCCESS) return mcast_free(m), cu_fail(r, "cuMemExportToShareableHandle (fabric)");
+  }
+  return CSR5G_OK;
+}
+
+int csr5g_mailbox_mcast_import(csr5g_mailbox mb, int32_t ndev, const void* handle64) {
+  if (!mb || !handle64 || ndev < 2) return fail(CSR5G_EINVAL, "csr5g: bad multicast arguments");
+  Mailbox* m = mb->m;
+  if (m->mc) return fail(CSR5G_EINVAL, "csr5g: the mailbox already has a multicast object");
+  const Drv* d = nullptr;
+  if (int rc = drv(&d)) return rc;
+  CSR5G_CUDA(cudaSetDevice(m->device));
+  auto* c = new Mcast;
+  c->ndev = ndev;
+  m->mc = c;
+  c->ht = CU_MEM_HANDLE_TYPE_FABRIC;
+  if (int rc = mc_size(d, m->device, ndev, m->vec_len, c->ht, &c->bytes)) return mcast_free(m), rc;
+  const CUresult r = d->import_h(&c->mc, const_cast<void*>(handle64), CU_MEM_HANDLE_TYPE_FABRIC);
+  if (r != CUDA_SUCCESS) return mcast_free(m), cu_fail(r, "cuMemImportFromShareableHandle (fabric)");
+  c->have_mc = true;
+  return CSR5G_OK;
+}
+
+int csr5g_mailbox_mcast_add(csr5g_mailbox mb) {
+  if (!mb || !mb->m->mc) return fail(CSR5G_EINVAL, "csr5g: no multicast object");
+  Mailbox* m = mb->m;
+  const Drv* d = nullptr;
+  if (int rc = drv(&d)) return rc;
+  CUdevice dev = 0;
+  CSR5G_CU(d->dev_get(&dev, m->device));
+  CSR5G_CU(d->mc_add(m->mc->mc, dev));
+  return CSR5G_OK;
+}
+
+// after every rank's device was added: this rank's x ping-pong in fresh
+// device memory, bound to the object, mapped unicast (reads) and multicast
+// (the kernels' mirror stores); the mailbox's x buffers become these
+int csr5g_mailbox_mcast_bind(csr5g_mailbox mb) {
+  if (!mb || !mb->m->mc) return fail(CSR5G_EINVAL, "csr5g: no multicast object");
+  Mailbox* m = mb->m;
+  Mcast* c = m->mc;
+  const Drv* d = nullptr;
+  if (int rc = drv(&d)) return rc;
+  CSR5G_CUDA(cudaSetDevice(m->device));
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = m->device;
+  ap.requestedHandleTypes = c->ht;
+  CSR5G_CU(d->mem_create(&c->mem, c->bytes, &ap, 0));
+  c->have_mem = true;
+  CSR5G_CU(d->mc_bind(c->mc, 0, c->mem, 0, c->bytes, 0));
+  c->bound = true;
+  if (int rc = map_rw(d, m->device, c->mem, c->bytes, &c->local_va)) return rc;
+  c->local_mapped = true;
+  if (int rc = map_rw(d, m->device, c->mc, c->bytes, &c->mc_va)) return rc;
+  c->mc_mapped = true;
+  CSR5G_CUDA(cudaMemset(reinterpret_cast<void*>(c->local_va), 0, c->bytes));
+  m->mc_local = reinterpret_cast<double*>(c->local_va);
+  m->mc_multi = reinterpret_cast<double*>(c->mc_va);
+  return CSR5G_OK;
+}
+
+namespace csr5g {
+namespace {
+__global__ void k_mcast_write(double* mc, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    asm volatile("multimem.st.global.f64 [%0], %1;" ::"l"(mc + i), "d"((double)i * 0.5 + 1.0) : "memory");
+}
+__global__ void k_mcast_check(const double* local, int64_t n, unsigned long long* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (local[i] != (double)i * 0.5 + 1.0) atomicAdd(bad, 1ull);
+}
+}  // namespace
+}  // namespace csr5g
+
+// test hook: multimem stores into the multicast mapping of x buffer 1 land in
+// this rank's bound copy (the count of mismatching values; buffer 1 is left
+// holding the pattern)
+int csr5g_mailbox_mcast_selftest(csr5g_mailbox mb, int64_t* mismatches) {
+  if (!mb || !mismatches || !mb->m->mc_multi) return fail(CSR5G_EINVAL, "csr5g: no bound multicast");
+  Mailbox* m = mb->m;
+  CSR5G_CUDA(cudaSetDevice(m->device));
+  unsigned long long* bad = nullptr;
+  CSR5G_CUDA(cudaMalloc(&bad, sizeof *bad));
+  cudaError_t e = cudaMemset(bad, 0, sizeof *bad);
+  if (e == cudaSuccess) {
+    k_mcast_write<<<264, 256>>>(m->mc_multi + m->vec_len, m->vec_len);
+    e = cudaDeviceSynchronize();
+  }
+  if (e == cudaSuccess) {
+    k_mcast_check<<<264, 256>>>(m->mc_local + m->vec_len, m->vec_len, bad);
+    e = cudaDeviceSynchronize();
+  }
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&h, bad, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(bad);
+  if (e != cudaSuccess) return cuda_fail(e, "csr5g_mailbox_mcast_selftest");
+  *mismatches = (int64_t)h;
+  return CSR5G_OK;
+}
+
+int csr5g_mailbox_mcast_release(csr5g_mailbox mb) {
+  if (!mb) return CSR5G_OK;
+  cudaSetDevice(mb->m->device);
+  cudaDeviceSynchronize();
+  mcast_free(mb->m);
+  return CSR5G_OK;
+}

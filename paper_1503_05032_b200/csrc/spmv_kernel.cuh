@@ -61,7 +61,7 @@ __device__ void rows_part(const SpmvArgs& a) {
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
     if (idx < a.lead_rows) {
       a.y[idx] = 0.0;
-      if (a.mir.n) mirror_store(a.mir, idx, 0.0);
+      if (mir_on(a.mir)) mirror_store(a.mir, idx, 0.0);
       continue;
     }
     const int64_t r = a.tail_row_begin + (idx - a.lead_rows);
@@ -80,7 +80,7 @@ __device__ void rows_part(const SpmvArgs& a) {
       }
     } else {
       a.y[r] = s;
-      if (a.mir.n) mirror_store(a.mir, r, s);
+      if (mir_on(a.mir)) mirror_store(a.mir, r, s);
     }
   }
 }
@@ -106,7 +106,7 @@ __device__ __forceinline__ void write_run(int64_t row, double v, double* y, int6
     }
   } else {
     y[row] = v;
-    if (mir.n && row != mir.skip_row) mirror_store(mir, row, v);
+    if (mir_on(mir) && row != mir.skip_row) mirror_store(mir, row, v);
   }
 }
 
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
   if (has_tiles) {
     double* __restrict__ y = a.y;
     const bool yh = KNOBS && a.y_hint != 0;
-    const bool mirrored = a.mir.n != 0;
+    const bool mirrored = mir_on(a.mir);
     auto put_y = [&](int64_t r, double v) {
       if (TR) return;
       if (yh)

@@ -236,6 +236,7 @@ class Csr5Sharded:
         self.ranges = [(t[4 * g], t[4 * g + 1]) for g in range(world)]
         self.exchange = os.environ.get("CSR5G_EXCHANGE", "p2p")
         self.mailbox = None
+        self.mcast = False
         self.iterative = iterative and self.exchange == "p2p"
         if self.iterative and m != n:
             raise ValueError("iterative mode needs a square matrix")
@@ -270,18 +271,68 @@ class Csr5Sharded:
         all_gather_flat(dist, allu, uid, self.group)
         allu = allu.cpu().numpy().reshape(self.world, 16)
         self.shared_gpu = len({bytes(u) for u in allu}) < self.world
-        if not self.active:
-            return
-        d = self.dest[self.rank]
-        sb, se = self.senders[self.rank]
-        peers = set(([d] if d >= 0 else []) + list(range(sb, se)))
-        if self.iterative:  # every active rank stores its rows of the next x here
-            peers |= set(range(self.world_eff))
-        peers.discard(self.rank)
-        for peer in sorted(peers):
-            h = allh[IPC_HANDLE_BYTES * peer:IPC_HANDLE_BYTES * (peer + 1)]
-            check(L.csr5g_mailbox_open_peer(mb, peer, (C.c_uint8 * IPC_HANDLE_BYTES)(*h.tolist())))
-        check(L.csr5g_mg_bind(self.a5.handle, mb, d, sb, se, self.world_eff))
+        if self.active:
+            d = self.dest[self.rank]
+            sb, se = self.senders[self.rank]
+            peers = set(([d] if d >= 0 else []) + list(range(sb, se)))
+            if self.iterative:  # every active rank stores its rows of the next x here
+                peers |= set(range(self.world_eff))
+            peers.discard(self.rank)
+            for peer in sorted(peers):
+                h = allh[IPC_HANDLE_BYTES * peer:IPC_HANDLE_BYTES * (peer + 1)]
+                check(L.csr5g_mailbox_open_peer(mb, peer,
+                                                (C.c_uint8 * IPC_HANDLE_BYTES)(*h.tolist())))
+            check(L.csr5g_mg_bind(self.a5.handle, mb, d, sb, se, self.world_eff))
+        self.mcast = self.iterative and self._setup_mcast(dev)
+
+    def _agree(self, dev, ok: bool) -> bool:
+        """True when every rank's flag is set (all-gather of one int each)."""
+        torch = self.torch
+        mine = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        allf = torch.zeros(self.world, dtype=torch.int32, device=dev)
+        all_gather_flat(self.dist, allf, mine, self.group)
+        return bool(allf.min().item())
+
+    def _setup_mcast(self, dev) -> bool:
+        """NVSwitch multicast x buffers for the fused iterative mode (p2p.cu,
+        csr5g_mailbox_mcast_*): rank 0 creates the object and exports its
+        fabric handle, the other active ranks import it, every active rank adds
+        its device, then binds its x ping-pong.  Every step is agreed by all
+        ranks; any failure (no multicast, no fabric handles, ranks sharing a
+        GPU) leaves the peer-store path.  Opt-in: CSR5G_MCAST=1."""
+        torch, L = self.torch, lib()
+        # opt-in until it has run on a multi-GPU box: on the one-GPU test box
+        # cuMulticastCreate rejects every configuration (tools/mc_probe_raw.py)
+        want = os.environ.get("CSR5G_MCAST", "0") == "1" and not self.shared_gpu
+        sup = C.c_int32(0)
+        if want and self.active:
+            want = L.csr5g_mcast_supported(dev.index or 0, C.byref(sup)) == 0 and sup.value == 1
+        if not self._agree(dev, want or not self.active):
+            return False
+        n = self.world_eff
+        handle = (C.c_uint8 * 64)()
+        ok = True
+        if self.rank == 0:
+            ok = L.csr5g_mailbox_mcast_create(self.mailbox, n, handle) == 0
+        hb = torch.tensor(list(handle), dtype=torch.uint8, device=dev)
+        allh = torch.zeros(64 * self.world, dtype=torch.uint8, device=dev)
+        all_gather_flat(self.dist, allh, hb, self.group)
+        if not self._agree(dev, ok):
+            return False
+        h0 = (C.c_uint8 * 64)(*allh[:64].cpu().tolist())
+        if self.active and self.rank != 0:
+            ok = L.csr5g_mailbox_mcast_import(self.mailbox, n, h0) == 0
+        if self.active and ok:
+            ok = L.csr5g_mailbox_mcast_add(self.mailbox) == 0
+        if not self._agree(dev, ok):
+            L.csr5g_mailbox_mcast_release(self.mailbox)
+            return False
+        if self.active:  # every device was added before anyone binds
+            ok = L.csr5g_mailbox_mcast_bind(self.mailbox) == 0
+        if not self._agree(dev, ok):
+            L.csr5g_mailbox_mcast_release(self.mailbox)
+            return False
+        return True
 
     def mailbox_errors(self) -> int:
         """Protocol violations seen by this rank's fix-ups (synchronous)."""
