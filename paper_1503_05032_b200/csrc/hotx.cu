@@ -159,17 +159,15 @@ int build_hot_plan(Handle* h, cudaStream_t stream, int64_t* bytes) {
   CSR5G_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device));
   CSR5G_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   if (mode < 0 && (double)n * 8.0 <= 0.75 * (double)l2) return CSR5G_OK;
-  // x several times the L2 (R-MAT s27): hottest first and L1-allocated hot
-  // gathers; x around the L2 (R-MAT s24): ascending column order, no L1
-  // allocation (the other way round measured slower on each,
-  // profiles/r02_hot_sweep.txt)
-  const bool big = (double)n * 8.0 > 3.0 * (double)l2;
-  h->hot_l1 = (int)env_i64("CSR5G_HOT_L1", big ? 1 : 0);
+  // hottest first and L1-allocated hot gathers (GM 3), for x several times
+  // the L2 (R-MAT s27) and around it (R-MAT s24: 1.22 ms against 1.45 for
+  // ascending order without L1 at 16 warps, profiles/r02_hot_sweep.txt r02ap)
+  h->hot_l1 = (int)env_i64("CSR5G_HOT_L1", 1);
   const int64_t hmax = env_i64("CSR5G_HOT_COLS", env_i64("CSR5G_HOT_MB", 64) * (1 << 20) / 8);
   // sample: every entry up to 2^28 of them, then every stride-th
   const int stride = (int)std::max<int64_t>(
       1, env_i64("CSR5G_HOT_STRIDE", (tiled + (int64_t(1) << 28) - 1) >> 28));
-  const bool by_count = env_i64("CSR5G_HOT_ORDER", big ? 1 : 0) != 0;
+  const bool by_count = env_i64("CSR5G_HOT_ORDER", 1) != 0;
 
   uint32_t* cnt = nullptr;
   unsigned long long* hist = nullptr;

@@ -127,7 +127,10 @@ int spmv_plan(Handle* h, int sms) {
     // with hot-column staging most gathers hit the dense staged values in L2
     // and more warps win again: R-MAT s24 10 / 13 / 16 warps (budget 60 / 80 /
     // 100 KB) -> 1.45 / 1.37 / 1.28 ms
-    if (h->n_hot > 0) budget = 100 * 1024;
+    if (h->n_hot > 0) {
+      budget = 100 * 1024;
+      h->x_mode = 5;  // staged hot values L1-allocated, cold ones 64-byte prefetched (GM 3)
+    }
     // x several times the L2 (R-MAT s26/s27: 537 MB / 1.07 GB): the gathers
     // are DRAM-random-access bound.  Issued in CSR order (lane L fetches the
     // tile's logical entry u*32 + L, exchanged into the lane-per-column order

@@ -20,17 +20,19 @@ pytestmark = pytest.mark.gpu
 def _build(d, monkeypatch, **env):
     from paper_1503_05032_b200 import csr5
     for k in ("CSR5G_HOT", "CSR5G_HOT_COLS", "CSR5G_HOT_STRIDE", "CSR5G_HOT_L1", "CSR5G_HOT_ORDER",
-              "CSR5G_XMODE"):
+              "CSR5G_XMODE", "CSR5G_GM"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, str(v))
     return csr5.csr_to_csr5(d, csr5.TuningParams())
 
 
-# the two staged gather paths: x around the L2 (ascending order, no L1
-# allocation: GM 5) and x several times the L2 (hottest first, hot values
-# L1-allocated, cold ones 64-byte prefetched: GM 3), forced on small matrices
-PATHS = {"gm5": {}, "gm3": {"CSR5G_HOT_L1": 1, "CSR5G_HOT_ORDER": 1, "CSR5G_XMODE": 5}}
+# the staged gather paths, forced on small matrices: the plans' default
+# (hottest first, hot values L1-allocated, cold ones 64-byte prefetched:
+# GM 3), the ascending-order path without L1 allocation (GM 5), and the
+# runtime switch (GM 0)
+PATHS = {"gm3": {}, "gm5": {"CSR5G_HOT_L1": 0, "CSR5G_HOT_ORDER": 0, "CSR5G_XMODE": 1},
+         "gm0": {"CSR5G_GM": 0}}
 
 
 @pytest.mark.parametrize("path", sorted(PATHS))
@@ -47,8 +49,7 @@ def test_hot_staging_is_bit_identical(scale, stride, path, orc, monkeypatch):
                  **PATHS[path])
     assert plain.info.kernel_variant == 1, "R-MAT should take the random-gather (VR) plan"
     assert plain.info.hot_cols == 0
-    if path == "gm3":
-        assert hot.info.x_mode == 5
+    assert hot.info.x_mode == (1 if path == "gm5" else 5)
     assert 0 < hot.info.hot_cols <= 2 * (n // 16), hot.info.hot_cols
     assert hot.info.hot_coverage > 0.3, hot.info.hot_coverage  # power law: few columns, most gathers
     # the exported CSR5 arrays are the reference's, not the execution copy
