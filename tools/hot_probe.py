@@ -13,7 +13,7 @@ from paper_1503_05032_b200 import csr5  # noqa: E402
 from paper_1503_05032_b200.synthetic import WORKLOADS, bench_x, make_matrix  # noqa: E402
 
 KNOBS = ("CSR5G_HOT", "CSR5G_HOT_MB", "CSR5G_HOT_ORDER", "CSR5G_HOT_L1", "CSR5G_HOT_COLS", "CSR5G_HOT_STRIDE", "CSR5G_HOT_COLD_POL",
-         "CSR5G_XMODE", "CSR5G_NW", "CSR5G_BUDGET_KB", "CSR5G_GM")
+         "CSR5G_XMODE", "CSR5G_NW", "CSR5G_BUDGET_KB", "CSR5G_GM", "CSR5G_STAGES")
 name, configs = sys.argv[1], sys.argv[2:] or [""]
 a = make_matrix(WORKLOADS[name])
 x = torch.as_tensor(bench_x(a.n)).cuda()
