@@ -129,6 +129,8 @@ __global__ void k_col_exec(const int4* __restrict__ col, int64_t len4, const uin
 
 __global__ void k_xhot_fill(const double* __restrict__ x, const int32_t* __restrict__ hot, int64_t H,
                             double* __restrict__ xh) {
+  // the tile kernel may launch now: it waits for this grid before it reads xh
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint64_t pol = policy_evict_last();
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < H; i += step)

@@ -123,6 +123,7 @@ struct SpmvArgs {
   const double* xh;
   int32_t cold_pol;        // cold gathers: 0 evict_first, 1 evict_normal, 2 evict_last
   int32_t hot_l1;          // hot gathers allocate in L1
+  int32_t pdl;             // launched as a programmatic dependent of k_xhot_fill
 };
 
 struct Pipeline;  // pipeline.cu: host-vector copy/compute pipeline

@@ -315,6 +315,14 @@ int scratch_done(Handle* h, cudaStream_t stream) {
   return CSR5G_OK;
 }
 
+bool pdl_env() {  // CSR5G_PDL=0: launch the tile kernel after the fill completes (A/B)
+  static const bool on = [] {
+    const char* e = std::getenv("CSR5G_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_t stream,
                 cudaEvent_t ev0, cudaEvent_t ev1) {
   CSR5G_CUDA(cudaSetDevice(h->device));
@@ -412,7 +420,18 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = h->smem_bytes;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
+    int nattr = 0;
+    // staged plans: the tile kernel launches while k_xhot_fill drains
+    // (programmatic dependent launch) and waits for it only before its first
+    // gather (griddepcontrol.wait, spmv_kernel.cuh); the ring prologue and the
+    // rows part overlap the fill
+    if (a.xh && pdl_env()) {
+      attr[nattr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[nattr].val.programmaticStreamSerializationAllowed = 1;
+      ++nattr;
+      a.pdl = 1;
+    }
     if (x_window) {
       // keep x resident in an L2 persisting window (set-aside sized at build)
       int max_win = 0, max_persist = 0;
@@ -424,15 +443,18 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
         limit_set = true;
       }
       const size_t xb = std::min<size_t>((size_t)in.n * 8, (size_t)max_win);
-      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      attr[0].val.accessPolicyWindow.base_ptr = const_cast<double*>(d_x);
-      attr[0].val.accessPolicyWindow.num_bytes = xb;
-      attr[0].val.accessPolicyWindow.hitRatio =
+      attr[nattr].id = cudaLaunchAttributeAccessPolicyWindow;
+      attr[nattr].val.accessPolicyWindow.base_ptr = const_cast<double*>(d_x);
+      attr[nattr].val.accessPolicyWindow.num_bytes = xb;
+      attr[nattr].val.accessPolicyWindow.hitRatio =
           xb ? std::min(1.0f, (float)max_persist / (float)xb) : 1.0f;
-      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      attr[nattr].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr[nattr].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      ++nattr;
+    }
+    if (nattr) {
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = nattr;
     }
     const SpmvFn fn = spmv_fn(a.sigma, h->vr, h->nf, h->gm);
     if (int rc = func_attrs((const void*)fn, h->device, h->smem_bytes, h->carveout_pct)) return rc;

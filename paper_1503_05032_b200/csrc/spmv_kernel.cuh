@@ -497,6 +497,8 @@ __global__ void __launch_bounds__(spmv_threads_of(SIG, VR, NF, GM), 1)
       }
     };
     double xa[CH];
+    // staged plans: the staged values are complete from here on (k_xhot_fill)
+    if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     mbar_wait(bars, 0);
     gather(0, kb, xa);
 
