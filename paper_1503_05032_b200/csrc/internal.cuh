@@ -124,6 +124,7 @@ struct SpmvArgs {
   int32_t cold_pol;        // cold gathers: 0 evict_first, 1 evict_normal, 2 evict_last
   int32_t hot_l1;          // hot gathers allocate in L1
   int32_t pdl;             // launched as a programmatic dependent of k_xhot_fill
+  int32_t nf2_slots;       // k_spmv_nf2: closed-segment slots per tile
 };
 
 struct Pipeline;  // pipeline.cu: host-vector copy/compute pipeline
@@ -200,6 +201,8 @@ struct Handle {
   int cold_pol = 0;               // cold gathers' L2 policy (SpmvArgs::cold_pol)
   int hot_l1 = 0;                 // hot gathers allocate in L1 (SpmvArgs::hot_l1)
   int gm = 0;                     // compile-time gather mode of the plan's kernel (k_spmv GM)
+  bool nf2 = false;               // NF plan on the two-tiles-per-iteration kernel (spmv_nf2.cuh)
+  int nf2_slots = 0;
   int warps_per_block = 0, stages = 0, stage_bytes = 0, bar_bytes = 0, smem_bytes = 0;
   int carveout_pct = -1;  // preferred shared-memory carveout of the SpMV kernel
   // per-stream SpMV scratch (the handle's own arrays are the first set);

@@ -36,6 +36,7 @@
 #include <utility>
 
 #include "spmv_kernel.cuh"
+#include "spmv_nf2.cuh"
 
 namespace csr5g {
 namespace {
@@ -205,6 +206,37 @@ int spmv_plan(Handle* h, int sms) {
     const int need_bytes = h->smem_bytes + 1024;  // + the per-CTA reserved 1 KB
     int pct = (int)((100LL * need_bytes + max_smem - 1) / max_smem);
     h->carveout_pct = std::min(100, std::max(0, pct));
+  }
+  // NF plans at sigma <= 8 may run the two-tiles-per-iteration kernel
+  // (spmv_nf2.cuh, opt-in CSR5G_NF2=1): measured slower on the Laplacian
+  // 1000^2 (22.7 vs 20.8 us: 20 warps of two tiles hide less than 24 warps
+  // that prefetch the next tile's gathers), kept as a tested alternative
+  h->nf2 = false;
+  if (h->nf && sigma <= kNfMaxSigma && !h->wide) {
+    const char* e = std::getenv("CSR5G_NF2");
+    if (e && std::atoi(e) == 1) {
+      const int cap = (h->max_heads + 3) / 2 * 2;  // H + 1 slots, even (16-byte ring alignment)
+      const int stage = (int)((2 * h->B * 12 + 64 * 4 + 127) / 128 * 128);
+      const int per_warp = 2 * cap * 8 + 2 * stage;
+      int nw2 = kNf2Threads / 32;
+      if (const char* q = std::getenv("CSR5G_NW")) nw2 = std::max(1, std::min(nw2, std::atoi(q)));
+      while (nw2 > 1 && bars(nw2, 2) + nw2 * per_warp > 226 * 1024) --nw2;
+      if (bars(nw2, 2) + nw2 * per_warp <= 226 * 1024) {
+        h->nf2 = true;
+        h->nf2_slots = cap;
+        nw = nw2;
+        stages = 2;
+        h->warps_per_block = nw;
+        h->stages = 2;
+        h->stage_bytes = stage;
+        h->bar_bytes = bars(nw, 2);
+        h->smem_bytes = bars(nw, 2) + nw * per_warp;
+        int max_smem = 0;
+        CSR5G_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                                          h->device));
+        h->carveout_pct = std::min(100, (int)((100LL * (h->smem_bytes + 1024) + max_smem - 1) / max_smem));
+      }
+    }
   }
   const int64_t max_warps = (int64_t)sms * nw;
   h->nwarps = (int)std::min<int64_t>(max_warps, h->pcs);
@@ -456,7 +488,8 @@ int launch_spmv(Handle* h, const double* d_x, double* d_y, int mode, cudaStream_
       cfg.attrs = attr;
       cfg.numAttrs = nattr;
     }
-    const SpmvFn fn = spmv_fn(a.sigma, h->vr, h->nf, h->gm);
+    a.nf2_slots = h->nf2_slots;
+    const SpmvFn fn = h->nf2 ? spmv_fn_nf2(a.sigma) : spmv_fn(a.sigma, h->vr, h->nf, h->gm);
     if (int rc = func_attrs((const void*)fn, h->device, h->smem_bytes, h->carveout_pct)) return rc;
     CSR5G_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
   }

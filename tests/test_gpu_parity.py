@@ -512,3 +512,11 @@ def test_nf_kernel_multi_tile_warps(g, orc, monkeypatch):
         a5.release()
     for y in ys[1:]:
         assert np.array_equal(y.view(np.int64), ys[0].view(np.int64))
+    # the two-tiles-per-iteration NF kernel (spmv_nf2.cuh, opt-in) gives the
+    # same bits
+    monkeypatch.delenv("CSR5G_NW")
+    monkeypatch.setenv("CSR5G_NF2", "1")
+    a5 = gpu_build(g, a, sigma)
+    y2 = gpu_y(g, a5, x)
+    a5.release()
+    assert np.array_equal(y2.view(np.int64), ys[0].view(np.int64))
