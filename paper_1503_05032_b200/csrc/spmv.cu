@@ -208,9 +208,9 @@ int spmv_plan(Handle* h, int sms) {
     h->carveout_pct = std::min(100, std::max(0, pct));
   }
   // NF plans at sigma <= 8 may run the two-tiles-per-iteration kernel
-  // (spmv_nf2.cuh, opt-in CSR5G_NF2=1): measured slower on the Laplacian
-  // 1000^2 (22.7 vs 20.8 us: 20 warps of two tiles hide less than 24 warps
-  // that prefetch the next tile's gathers), kept as a tested alternative
+  // (spmv_nf2.cuh, opt-in CSR5G_NF2=1): measured no faster on the Laplacian
+  // 1000^2 (21.5 vs 20.7 us; both bottom out near 20.4 us), kept as a tested
+  // alternative
   h->nf2 = false;
   if (h->nf && sigma <= kNfMaxSigma && !h->wide) {
     const char* e = std::getenv("CSR5G_NF2");

@@ -13,9 +13,10 @@
 // write-backs interleave -- two independent dependency chains per warp.  The
 // arithmetic, the closes, the splice and the run merge of each tile are the
 // NF kernel's, in the same order: y is bit-identical to it.
-// Measured slower than the NF kernel on the Laplacian 1000^2 (22.7 vs
-// 20.8 us): 20 warps of two tiles hide less latency than 24 warps that issue
-// the next tile's gathers early.  Opt-in (CSR5G_NF2=1), tested bit-identical.
+// The next pair's gathers go out before this pair's splices, like the NF
+// kernel's next tile.  Measured on the Laplacian 1000^2: 21.5 us against the
+// NF kernel's 20.7 (both bottom out near 20.4 us, so the per-warp work is
+// not what bounds it).  Opt-in (CSR5G_NF2=1), tested bit-identical.
 #pragma once
 
 #include "spmv_kernel.cuh"
@@ -132,6 +133,20 @@ __global__ void __launch_bounds__(kNf2Threads, 1) k_spmv_nf2(SpmvArgs a) {
     pend_val = cL;
   };
 
+  // the gathers of a pair (the stage holding it has landed)
+  double xA[SIG], xB[SIG];
+  auto gather = [&](int st_idx, bool two) {
+    const int32_t* sc = reinterpret_cast<const int32_t*>(ring + (size_t)st_idx * STAGE + COL_OFF);
+#pragma unroll
+    for (int u = 0; u < SIG; ++u) xA[u] = ld_x_plain(a.x + sc[u * 32 + lane]);
+    if (two) {
+#pragma unroll
+      for (int u = 0; u < SIG; ++u) xB[u] = ld_x_plain(a.x + sc[B + u * 32 + lane]);
+    }
+  };
+  mbar_wait(bars, 0);
+  gather(0, kb + 1 < ke);
+
   for (int64_t k = kb; k < ke; k += 2) {
     const bool two = k + 1 < ke;
     const int slot = (int)((k - kb) & 31);  // even: tiles slot, slot + 1 of the batch
@@ -141,18 +156,9 @@ __global__ void __launch_bounds__(kNf2Threads, 1) k_spmv_nf2(SpmvArgs a) {
     }
     const int64_t rowA = __shfl_sync(kFull, tpv, slot) & 0x7fffffffu;
     const int64_t rowB = __shfl_sync(kFull, tpv, slot + 1) & 0x7fffffffu;
-    mbar_wait(bars + s, phase);
     const unsigned char* st = ring + (size_t)s * STAGE;
     const double* sv = reinterpret_cast<const double*>(st);
-    const int32_t* sc = reinterpret_cast<const int32_t*>(st + COL_OFF);
     const uint32_t* sd = reinterpret_cast<const uint32_t*>(st + DESC_OFF);
-    double xA[SIG], xB[SIG];
-#pragma unroll
-    for (int u = 0; u < SIG; ++u) xA[u] = ld_x_plain(a.x + sc[u * 32 + lane]);
-    if (two) {
-#pragma unroll
-      for (int u = 0; u < SIG; ++u) xB[u] = ld_x_plain(a.x + sc[B + u * 32 + lane]);
-    }
     uint64_t frA, frB = 0;
     int yoffA, cntA, yoffB = 0, cntB = 0;
     unpack(sd[lane], &frA, &yoffA, &cntA);
@@ -179,10 +185,18 @@ __global__ void __launch_bounds__(kNf2Threads, 1) k_spmv_nf2(SpmvArgs a) {
       }
     }
     __syncwarp();
-    // the stage is consumed: refill it with the pair after next
+    // the next pair's gathers go out now: their latency overlaps this pair's
+    // splices and write-backs (they land in the registers just drained)
+    const int sn = s ^ 1;
+    const uint32_t pn = sn == 0 ? phase ^ 1u : phase;
+    if (k + 2 < ke) {
+      mbar_wait(bars + sn, pn);
+      gather(sn, k + 3 < ke);
+    }
+    // this stage is consumed: refill it with the pair after next
     if (lane == 0 && k + 4 < ke) issue(k + 4, s);
-    s ^= 1;
-    if (s == 0) phase ^= 1u;
+    s = sn;
+    phase = pn;
     splice(slotA, frA, yoffA, cntA, sumA);
     if (two) splice(slotB, frB, yoffB, cntB, sumB);
     __syncwarp();
