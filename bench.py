@@ -24,8 +24,10 @@ ranks of CUDA-event time on the launching stream.  L2 is flushed between timed
 calls (2x L2 read outside the events).  `e2e` is the same metric through
 the host-buffer call (csr5.spmv_host_batch): per step pinned x H2D + SpMV + y
 D2H, pipelined across steps on separate copy engines.  The roofline
-figure is for the dominant tile kernel alone (events around it), with the
-algorithmic bytes of SURVEY 8(d).
+figure is for the SpMV's kernels (events around the hot-x staging, when the
+plan has one, and the tile kernel), with the algorithmic bytes of SURVEY
+8(d); `traffic` is the ncu-measured DRAM bytes of one tile-kernel launch
+(profiles/ncu_traffic.json).
 """
 from __future__ import annotations
 
